@@ -1,0 +1,152 @@
+/*
+ * skv_b200.h -- C ABI of the B200 (sm_100a) SWA decode hot path.
+ *
+ * Drop-in boundary for the reference's header-only C++ library `skv`
+ * (/root/reference/proj/include/skv, consumed through the CMake INTERFACE
+ * target at proj/CMakeLists.txt:10-14). Each entry point names the reference
+ * function it replaces. Plain pointers and sizes only; `stream` is a
+ * cudaStream_t passed as void* (NULL = legacy default stream).
+ *
+ * Errors: every call returns skv_status; the codes map 1:1 onto the
+ * reference exception classes (common.hpp:12-34) and skv_last_error()
+ * returns the message of the calling thread's last failure.
+ *
+ * Threading: like AttentionState a cache handle has one
+ * owner; calls on distinct handles are independent. One handle lives on one
+ * device.
+ */
+#ifndef SKV_B200_H
+#define SKV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum skv_status {
+    SKV_OK = 0,
+    SKV_ERR_CONTRACT = 1,    /* skv::ContractViolation   (common.hpp:12) */
+    SKV_ERR_OOM = 2,         /* skv::OutOfDeviceMemory   (common.hpp:17) */
+    SKV_ERR_INFEASIBLE = 3,  /* skv::InfeasiblePlan      (common.hpp:22) */
+    SKV_ERR_CUDA = 4,        /* CUDA runtime failure                      */
+    SKV_ERR_UNSUPPORTED = 5  /* shape/dtype outside the compiled kernels  */
+} skv_status;
+
+typedef enum skv_dtype {
+    SKV_F32 = 0,
+    SKV_F16 = 1,
+    SKV_BF16 = 2,
+    /* 8-bit affine codes, one (scale, bias) fp32 pair per (token, K|V, head):
+     * quant.hpp:43-95 applied per head_dim group as engine.hpp:469-483 does. */
+    SKV_U8 = 3
+} skv_dtype;
+
+typedef struct skv_cache skv_cache;
+
+typedef struct skv_cache_desc {
+    int32_t layers;    /* L */
+    int32_t batch;     /* B sequences (the reference has one; engine.hpp:289) */
+    int32_t heads;     /* H */
+    int32_t head_dim;  /* D (128) */
+    int32_t capacity;  /* tokens per sequence (Ncap) */
+    int32_t kv_dtype;  /* skv_dtype of stored K/V */
+    int32_t q_dtype;   /* compute dtype of q / new k,v / out: F32, F16, BF16 */
+    int32_t device;    /* CUDA ordinal */
+} skv_cache_desc;
+
+const char* skv_last_error(void);
+const char* skv_version(void);
+/* Kernels launched by this library since load (all entry points). */
+uint64_t skv_launch_count(void);
+
+/* attention.hpp:122-138. Return 0 (and set SKV_ERR_CONTRACT's message) for r
+ * outside (0, 1]. */
+size_t skv_swa_window_k(size_t n, double r);
+size_t skv_swa_keep_count(size_t n, double r);
+
+/* ---- cache: AttentionState (attention.hpp:45-86) for L layers x B sequences.
+ * Device layout: K/V [L][B][Ncap][2][H][D] (token-major), fp64 head-summed
+ * importance [L][B][Ncap] (attention.hpp:77-85 kept pre-reduced). */
+skv_status skv_cache_create(const skv_cache_desc* desc, skv_cache** out);
+skv_status skv_cache_destroy(skv_cache* cache);
+skv_status skv_cache_get_desc(const skv_cache* cache, skv_cache_desc* desc, uint64_t* device_bytes);
+
+/* AttentionState::append_token for tokens [t0, t0+nt) of sequences
+ * [b0, b0+nb) (attention.hpp:65-74; fake-quant as engine.hpp:469-483 when
+ * kv_dtype is SKV_U8). k, v: device [nb][nt][H][D] in q_dtype. Zeroes the
+ * importance of the written tokens (acc.resize(n, 0.0), attention.hpp:219). */
+skv_status skv_cache_write(skv_cache* cache, int layer, int b0, int nb, int t0, int nt,
+                           const void* k, const void* v, void* stream);
+/* Read back (dequantized) K/V as fp32 into device out [nb][nt][2][H][D]. */
+skv_status skv_cache_read(const skv_cache* cache, int layer, int b0, int nb, int t0, int nt,
+                          float* out, void* stream);
+/* Importance accumulator rows: device src/dst [nb][len] fp64. */
+skv_status skv_importance_set(skv_cache* cache, int layer, int b0, int nb, int len,
+                              const double* src, void* stream);
+skv_status skv_importance_get(const skv_cache* cache, int layer, int b0, int nb, int len,
+                              double* dst, void* stream);
+
+/* Prefill seeding (engine.hpp:508-512): attend the prompt's last query over
+ * all n cached tokens of every sequence and set importance[0, n) to the
+ * head-summed attention row. q_last, out: device [B][H][D] q_dtype. */
+skv_status skv_prefill_seed(skv_cache* cache, int layer, int n, const void* q_last, void* out,
+                            void* stream);
+
+/* ---- the hot path ---------------------------------------------------------
+ * One SWA decode step of one layer for all B sequences, in the engine's
+ * order (engine.hpp:592-629): append the new K/V as token n-1, select from
+ * the pre-step importance (swa_select, attention.hpp:142-171; dense when
+ * 2k >= n), attend over the selection (attend_over_indices,
+ * attention.hpp:183-231) and fold the weights into the importance.
+ * n counts the current token. q, k_new, v_new, out: device [B][H][D] q_dtype.
+ * idx_out (nullable): device int32 [B][m] ascending (SparseSelection::all);
+ * w_out (nullable): device fp32 [B][H][m] softmax weights in idx order.
+ * m = skv_swa_keep_count(n, r). One kernel launch. */
+skv_status skv_swa_decode_layer(skv_cache* cache, int layer, int n, double r, const void* q,
+                                const void* k_new, const void* v_new, void* out,
+                                int32_t* idx_out, float* w_out, void* stream);
+/* All L layers of one decode step (q/k/v/out device [L][B][H][D]); L launches. */
+skv_status skv_swa_decode_step(skv_cache* cache, int n, double r, const void* q,
+                               const void* k_new, const void* v_new, void* out, void* stream);
+/* Same with HOST buffers (pageable or pinned): copies q/k/v in, runs the
+ * step, copies out back, all on `stream`; returns after enqueueing
+ * (synchronize the stream before reading out_host). */
+skv_status skv_swa_decode_step_host(skv_cache* cache, int n, double r, const void* q_host,
+                                    const void* k_host, const void* v_host, void* out_host,
+                                    void* stream);
+
+/* attend_over_indices (attention.hpp:183-231) with caller-chosen ascending
+ * indices (device int32 [B][m], each < n); importance[idx] += w. */
+skv_status skv_attend_over_indices(skv_cache* cache, int layer, int n, const int32_t* idx,
+                                   int m, const void* q, void* out, float* w_out, void* stream);
+
+/* ---- standalone primitives on device buffers ----------------------------- */
+/* swa_select (attention.hpp:142-171) for `batch` rows of importance
+ * (row stride ld): writes SparseSelection::all() ascending to idx_out
+ * [batch][m]; *m_out = m (host). */
+skv_status skv_swa_select(const double* importance, int batch, int64_t ld, int n, double r,
+                          int32_t* idx_out, int32_t* m_out, void* stream);
+/* top_k_indices (matrix.hpp:162-176) per row: out [batch][k] ascending. */
+skv_status skv_top_k_indices(const double* v, int batch, int64_t ld, int len, int k,
+                             int32_t* out, void* stream);
+/* quantize / dequantize (quant.hpp:43-95), bit-exact fp64. */
+skv_status skv_quantize(const double* x, size_t len, uint32_t bits, size_t channel_size,
+                        uint16_t* codes, double* scales, int64_t* zero_points, void* stream);
+skv_status skv_dequantize(const uint16_t* codes, size_t len, size_t channel_size,
+                          const double* scales, const int64_t* zero_points, double* out,
+                          void* stream);
+
+/* ---- measurement hooks (bench.py) ----------------------------------------
+ * While enabled, every decode-kernel launch on a cache is bracketed by CUDA
+ * events on its own stream; skv_profile_read sums the measured durations. */
+skv_status skv_profile_enable(skv_cache* cache, int enable);
+skv_status skv_profile_read(skv_cache* cache, double* total_ms, int64_t* launches,
+                            uint64_t* algo_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SKV_B200_H */

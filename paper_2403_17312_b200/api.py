@@ -1,0 +1,260 @@
+"""Python view of the reference `skv` API for the SWA decode hot path.
+
+Same names, argument meaning and error classes as the reference C++
+functions (cited per function); every call goes through the C ABI in
+include/skv_b200.h into sm_100a kernels. torch tensors are only the device
+memory and stream plumbing. There is no CPU path: CPU tensors are rejected.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from ._lib import ContractViolation, check, lib
+
+SKV_F32, SKV_F16, SKV_BF16, SKV_U8 = 0, 1, 2, 3
+_DT = {torch.float32: SKV_F32, torch.float16: SKV_F16, torch.bfloat16: SKV_BF16, torch.uint8: SKV_U8}
+_TORCH = {v: k for k, v in _DT.items()}
+_NAMES = {"f32": SKV_F32, "fp32": SKV_F32, "f16": SKV_F16, "fp16": SKV_F16, "bf16": SKV_BF16,
+          "u8": SKV_U8, "int8": SKV_U8}
+
+
+def _code(dt) -> int:
+    if isinstance(dt, str):
+        return _NAMES[dt]
+    return _DT[dt]
+
+
+def _stream(t: torch.Tensor | None = None):
+    dev = t.device if t is not None else torch.device("cuda", torch.cuda.current_device())
+    return C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ContractViolation("device tensor required (no CPU path)")
+    if not t.is_contiguous():
+        raise ContractViolation("contiguous tensor required")
+    return C.c_void_p(t.data_ptr())
+
+
+# ---- attention.hpp:122-138 -------------------------------------------------
+def swa_window_k(n: int, r: float) -> int:
+    k = lib().skv_swa_window_k(n, r)
+    if k == 0:
+        raise ContractViolation(lib().skv_last_error().decode())
+    return k
+
+
+def swa_keep_count(n: int, r: float) -> int:
+    return min(2 * swa_window_k(n, r), n)
+
+
+# ---- matrix.hpp:162-176 ----------------------------------------------------
+def top_k_indices(v: torch.Tensor, k: int) -> torch.Tensor:
+    """k largest per row (ties -> lower index), ascending. v: fp64 [len] or [B, len]."""
+    v2 = v.reshape(1, -1) if v.dim() == 1 else v
+    if v2.dtype != torch.float64:
+        raise ContractViolation("top_k_indices: fp64 input required")
+    out = torch.empty((v2.shape[0], max(k, 1)), dtype=torch.int32, device=v2.device)
+    check(lib().skv_top_k_indices(_ptr(v2.contiguous()), v2.shape[0], v2.stride(0), v2.shape[1], k,
+                                  _ptr(out), _stream(v2)))
+    out = out[:, :k]
+    return out[0] if v.dim() == 1 else out
+
+
+# ---- attention.hpp:142-171 -------------------------------------------------
+@dataclass
+class SparseSelection:
+    """attention.hpp:26-39; `all` is SparseSelection::all() per row."""
+    all: torch.Tensor  # int32 [B, m] ascending
+    k: int
+
+
+def swa_select(importance: torch.Tensor, n: int, r: float) -> SparseSelection:
+    imp = importance.reshape(1, -1) if importance.dim() == 1 else importance
+    k = swa_window_k(n, r)
+    m = n if (n < 2 or 2 * k >= n) else 2 * k
+    if not (n < 2 or 2 * k >= n) and imp.shape[1] < n - 1:
+        raise ContractViolation("swa_select: importance length must be n-1")
+    out = torch.empty((imp.shape[0], max(m, 1)), dtype=torch.int32, device=imp.device)
+    mo = C.c_int32()
+    check(lib().skv_swa_select(_ptr(imp.contiguous()), imp.shape[0], imp.stride(0), n, r, _ptr(out),
+                               C.byref(mo), _stream(imp)))
+    out = out[:, :mo.value]
+    return SparseSelection(out[0] if importance.dim() == 1 else out, k)
+
+
+# ---- quant.hpp:43-95 -------------------------------------------------------
+def quantize(x: torch.Tensor, bits: int = 8, channel_size: int = 0):
+    """-> (codes uint16, scales fp64 [groups], zero_points int64 [groups])."""
+    if x.dtype != torch.float64:
+        raise ContractViolation("quantize: fp64 input required")
+    n = x.numel()
+    cs = channel_size or max(n, 1)
+    groups = max(n // cs, 1)
+    codes = torch.empty(max(n, 1), dtype=torch.uint16, device=x.device)
+    scales = torch.empty(groups, dtype=torch.float64, device=x.device)
+    zps = torch.empty(groups, dtype=torch.int64, device=x.device)
+    check(lib().skv_quantize(_ptr(x.contiguous()), n, bits, channel_size, _ptr(codes), _ptr(scales),
+                             _ptr(zps), _stream(x)))
+    return codes[:n], scales, zps
+
+
+def dequantize(codes: torch.Tensor, channel_size: int, scales: torch.Tensor, zps: torch.Tensor):
+    out = torch.empty(codes.numel(), dtype=torch.float64, device=codes.device)
+    check(lib().skv_dequantize(_ptr(codes), codes.numel(), channel_size, _ptr(scales), _ptr(zps),
+                               _ptr(out), _stream(codes)))
+    return out
+
+
+def quantize_roundtrip(x: torch.Tensor, bits: int, channel_size: int) -> torch.Tensor:
+    """quant.hpp:98-101"""
+    codes, scales, zps = quantize(x, bits, channel_size)
+    return dequantize(codes, channel_size or x.numel(), scales, zps)
+
+
+# ---- AttentionState x L layers x B sequences ---------------------------------
+class _Desc(C.Structure):
+    _fields_ = [("layers", C.c_int32), ("batch", C.c_int32), ("heads", C.c_int32),
+                ("head_dim", C.c_int32), ("capacity", C.c_int32), ("kv_dtype", C.c_int32),
+                ("q_dtype", C.c_int32), ("device", C.c_int32)]
+
+
+class SwaCache:
+    """Device-resident decode state: the reference's AttentionState
+    (attention.hpp:45-86) for `layers` x `batch` sequences, K/V token-major in
+    HBM, fp64 head-summed importance accumulator."""
+
+    def __init__(self, layers: int, batch: int, heads: int, head_dim: int, capacity: int,
+                 kv_dtype="f16", q_dtype=None, device: int | None = None):
+        self.layers, self.batch, self.heads, self.head_dim, self.capacity = (
+            layers, batch, heads, head_dim, capacity)
+        self.kv_code = _code(kv_dtype)
+        self.q_code = _code(q_dtype) if q_dtype is not None else (
+            SKV_F16 if self.kv_code == SKV_U8 else self.kv_code)
+        self.q_dtype = _TORCH[self.q_code]
+        self.device = torch.cuda.current_device() if device is None else device
+        self.dev = torch.device("cuda", self.device)
+        d = _Desc(layers, batch, heads, head_dim, capacity, self.kv_code, self.q_code, self.device)
+        h = C.c_void_p()
+        check(lib().skv_cache_create(C.byref(d), C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().skv_cache_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def device_bytes(self) -> int:
+        b = C.c_uint64()
+        check(lib().skv_cache_get_desc(self._h, None, C.byref(b)))
+        return b.value
+
+    def _q(self, t: torch.Tensor, shape) -> torch.Tensor:
+        if t.dtype != self.q_dtype or tuple(t.shape) != tuple(shape):
+            raise ContractViolation(f"expected {self.q_dtype} {tuple(shape)}, got {t.dtype} {tuple(t.shape)}")
+        return t
+
+    # AttentionState::append_token over a block of tokens (attention.hpp:65-74)
+    def append_tokens(self, layer: int, b0: int, t0: int, k: torch.Tensor, v: torch.Tensor):
+        nb, nt = k.shape[0], k.shape[1]
+        shp = (nb, nt, self.heads, self.head_dim)
+        check(lib().skv_cache_write(self._h, layer, b0, nb, t0, nt, _ptr(self._q(k, shp)),
+                                    _ptr(self._q(v, shp)), _stream(k)))
+
+    def read(self, layer: int, b0: int, nb: int, t0: int, nt: int) -> torch.Tensor:
+        out = torch.empty((nb, nt, 2, self.heads, self.head_dim), dtype=torch.float32, device=self.dev)
+        check(lib().skv_cache_read(self._h, layer, b0, nb, t0, nt, _ptr(out), _stream(out)))
+        return out
+
+    def set_importance(self, layer: int, imp: torch.Tensor, b0: int = 0):
+        imp = imp.to(torch.float64).contiguous()
+        check(lib().skv_importance_set(self._h, layer, b0, imp.shape[0], imp.shape[1], _ptr(imp),
+                                       _stream(imp)))
+
+    def importance(self, layer: int, length: int, b0: int = 0, nb: int | None = None) -> torch.Tensor:
+        nb = self.batch - b0 if nb is None else nb
+        out = torch.empty((nb, length), dtype=torch.float64, device=self.dev)
+        check(lib().skv_importance_get(self._h, layer, b0, nb, length, _ptr(out), _stream(out)))
+        return out
+
+    # Engine::prefill accumulator seeding (engine.hpp:508-512)
+    def prefill_seed(self, layer: int, n: int, q_last: torch.Tensor) -> torch.Tensor:
+        out = torch.empty_like(self._q(q_last, (self.batch, self.heads, self.head_dim)))
+        check(lib().skv_prefill_seed(self._h, layer, n, _ptr(q_last), _ptr(out), _stream(q_last)))
+        return out
+
+    # One decode step of one layer (engine.hpp:592-629 order; swa_attention)
+    def swa_decode_layer(self, layer: int, n: int, r: float, q, k_new, v_new, out=None,
+                         return_indices: bool = False, return_weights: bool = False):
+        shp = (self.batch, self.heads, self.head_dim)
+        for t in (q, k_new, v_new):
+            self._q(t, shp)
+        out = torch.empty_like(q) if out is None else out
+        m = swa_keep_count(n, r)
+        idx = torch.empty((self.batch, m), dtype=torch.int32, device=self.dev) if return_indices else None
+        w = (torch.empty((self.batch, self.heads, m), dtype=torch.float32, device=self.dev)
+             if return_weights else None)
+        check(lib().skv_swa_decode_layer(self._h, layer, n, r, _ptr(q), _ptr(k_new), _ptr(v_new),
+                                         _ptr(out), _ptr(idx), _ptr(w), _stream(q)))
+        return out, idx, w
+
+    def swa_decode_step(self, n: int, r: float, q, k_new, v_new, out=None):
+        shp = (self.layers, self.batch, self.heads, self.head_dim)
+        for t in (q, k_new, v_new):
+            self._q(t, shp)
+        out = torch.empty_like(q) if out is None else out
+        check(lib().skv_swa_decode_step(self._h, n, r, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(out),
+                                        _stream(q)))
+        return out
+
+    def swa_decode_step_host(self, n: int, r: float, q, k_new, v_new, out):
+        """Host (CPU, ideally pinned) tensors in and out; enqueued on the
+        current stream of this cache's device."""
+        for t in (q, k_new, v_new, out):
+            if t.is_cuda or not t.is_contiguous():
+                raise ContractViolation("host contiguous tensors required")
+        s = C.c_void_p(torch.cuda.current_stream(self.dev).cuda_stream)
+        check(lib().skv_swa_decode_step_host(self._h, n, r, C.c_void_p(q.data_ptr()),
+                                             C.c_void_p(k_new.data_ptr()), C.c_void_p(v_new.data_ptr()),
+                                             C.c_void_p(out.data_ptr()), s))
+        return out
+
+    # attend_over_indices (attention.hpp:183-231)
+    def attend_over_indices(self, layer: int, n: int, idx: torch.Tensor, q: torch.Tensor,
+                            return_weights: bool = False):
+        idx = idx.to(torch.int32).contiguous()
+        if idx.dim() == 1:
+            idx = idx.reshape(1, -1).expand(self.batch, -1).contiguous()
+        m = idx.shape[1]
+        out = torch.empty_like(self._q(q, (self.batch, self.heads, self.head_dim)))
+        w = (torch.empty((self.batch, self.heads, m), dtype=torch.float32, device=self.dev)
+             if return_weights else None)
+        check(lib().skv_attend_over_indices(self._h, layer, n, _ptr(idx), m, _ptr(q), _ptr(out), _ptr(w),
+                                            _stream(q)))
+        return out, w
+
+    # measurement hooks
+    def profile(self, enable: bool):
+        check(lib().skv_profile_enable(self._h, int(enable)))
+
+    def profile_read(self):
+        ms, n, b = C.c_double(), C.c_int64(), C.c_uint64()
+        check(lib().skv_profile_read(self._h, C.byref(ms), C.byref(n), C.byref(b)))
+        return ms.value, n.value, b.value
+
+
+def launch_count() -> int:
+    return lib().skv_launch_count()

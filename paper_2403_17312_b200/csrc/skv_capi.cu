@@ -1,0 +1,574 @@
+// skv_capi.cu -- the C ABI (include/skv_b200.h): argument checking with the
+// reference's error semantics, the device cache object, kernel selection and
+// launch, host-buffer step, and the measurement hooks used by bench.py.
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "skv_internal.h"
+
+namespace skv_impl {
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace skv_impl
+
+using namespace skv_impl;
+
+namespace {
+
+thread_local std::string g_err;
+
+skv_status fail(skv_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+#define SKV_CUDA(expr)                                                                   \
+    do {                                                                                 \
+        const cudaError_t e_ = (expr);                                                   \
+        if (e_ != cudaSuccess) return fail(SKV_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+    } while (0)
+
+#define SKV_REQUIRE(cond, msg)                                \
+    do {                                                      \
+        if (!(cond)) return fail(SKV_ERR_CONTRACT, "%s", msg); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+size_t dtype_size(int dt) {
+    switch (dt) {
+    case SKV_F32: return 4;
+    case SKV_F16: return 2;
+    case SKV_BF16: return 2;
+    case SKV_U8: return 1;
+    }
+    return 0;
+}
+
+// common.hpp:43-54 semantics: floor-based half-to-even, FP-env independent.
+long long round_half_even_host(double x) {
+    const double f = std::floor(x);
+    const double frac = x - f;
+    const long long lo = static_cast<long long>(f);
+    if (frac > 0.5) return lo + 1;
+    if (frac < 0.5) return lo;
+    return (lo % 2 == 0) ? lo : lo + 1;
+}
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+struct skv_cache {
+    skv_cache_desc d{};
+    size_t row_bytes = 0;    // one head row of D elements (storage dtype)
+    size_t tok_bytes = 0;    // K+V of one token, all heads
+    size_t layer_bytes = 0;  // [B][Ncap] tokens
+    uint8_t* kv = nullptr;
+    float2* meta = nullptr;
+    double* imp = nullptr;
+    float* wpart = nullptr;
+    unsigned* counters = nullptr;
+    uint64_t device_bytes = 0;
+    int num_sms = 0;
+    int max_smem = 0;
+    // host-buffer step staging
+    uint8_t* stage = nullptr;
+    size_t stage_bytes = 0;
+    // measurement
+    bool prof = false;
+    std::vector<cudaEvent_t> ev;  // start/stop pairs
+    std::vector<cudaEvent_t> ev_pool;
+    int64_t prof_launches = 0;
+    uint64_t prof_bytes = 0;
+};
+
+extern "C" {
+
+const char* skv_last_error(void) { return g_err.c_str(); }
+
+const char* skv_version(void) { return "skv_b200 0.1 sm_100a"; }
+
+uint64_t skv_launch_count(void) { return g_launches.load(); }
+
+// attention.hpp:122-132
+size_t skv_swa_window_k(size_t n, double r) {
+    if (!(r > 0.0 && r <= 1.0)) {
+        fail(SKV_ERR_CONTRACT, "swa_window_k: ratio out of (0,1]");
+        return 0;
+    }
+    if (n < 2) return 1;
+    if (r >= 1.0) return (n + 1) / 2;
+    const long long rounded = round_half_even_host(static_cast<double>(n) * r / 2.0);
+    return rounded < 1 ? 1 : static_cast<size_t>(rounded);
+}
+
+// attention.hpp:136-138
+size_t skv_swa_keep_count(size_t n, double r) {
+    const size_t k = skv_swa_window_k(n, r);
+    if (k == 0) return 0;
+    return 2 * k < n ? 2 * k : n;
+}
+
+skv_status skv_cache_create(const skv_cache_desc* desc, skv_cache** out) {
+    SKV_REQUIRE(desc != nullptr && out != nullptr, "skv_cache_create: null argument");
+    const skv_cache_desc& d = *desc;
+    SKV_REQUIRE(d.layers > 0 && d.batch > 0 && d.heads > 0 && d.capacity > 0,
+                "skv_cache_create: zero dimension");
+    if (d.head_dim != skvd::kHeadDim)
+        return fail(SKV_ERR_UNSUPPORTED, "skv_cache_create: head_dim %d (compiled for %d)", d.head_dim,
+                    skvd::kHeadDim);
+    const bool ok_pair = (d.kv_dtype == d.q_dtype && d.kv_dtype != SKV_U8) ||
+                         (d.kv_dtype == SKV_U8 && d.q_dtype != SKV_U8 && dtype_size(d.q_dtype) > 0);
+    if (!ok_pair || dtype_size(d.kv_dtype) == 0)
+        return fail(SKV_ERR_UNSUPPORTED, "skv_cache_create: kv_dtype %d with q_dtype %d", d.kv_dtype,
+                    d.q_dtype);
+    DeviceGuard guard(d.device);
+    skv_cache* c = new skv_cache();
+    c->d = d;
+    c->row_bytes = static_cast<size_t>(d.head_dim) * dtype_size(d.kv_dtype);
+    c->tok_bytes = 2 * static_cast<size_t>(d.heads) * c->row_bytes;
+    c->layer_bytes = static_cast<size_t>(d.batch) * d.capacity * c->tok_bytes;
+    const size_t kv_bytes = c->layer_bytes * d.layers;
+    const size_t meta_bytes =
+        d.kv_dtype == SKV_U8 ? static_cast<size_t>(d.layers) * d.batch * d.capacity * 2 * d.heads * 8 : 0;
+    const size_t imp_bytes = static_cast<size_t>(d.layers) * d.batch * d.capacity * 8;
+    const size_t wpart_bytes = static_cast<size_t>(d.batch) * d.heads * d.capacity * 4;
+    const size_t cnt_bytes = static_cast<size_t>(d.layers) * d.batch * 4;
+    auto alloc = [&](void** p, size_t bytes) -> bool {
+        if (bytes == 0) return true;
+        if (cudaMalloc(p, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        c->device_bytes += bytes;
+        return true;
+    };
+    if (!alloc(reinterpret_cast<void**>(&c->kv), kv_bytes) ||
+        !alloc(reinterpret_cast<void**>(&c->meta), meta_bytes) ||
+        !alloc(reinterpret_cast<void**>(&c->imp), imp_bytes) ||
+        !alloc(reinterpret_cast<void**>(&c->wpart), wpart_bytes) ||
+        !alloc(reinterpret_cast<void**>(&c->counters), cnt_bytes)) {
+        const uint64_t want = kv_bytes + meta_bytes + imp_bytes + wpart_bytes + cnt_bytes;
+        skv_cache_destroy(c);
+        return fail(SKV_ERR_OOM, "skv_cache_create: cannot allocate %llu device bytes",
+                    static_cast<unsigned long long>(want));
+    }
+    SKV_CUDA(cudaMemset(c->imp, 0, imp_bytes));
+    SKV_CUDA(cudaMemset(c->counters, 0, cnt_bytes));
+    if (meta_bytes) SKV_CUDA(cudaMemset(c->meta, 0, meta_bytes));
+    SKV_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, d.device));
+    SKV_CUDA(cudaDeviceGetAttribute(&c->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, d.device));
+    *out = c;
+    return SKV_OK;
+}
+
+skv_status skv_cache_destroy(skv_cache* c) {
+    if (c == nullptr) return SKV_OK;
+    DeviceGuard guard(c->d.device);
+    cudaFree(c->kv);
+    cudaFree(c->meta);
+    cudaFree(c->imp);
+    cudaFree(c->wpart);
+    cudaFree(c->counters);
+    cudaFree(c->stage);
+    for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    delete c;
+    return SKV_OK;
+}
+
+skv_status skv_cache_get_desc(const skv_cache* c, skv_cache_desc* desc, uint64_t* device_bytes) {
+    SKV_REQUIRE(c != nullptr, "skv_cache_get_desc: null cache");
+    if (desc) *desc = c->d;
+    if (device_bytes) *device_bytes = c->device_bytes;
+    return SKV_OK;
+}
+
+static skv_status check_block(const skv_cache* c, int layer, int b0, int nb, int t0, int nt) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    SKV_REQUIRE(layer >= 0 && layer < c->d.layers, "KvLedger: layer out of range");
+    SKV_REQUIRE(b0 >= 0 && nb > 0 && b0 + nb <= c->d.batch, "batch range out of bounds");
+    SKV_REQUIRE(t0 >= 0 && nt > 0 && t0 + nt <= c->d.capacity, "token range exceeds cache capacity");
+    return SKV_OK;
+}
+
+skv_status skv_cache_write(skv_cache* c, int layer, int b0, int nb, int t0, int nt, const void* k,
+                           const void* v, void* stream) {
+    if (skv_status s = check_block(c, layer, b0, nb, t0, nt)) return s;
+    SKV_REQUIRE(k != nullptr && v != nullptr, "append_token: null rows");
+    DeviceGuard guard(c->d.device);
+    const size_t lt = static_cast<size_t>(layer) * c->d.batch * c->d.capacity;
+    SKV_CUDA(launch_cache_write(c->d.kv_dtype, c->d.q_dtype, c->kv + layer * c->layer_bytes,
+                                c->meta ? c->meta + lt * 2 * c->d.heads : nullptr, c->imp + lt, k, v,
+                                c->d.heads, c->d.capacity, b0, nb, t0, nt, as_stream(stream)));
+    return SKV_OK;
+}
+
+skv_status skv_cache_read(const skv_cache* c, int layer, int b0, int nb, int t0, int nt, float* out,
+                          void* stream) {
+    if (skv_status s = check_block(c, layer, b0, nb, t0, nt)) return s;
+    SKV_REQUIRE(out != nullptr, "skv_cache_read: null output");
+    DeviceGuard guard(c->d.device);
+    const size_t lt = static_cast<size_t>(layer) * c->d.batch * c->d.capacity;
+    SKV_CUDA(launch_cache_read(c->d.kv_dtype, c->kv + layer * c->layer_bytes,
+                               c->meta ? c->meta + lt * 2 * c->d.heads : nullptr, out, c->d.heads,
+                               c->d.capacity, b0, nb, t0, nt, as_stream(stream)));
+    return SKV_OK;
+}
+
+skv_status skv_importance_set(skv_cache* c, int layer, int b0, int nb, int len, const double* src,
+                              void* stream) {
+    if (skv_status s = check_block(c, layer, b0, nb, 0, len)) return s;
+    DeviceGuard guard(c->d.device);
+    double* dst = c->imp + (static_cast<size_t>(layer) * c->d.batch + b0) * c->d.capacity;
+    SKV_CUDA(cudaMemcpy2DAsync(dst, c->d.capacity * 8, src, static_cast<size_t>(len) * 8,
+                               static_cast<size_t>(len) * 8, nb, cudaMemcpyDefault, as_stream(stream)));
+    return SKV_OK;
+}
+
+skv_status skv_importance_get(const skv_cache* c, int layer, int b0, int nb, int len, double* dst,
+                              void* stream) {
+    if (skv_status s = check_block(c, layer, b0, nb, 0, len)) return s;
+    DeviceGuard guard(c->d.device);
+    const double* src = c->imp + (static_cast<size_t>(layer) * c->d.batch + b0) * c->d.capacity;
+    SKV_CUDA(cudaMemcpy2DAsync(dst, static_cast<size_t>(len) * 8, src, c->d.capacity * 8,
+                               static_cast<size_t>(len) * 8, nb, cudaMemcpyDefault, as_stream(stream)));
+    return SKV_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Pick heads-per-CTA: the smallest head group whose grid still fits in one
+// wave of resident CTAs (all CTAs stream concurrently and finish together);
+// otherwise the largest available group. SKV_HG overrides (tuning).
+skv_status pick_decode(skv_cache* c, int m, int nc, const DecodeLaunch** dl_out, size_t* smem_out) {
+    static const int env_hg = [] {
+        const char* s = std::getenv("SKV_HG");
+        return s ? std::atoi(s) : 0;
+    }();
+    const int cands[4] = {1, 2, 4, 8};
+    const DecodeLaunch* best = nullptr;
+    size_t best_smem = 0;
+    for (int hg : cands) {
+        if (c->d.heads % hg != 0) continue;
+        if (env_hg && hg != env_hg) continue;
+        const DecodeLaunch* dl = find_decode(c->d.kv_dtype, c->d.q_dtype, hg);
+        if (!dl) continue;
+        const size_t smem = dl->smem(m, nc);
+        if (smem > static_cast<size_t>(c->max_smem)) continue;
+        best = dl;
+        best_smem = smem;
+        SKV_CUDA(cudaFuncSetAttribute(dl->func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        int occ = 0;
+        SKV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dl->func, skvd::kDecodeThreads, smem));
+        const long long ctas = static_cast<long long>(c->d.batch) * (c->d.heads / hg);
+        if (occ > 0 && ctas <= static_cast<long long>(occ) * c->num_sms) break;
+    }
+    if (!best)
+        return fail(SKV_ERR_UNSUPPORTED, "no decode kernel fits (heads %d, m %d, shared memory %d)",
+                    c->d.heads, m, c->max_smem);
+    *dl_out = best;
+    *smem_out = best_smem;
+    return SKV_OK;
+}
+
+uint64_t algo_bytes(const skv_cache* c, int n, int m, int nc, bool append) {
+    const uint64_t H = c->d.heads, D = c->d.head_dim;
+    const uint64_t eq = dtype_size(c->d.q_dtype), ekv = dtype_size(c->d.kv_dtype);
+    const uint64_t meta = c->d.kv_dtype == SKV_U8 ? 8 : 0;
+    const uint64_t row = D * ekv + meta;  // one head row as stored
+    uint64_t per = H * D * eq * 2;        // q in, out
+    uint64_t gathered = static_cast<uint64_t>(m);
+    if (append) {
+        per += 2 * H * D * eq + 2 * H * row;  // new k,v in; stored rows out
+        gathered -= 1;                        // the new token is not re-read
+    }
+    per += static_cast<uint64_t>(nc) * 8;            // importance candidates
+    per += 2 * gathered * H * row;                   // K and V gather
+    per += static_cast<uint64_t>(m) * 16;            // importance read-modify-write
+    (void)n;
+    return per * static_cast<uint64_t>(c->d.batch);
+}
+
+skv_status run_decode(skv_cache* c, int layer, int n, int k, int m, int nc, int mode, bool append,
+                      bool dense, const void* q, const void* k_new, const void* v_new, void* out,
+                      const int32_t* idx_in, int32_t* idx_out, float* w_out, cudaStream_t st) {
+    const DecodeLaunch* dl = nullptr;
+    size_t smem = 0;
+    if (skv_status s = pick_decode(c, m, nc, &dl, &smem)) return s;
+    const size_t lt = static_cast<size_t>(layer) * c->d.batch * c->d.capacity;
+    skvd::DecodeParams p{};
+    p.kv = c->kv + layer * c->layer_bytes;
+    p.kv_w = c->kv + layer * c->layer_bytes;
+    p.meta = c->meta ? c->meta + lt * 2 * c->d.heads : nullptr;
+    p.meta_w = const_cast<float2*>(p.meta);
+    p.imp = c->imp + lt;
+    p.q = q;
+    p.k_new = k_new;
+    p.v_new = v_new;
+    p.out = out;
+    p.idx_in = idx_in;
+    p.idx_out = idx_out;
+    p.w_out = w_out;
+    p.wpart = c->wpart;
+    p.counters = c->counters + static_cast<size_t>(layer) * c->d.batch;
+    p.B = c->d.batch;
+    p.H = c->d.heads;
+    p.Ncap = c->d.capacity;
+    p.n = n;
+    p.k = k;
+    p.m = m;
+    p.mode = mode;
+    p.append = append ? 1 : 0;
+    p.dense = dense ? 1 : 0;
+    p.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d.head_dim)));
+    const int grid_g = c->d.heads / dl->hg;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->prof) {
+        auto take = [&]() {
+            cudaEvent_t e;
+            if (!c->ev_pool.empty()) {
+                e = c->ev_pool.back();
+                c->ev_pool.pop_back();
+            } else {
+                cudaEventCreate(&e);
+            }
+            return e;
+        };
+        e0 = take();
+        e1 = take();
+        SKV_CUDA(cudaEventRecord(e0, st));
+    }
+    SKV_CUDA(launch_decode(*dl, p, grid_g, smem, st));
+    if (c->prof) {
+        SKV_CUDA(cudaEventRecord(e1, st));
+        c->ev.push_back(e0);
+        c->ev.push_back(e1);
+        c->prof_launches += 1;
+        c->prof_bytes += algo_bytes(c, n, m, nc, append);
+    }
+    return SKV_OK;
+}
+
+struct StepShape {
+    int k, m, nc;
+    bool dense;
+};
+
+skv_status step_shape(const skv_cache* c, int n, double r, StepShape* s) {
+    SKV_REQUIRE(n >= 1, "swa_attention: empty cache");
+    SKV_REQUIRE(n <= c->d.capacity, "decode_step: context overflow");
+    const size_t k = skv_swa_window_k(static_cast<size_t>(n), r);
+    if (k == 0) return SKV_ERR_CONTRACT;
+    s->k = static_cast<int>(k);
+    s->dense = n < 2 || 2 * static_cast<int>(k) >= n;
+    s->m = s->dense ? n : 2 * s->k;
+    s->nc = s->dense ? 0 : n - s->k;
+    return SKV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+skv_status skv_prefill_seed(skv_cache* c, int layer, int n, const void* q_last, void* out, void* stream) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    SKV_REQUIRE(layer >= 0 && layer < c->d.layers, "KvLedger: layer out of range");
+    SKV_REQUIRE(n >= 1 && n <= c->d.capacity, "prefill: prompt length out of range");
+    SKV_REQUIRE(q_last != nullptr && out != nullptr, "prefill: null argument");
+    DeviceGuard guard(c->d.device);
+    return run_decode(c, layer, n, 1, n, 0, skvd::kModeSeed, false, true, q_last, nullptr, nullptr, out,
+                      nullptr, nullptr, nullptr, as_stream(stream));
+}
+
+skv_status skv_swa_decode_layer(skv_cache* c, int layer, int n, double r, const void* q, const void* k_new,
+                                const void* v_new, void* out, int32_t* idx_out, float* w_out, void* stream) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    SKV_REQUIRE(layer >= 0 && layer < c->d.layers, "KvLedger: layer out of range");
+    SKV_REQUIRE(q && k_new && v_new && out, "decode_step: null argument");
+    StepShape s;
+    if (skv_status st = step_shape(c, n, r, &s)) return st;
+    DeviceGuard guard(c->d.device);
+    return run_decode(c, layer, n, s.k, s.m, s.nc, skvd::kModeSwaStep, true, s.dense, q, k_new, v_new, out,
+                      nullptr, idx_out, w_out, as_stream(stream));
+}
+
+skv_status skv_swa_decode_step(skv_cache* c, int n, double r, const void* q, const void* k_new,
+                               const void* v_new, void* out, void* stream) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    SKV_REQUIRE(q && k_new && v_new && out, "decode_step: null argument");
+    StepShape s;
+    if (skv_status st = step_shape(c, n, r, &s)) return st;
+    DeviceGuard guard(c->d.device);
+    const size_t per_layer = static_cast<size_t>(c->d.batch) * c->d.heads * c->d.head_dim * dtype_size(c->d.q_dtype);
+    for (int l = 0; l < c->d.layers; ++l) {
+        const size_t o = per_layer * l;
+        if (skv_status st = run_decode(c, l, n, s.k, s.m, s.nc, skvd::kModeSwaStep, true, s.dense,
+                                       static_cast<const uint8_t*>(q) + o, static_cast<const uint8_t*>(k_new) + o,
+                                       static_cast<const uint8_t*>(v_new) + o, static_cast<uint8_t*>(out) + o,
+                                       nullptr, nullptr, nullptr, as_stream(stream)))
+            return st;
+    }
+    return SKV_OK;
+}
+
+skv_status skv_swa_decode_step_host(skv_cache* c, int n, double r, const void* q_host, const void* k_host,
+                                    const void* v_host, void* out_host, void* stream) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    SKV_REQUIRE(q_host && k_host && v_host && out_host, "decode_step: null argument");
+    DeviceGuard guard(c->d.device);
+    const size_t bytes = static_cast<size_t>(c->d.layers) * c->d.batch * c->d.heads * c->d.head_dim *
+                         dtype_size(c->d.q_dtype);
+    if (c->stage_bytes < 4 * bytes) {
+        cudaFree(c->stage);
+        c->stage = nullptr;
+        if (cudaMalloc(reinterpret_cast<void**>(&c->stage), 4 * bytes) != cudaSuccess) {
+            cudaGetLastError();
+            c->stage_bytes = 0;
+            return fail(SKV_ERR_OOM, "decode_step_host: cannot allocate staging");
+        }
+        c->stage_bytes = 4 * bytes;
+    }
+    const cudaStream_t st = as_stream(stream);
+    uint8_t *dq = c->stage, *dk = dq + bytes, *dv = dk + bytes, *dout = dv + bytes;
+    SKV_CUDA(cudaMemcpyAsync(dq, q_host, bytes, cudaMemcpyHostToDevice, st));
+    SKV_CUDA(cudaMemcpyAsync(dk, k_host, bytes, cudaMemcpyHostToDevice, st));
+    SKV_CUDA(cudaMemcpyAsync(dv, v_host, bytes, cudaMemcpyHostToDevice, st));
+    if (skv_status s = skv_swa_decode_step(c, n, r, dq, dk, dv, dout, stream)) return s;
+    SKV_CUDA(cudaMemcpyAsync(out_host, dout, bytes, cudaMemcpyDeviceToHost, st));
+    return SKV_OK;
+}
+
+skv_status skv_attend_over_indices(skv_cache* c, int layer, int n, const int32_t* idx, int m, const void* q,
+                                   void* out, float* w_out, void* stream) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    SKV_REQUIRE(layer >= 0 && layer < c->d.layers, "KvLedger: layer out of range");
+    SKV_REQUIRE(n >= 1 && n <= c->d.capacity, "attend_over_indices: empty cache");
+    SKV_REQUIRE(m >= 1, "attend_over_indices: empty selection");
+    SKV_REQUIRE(m <= n, "attend_over_indices: more indices than tokens");
+    SKV_REQUIRE(idx && q && out, "attend_over_indices: null argument");
+    DeviceGuard guard(c->d.device);
+    // The reference validates every index (attention.hpp:186-192); the fused
+    // kernel additionally needs them unique (ascending, as sel.all() gives).
+    std::vector<int32_t> h(static_cast<size_t>(c->d.batch) * m);
+    SKV_CUDA(cudaMemcpyAsync(h.data(), idx, h.size() * 4, cudaMemcpyDefault, as_stream(stream)));
+    SKV_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    for (int b = 0; b < c->d.batch; ++b)
+        for (int i = 0; i < m; ++i) {
+            const int32_t t = h[static_cast<size_t>(b) * m + i];
+            SKV_REQUIRE(t >= 0 && t < n, "attend_over_indices: index out of range");
+            SKV_REQUIRE(i == 0 || t > h[static_cast<size_t>(b) * m + i - 1],
+                        "attend_over_indices: indices must be strictly ascending");
+        }
+    return run_decode(c, layer, n, 1, m, 0, skvd::kModeExplicit, false, false, q, nullptr, nullptr, out, idx,
+                      nullptr, w_out, as_stream(stream));
+}
+
+skv_status skv_swa_select(const double* importance, int batch, int64_t ld, int n, double r, int32_t* idx_out,
+                          int32_t* m_out, void* stream) {
+    SKV_REQUIRE(batch >= 1, "swa_select: empty batch");
+    SKV_REQUIRE(idx_out != nullptr, "swa_select: null output");
+    const size_t k = skv_swa_window_k(static_cast<size_t>(n < 0 ? 0 : n), r);
+    if (k == 0) return SKV_ERR_CONTRACT;
+    SKV_REQUIRE(n >= 0, "swa_select: negative length");
+    const bool dense = n < 2 || 2 * static_cast<int>(k) >= n;
+    const int m = dense ? n : 2 * static_cast<int>(k);
+    if (m_out) *m_out = m;
+    if (m == 0) return SKV_OK;
+    if (!dense) {
+        SKV_REQUIRE(importance != nullptr, "swa_select: importance length must be n-1");
+        SKV_REQUIRE(ld >= n - 1, "swa_select: row stride shorter than n-1");
+        if (static_cast<size_t>(n - k) * 8 + 8192 > 220 * 1024)
+            return fail(SKV_ERR_UNSUPPORTED, "swa_select: %d candidates exceed shared memory", n - static_cast<int>(k));
+    }
+    SKV_CUDA(launch_swa_select(importance, batch, ld, n, static_cast<int>(k), m, dense, idx_out, as_stream(stream)));
+    return SKV_OK;
+}
+
+skv_status skv_top_k_indices(const double* v, int batch, int64_t ld, int len, int k, int32_t* out, void* stream) {
+    SKV_REQUIRE(k >= 0 && len >= 0 && k <= len, "top_k_indices: k exceeds length");
+    SKV_REQUIRE(batch >= 1 && ld >= len, "top_k_indices: bad batch layout");
+    if (k == 0) return SKV_OK;
+    SKV_REQUIRE(v != nullptr && out != nullptr, "top_k_indices: null argument");
+    if (static_cast<size_t>(len) * 8 + 8192 > 220 * 1024)
+        return fail(SKV_ERR_UNSUPPORTED, "top_k_indices: length %d exceeds shared memory", len);
+    SKV_CUDA(launch_top_k(v, batch, ld, len, k, out, as_stream(stream)));
+    return SKV_OK;
+}
+
+skv_status skv_quantize(const double* x, size_t len, uint32_t bits, size_t channel_size, uint16_t* codes,
+                        double* scales, int64_t* zero_points, void* stream) {
+    SKV_REQUIRE(len > 0, "quantize: empty input");
+    SKV_REQUIRE(bits == 4 || bits == 8, "quantize: bits must be 4 or 8");
+    if (channel_size == 0) channel_size = len;
+    SKV_REQUIRE(len % channel_size == 0, "quantize: channel_size must divide length");
+    SKV_REQUIRE(x && codes && scales && zero_points, "quantize: null argument");
+    SKV_CUDA(launch_quantize(x, static_cast<long long>(len), static_cast<long long>(channel_size), bits, codes,
+                             scales, reinterpret_cast<long long*>(zero_points), as_stream(stream)));
+    return SKV_OK;
+}
+
+skv_status skv_dequantize(const uint16_t* codes, size_t len, size_t channel_size, const double* scales,
+                          const int64_t* zero_points, double* out, void* stream) {
+    SKV_REQUIRE(channel_size > 0 && len % channel_size == 0, "dequantize: bad channel size");
+    if (len == 0) return SKV_OK;
+    SKV_REQUIRE(codes && scales && zero_points && out, "dequantize: null argument");
+    SKV_CUDA(launch_dequantize(codes, static_cast<long long>(len), static_cast<long long>(channel_size), scales,
+                               reinterpret_cast<const long long*>(zero_points), out, as_stream(stream)));
+    return SKV_OK;
+}
+
+skv_status skv_profile_enable(skv_cache* c, int enable) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    DeviceGuard guard(c->d.device);
+    c->prof = enable != 0;
+    for (cudaEvent_t e : c->ev) c->ev_pool.push_back(e);
+    c->ev.clear();
+    c->prof_launches = 0;
+    c->prof_bytes = 0;
+    return SKV_OK;
+}
+
+skv_status skv_profile_read(skv_cache* c, double* total_ms, int64_t* launches, uint64_t* algo) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    DeviceGuard guard(c->d.device);
+    double tot = 0.0;
+    for (size_t i = 0; i + 1 < c->ev.size(); i += 2) {
+        SKV_CUDA(cudaEventSynchronize(c->ev[i + 1]));
+        float ms = 0.f;
+        SKV_CUDA(cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]));
+        tot += ms;
+    }
+    if (total_ms) *total_ms = tot;
+    if (launches) *launches = c->prof_launches;
+    if (algo) *algo = c->prof_bytes;
+    return SKV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,42 @@
+// skv_internal.h -- declarations shared by the translation units of
+// libskv_b200.so (not part of the public ABI; see include/skv_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "skv_b200.h"
+#include "skv_decode.cuh"
+
+namespace skv_impl {
+
+void count_launch();
+
+cudaError_t launch_swa_select(const double* imp, int batch, long long ld, int n, int k, int m,
+                              bool dense, int* out, cudaStream_t st);
+cudaError_t launch_top_k(const double* v, int batch, long long ld, int len, int k, int* out,
+                         cudaStream_t st);
+cudaError_t launch_quantize(const double* x, long long len, long long cs, uint32_t bits,
+                            uint16_t* codes, double* scales, long long* zps, cudaStream_t st);
+cudaError_t launch_dequantize(const uint16_t* codes, long long len, long long cs,
+                              const double* scales, const long long* zps, double* out,
+                              cudaStream_t st);
+cudaError_t launch_cache_write(int kv_dtype, int q_dtype, uint8_t* kv, float2* meta, double* imp,
+                               const void* k, const void* v, int H, int Ncap, int b0, int nb,
+                               int t0, int nt, cudaStream_t st);
+cudaError_t launch_cache_read(int kv_dtype, const uint8_t* kv, const float2* meta, float* out,
+                              int H, int Ncap, int b0, int nb, int t0, int nt, cudaStream_t st);
+
+// Fused decode kernel: one instantiation per (kv dtype, q dtype, HG).
+struct DecodeLaunch {
+    const void* func;
+    size_t (*smem)(int m, int nc);
+    int hg;
+};
+// Returns nullptr when no kernel is compiled for the combination.
+const DecodeLaunch* find_decode(int kv_dtype, int q_dtype, int hg);
+cudaError_t launch_decode(const DecodeLaunch& dl, const skvd::DecodeParams& p, int grid_g,
+                          size_t smem, cudaStream_t st);
+
+}  // namespace skv_impl

@@ -1,0 +1,285 @@
+// skv_kernels.cu -- sm_100a kernels behind the C ABI other than the fused
+// decode kernel: batched swa_select / top_k, fp64 quantize / dequantize,
+// cache writes (append with fake-quant) and reads.
+#include "skv_internal.h"
+
+namespace skvd {
+
+// ---------------------------------------------------------------- selection
+constexpr int kSelThreads = 512;
+
+// swa_select (attention.hpp:142-171) + SparseSelection::all: one CTA per row.
+__global__ void __launch_bounds__(kSelThreads)
+    swa_select_kernel(const double* __restrict__ imp, long long ld, int n, int k, int m, int dense,
+                      int* __restrict__ out) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    TopkSmem<kSelThreads>& s = *reinterpret_cast<TopkSmem<kSelThreads>*>(smem);
+    uint64_t* keys = reinterpret_cast<uint64_t*>(smem + align_up(sizeof(TopkSmem<kSelThreads>), 16));
+    const int b = blockIdx.x, tid = threadIdx.x;
+    int* o = out + static_cast<size_t>(b) * m;
+    if (dense) {
+        for (int i = tid; i < m; i += kSelThreads) o[i] = i;
+        return;
+    }
+    const int nc = n - k;
+    const double* row = imp + static_cast<size_t>(b) * ld;
+    for (int i = tid; i < nc; i += kSelThreads) keys[i] = order_key(row[i]);
+    named_sync(1, kSelThreads);
+    block_topk<kSelThreads, 1>(keys, nc, k, o, s, tid);  // global picks first (ascending)
+    for (int i = tid; i < k; i += kSelThreads) o[k + i] = n - k + i;  // then the local window
+}
+
+// top_k_indices (matrix.hpp:162-176) per row.
+__global__ void __launch_bounds__(kSelThreads)
+    top_k_kernel(const double* __restrict__ v, long long ld, int len, int k, int* __restrict__ out) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    TopkSmem<kSelThreads>& s = *reinterpret_cast<TopkSmem<kSelThreads>*>(smem);
+    uint64_t* keys = reinterpret_cast<uint64_t*>(smem + align_up(sizeof(TopkSmem<kSelThreads>), 16));
+    const int b = blockIdx.x, tid = threadIdx.x;
+    const double* row = v + static_cast<size_t>(b) * ld;
+    for (int i = tid; i < len; i += kSelThreads) keys[i] = order_key(row[i]);
+    named_sync(1, kSelThreads);
+    block_topk<kSelThreads, 1>(keys, len, k, out + static_cast<size_t>(b) * k, s, tid);
+}
+
+// ------------------------------------------------------------------- quant
+// quantize (quant.hpp:43-81): one warp per channel group, fp64 throughout.
+__global__ void quantize_kernel(const double* __restrict__ x, long long groups, long long cs,
+                                uint32_t bits, uint16_t* __restrict__ codes,
+                                double* __restrict__ scales, long long* __restrict__ zps) {
+    const long long grp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (grp >= groups) return;
+    const double* c = x + grp * cs;
+    double lo = c[0], hi = c[0];
+    for (long long i = lane; i < cs; i += 32) {
+        lo = c[i] < lo ? c[i] : lo;
+        hi = hi < c[i] ? c[i] : hi;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double olo = __shfl_xor_sync(0xffffffffu, lo, off);
+        const double ohi = __shfl_xor_sync(0xffffffffu, hi, off);
+        lo = olo < lo ? olo : lo;
+        hi = hi < ohi ? ohi : hi;
+    }
+    double scale;
+    if (hi == lo) {
+        const double a = fabs(lo);
+        scale = a < 1e-12 ? 1e-12 : a;
+    } else {
+        const double levels = static_cast<double>((1ull << bits) - 1);
+        const double s = (hi - lo) / levels;
+        scale = s < 1e-12 ? 1e-12 : s;
+    }
+    const long long zp = rne_ref(-lo / scale);
+    const long long max_code = static_cast<long long>((1ull << bits) - 1);
+    for (long long i = lane; i < cs; i += 32) {
+        long long code = rne_ref(c[i] / scale + static_cast<double>(zp));
+        code = code < 0 ? 0 : (code > max_code ? max_code : code);
+        codes[grp * cs + i] = static_cast<uint16_t>(code);
+    }
+    if (lane == 0) {
+        scales[grp] = scale;
+        zps[grp] = zp;
+    }
+}
+
+// dequantize (quant.hpp:84-95)
+__global__ void dequantize_kernel(const uint16_t* __restrict__ codes, long long len, long long cs,
+                                  const double* __restrict__ scales,
+                                  const long long* __restrict__ zps, double* __restrict__ out) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= len) return;
+    const long long g = i / cs;
+    out[i] = scales[g] * (static_cast<double>(codes[i]) - static_cast<double>(zps[g]));
+}
+
+// ------------------------------------------------------------- cache write
+// AttentionState::append_token for a block of tokens (+ engine head_rows
+// fake-quant). One warp per (b, t, kv, head) row of D elements.
+template <class QT, class KV>
+__global__ void cache_write_kernel(uint8_t* __restrict__ kv, float2* __restrict__ meta,
+                                   double* __restrict__ imp, const QT* __restrict__ k,
+                                   const QT* __restrict__ v, int H, int Ncap, int b0, int nb, int t0,
+                                   int nt) {
+    constexpr int D = kHeadDim;
+    const long long row = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const long long rows = static_cast<long long>(nb) * nt * 2 * H;
+    if (row >= rows) return;
+    const int h = static_cast<int>(row % H);
+    const int which = static_cast<int>((row / H) % 2);
+    const int t = static_cast<int>((row / (2 * H)) % nt);
+    const int bb = static_cast<int>(row / (2LL * H * nt));
+    const QT* src = (which ? v : k) + ((static_cast<size_t>(bb) * nt + t) * H + h) * D;
+    const size_t tok = static_cast<size_t>(b0 + bb) * Ncap + (t0 + t);
+    uint8_t* dst = kv + ((tok * 2 + which) * H + h) * static_cast<size_t>(D) * KV::E;
+    if constexpr (!KV::QUANT) {
+        using T = typename KV::T;
+        T* d = reinterpret_cast<T*>(dst);
+        for (int i = lane; i < D; i += 32) d[i] = from_f<T>(to_f(src[i]));
+    } else {
+        double x[D / 32];
+        for (int i = 0; i < D / 32; ++i) x[i] = static_cast<double>(to_f(src[lane * (D / 32) + i]));
+        double lo = x[0], hi = x[0];
+        for (int i = 1; i < D / 32; ++i) {
+            lo = x[i] < lo ? x[i] : lo;
+            hi = hi < x[i] ? x[i] : hi;
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+            const double olo = __shfl_xor_sync(0xffffffffu, lo, off);
+            const double ohi = __shfl_xor_sync(0xffffffffu, hi, off);
+            lo = olo < lo ? olo : lo;
+            hi = hi < ohi ? ohi : hi;
+        }
+        double scale;
+        if (hi == lo) {
+            const double a = fabs(lo);
+            scale = a < 1e-12 ? 1e-12 : a;
+        } else {
+            const double s = (hi - lo) / 255.0;
+            scale = s < 1e-12 ? 1e-12 : s;
+        }
+        const long long zp = rne_ref(-lo / scale);
+        uint32_t packed = 0;
+        for (int i = 0; i < D / 32; ++i) {
+            long long c = rne_ref(x[i] / scale + static_cast<double>(zp));
+            c = c < 0 ? 0 : (c > 255 ? 255 : c);
+            packed |= static_cast<uint32_t>(c) << (8 * i);
+        }
+        reinterpret_cast<uint32_t*>(dst)[lane] = packed;
+        if (lane == 0)
+            meta[(tok * 2 + which) * H + h] =
+                make_float2(static_cast<float>(scale), static_cast<float>(-scale * static_cast<double>(zp)));
+    }
+    if (lane == 0 && h == 0 && which == 0) imp[tok] = 0.0;
+}
+
+// Cache read-back to fp32 [nb][nt][2][H][D].
+template <class KV>
+__global__ void cache_read_kernel(const uint8_t* __restrict__ kv, const float2* __restrict__ meta,
+                                  float* __restrict__ out, int H, int Ncap, int b0, int nb, int t0,
+                                  int nt) {
+    constexpr int D = kHeadDim;
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long total = static_cast<long long>(nb) * nt * 2 * H * D;
+    if (i >= total) return;
+    const int d = static_cast<int>(i % D);
+    const long long r = i / D;  // row over [nb][nt][2][H]
+    const int h = static_cast<int>(r % H);
+    const int which = static_cast<int>((r / H) % 2);
+    const int t = static_cast<int>((r / (2 * H)) % nt);
+    const int bb = static_cast<int>(r / (2LL * H * nt));
+    const size_t tok = static_cast<size_t>(b0 + bb) * Ncap + (t0 + t);
+    const size_t at = ((tok * 2 + which) * H + h) * D + d;
+    if constexpr (KV::QUANT) {
+        const float2 ms = meta[(tok * 2 + which) * H + h];
+        out[i] = fmaf(ms.x, static_cast<float>(kv[at]), ms.y);
+    } else {
+        using T = typename KV::T;
+        out[i] = to_f(reinterpret_cast<const T*>(kv)[at]);
+    }
+}
+
+}  // namespace skvd
+
+// ============================================================ launchers
+namespace skv_impl {
+using namespace skvd;
+
+cudaError_t launch_swa_select(const double* imp, int batch, long long ld, int n, int k, int m,
+                              bool dense, int* out, cudaStream_t st) {
+    const size_t smem = align_up(sizeof(TopkSmem<kSelThreads>), 16) +
+                        (dense ? 0 : static_cast<size_t>(n - k) * 8);
+    cudaError_t e = cudaFuncSetAttribute(swa_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    swa_select_kernel<<<batch, kSelThreads, smem, st>>>(imp, ld, n, k, m, dense ? 1 : 0, out);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_top_k(const double* v, int batch, long long ld, int len, int k, int* out,
+                         cudaStream_t st) {
+    const size_t smem = align_up(sizeof(TopkSmem<kSelThreads>), 16) + static_cast<size_t>(len) * 8;
+    cudaError_t e = cudaFuncSetAttribute(top_k_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    top_k_kernel<<<batch, kSelThreads, smem, st>>>(v, ld, len, k, out);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_quantize(const double* x, long long len, long long cs, uint32_t bits,
+                            uint16_t* codes, double* scales, long long* zps, cudaStream_t st) {
+    const long long groups = len / cs;
+    const int threads = 256;
+    const long long blocks = (groups * 32 + threads - 1) / threads;
+    quantize_kernel<<<static_cast<unsigned>(blocks), threads, 0, st>>>(x, groups, cs, bits, codes, scales, zps);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dequantize(const uint16_t* codes, long long len, long long cs, const double* scales,
+                              const long long* zps, double* out, cudaStream_t st) {
+    const int threads = 256;
+    const long long blocks = (len + threads - 1) / threads;
+    dequantize_kernel<<<static_cast<unsigned>(blocks), threads, 0, st>>>(codes, len, cs, scales, zps, out);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <class QT, class KV>
+static cudaError_t write_t(uint8_t* kv, float2* meta, double* imp, const void* k, const void* v, int H,
+                           int Ncap, int b0, int nb, int t0, int nt, cudaStream_t st) {
+    const long long rows = static_cast<long long>(nb) * nt * 2 * H;
+    const int threads = 256;
+    const long long blocks = (rows * 32 + threads - 1) / threads;
+    cache_write_kernel<QT, KV><<<static_cast<unsigned>(blocks), threads, 0, st>>>(
+        kv, meta, imp, static_cast<const QT*>(k), static_cast<const QT*>(v), H, Ncap, b0, nb, t0, nt);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cache_write(int kv_dtype, int q_dtype, uint8_t* kv, float2* meta, double* imp,
+                               const void* k, const void* v, int H, int Ncap, int b0, int nb, int t0,
+                               int nt, cudaStream_t st) {
+    switch (kv_dtype) {
+    case SKV_F32:
+        return write_t<float, KvF32>(kv, meta, imp, k, v, H, Ncap, b0, nb, t0, nt, st);
+    case SKV_F16:
+        return write_t<__half, KvF16>(kv, meta, imp, k, v, H, Ncap, b0, nb, t0, nt, st);
+    case SKV_BF16:
+        return write_t<__nv_bfloat16, KvBF16>(kv, meta, imp, k, v, H, Ncap, b0, nb, t0, nt, st);
+    case SKV_U8:
+        if (q_dtype == SKV_F32) return write_t<float, KvU8>(kv, meta, imp, k, v, H, Ncap, b0, nb, t0, nt, st);
+        if (q_dtype == SKV_F16) return write_t<__half, KvU8>(kv, meta, imp, k, v, H, Ncap, b0, nb, t0, nt, st);
+        return write_t<__nv_bfloat16, KvU8>(kv, meta, imp, k, v, H, Ncap, b0, nb, t0, nt, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <class KV>
+static cudaError_t read_t(const uint8_t* kv, const float2* meta, float* out, int H, int Ncap, int b0,
+                          int nb, int t0, int nt, cudaStream_t st) {
+    const long long total = static_cast<long long>(nb) * nt * 2 * H * kHeadDim;
+    const int threads = 256;
+    cache_read_kernel<KV><<<static_cast<unsigned>((total + threads - 1) / threads), threads, 0, st>>>(
+        kv, meta, out, H, Ncap, b0, nb, t0, nt);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cache_read(int kv_dtype, const uint8_t* kv, const float2* meta, float* out, int H,
+                              int Ncap, int b0, int nb, int t0, int nt, cudaStream_t st) {
+    switch (kv_dtype) {
+    case SKV_F32: return read_t<KvF32>(kv, meta, out, H, Ncap, b0, nb, t0, nt, st);
+    case SKV_F16: return read_t<KvF16>(kv, meta, out, H, Ncap, b0, nb, t0, nt, st);
+    case SKV_BF16: return read_t<KvBF16>(kv, meta, out, H, Ncap, b0, nb, t0, nt, st);
+    case SKV_U8: return read_t<KvU8>(kv, meta, out, H, Ncap, b0, nb, t0, nt, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace skv_impl
