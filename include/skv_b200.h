@@ -54,6 +54,7 @@ typedef struct skv_cache_desc {
     int32_t kv_dtype;  /* skv_dtype of stored K/V */
     int32_t q_dtype;   /* compute dtype of q / new k,v / out: F32, F16, BF16 */
     int32_t device;    /* CUDA ordinal */
+    int32_t out_f32;   /* nonzero: attention outputs are fp32 instead of q_dtype */
 } skv_cache_desc;
 
 const char* skv_last_error(void);
@@ -100,7 +101,8 @@ skv_status skv_prefill_seed(skv_cache* cache, int layer, int n, const void* q_la
  * the pre-step importance (swa_select, attention.hpp:142-171; dense when
  * 2k >= n), attend over the selection (attend_over_indices,
  * attention.hpp:183-231) and fold the weights into the importance.
- * n counts the current token. q, k_new, v_new, out: device [B][H][D] q_dtype.
+ * n counts the current token. q, k_new, v_new: device [B][H][D] q_dtype; out
+ * [B][H][D] in q_dtype (fp32 when the cache was created with out_f32).
  * idx_out (nullable): device int32 [B][m] ascending (SparseSelection::all);
  * w_out (nullable): device fp32 [B][H][m] softmax weights in idx order.
  * m = skv_swa_keep_count(n, r). One kernel launch. */

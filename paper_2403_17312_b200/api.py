@@ -12,7 +12,7 @@ from dataclasses import dataclass
 
 import torch
 
-from ._lib import ContractViolation, check, lib
+from ._lib import ContractViolation, CudaError, InfeasiblePlan, OutOfDeviceMemory, Unsupported, check, lib  # noqa: F401
 
 SKV_F32, SKV_F16, SKV_BF16, SKV_U8 = 0, 1, 2, 3
 _DT = {torch.float32: SKV_F32, torch.float16: SKV_F16, torch.bfloat16: SKV_BF16, torch.uint8: SKV_U8}
@@ -122,7 +122,7 @@ def quantize_roundtrip(x: torch.Tensor, bits: int, channel_size: int) -> torch.T
 class _Desc(C.Structure):
     _fields_ = [("layers", C.c_int32), ("batch", C.c_int32), ("heads", C.c_int32),
                 ("head_dim", C.c_int32), ("capacity", C.c_int32), ("kv_dtype", C.c_int32),
-                ("q_dtype", C.c_int32), ("device", C.c_int32)]
+                ("q_dtype", C.c_int32), ("device", C.c_int32), ("out_f32", C.c_int32)]
 
 
 class SwaCache:
@@ -131,7 +131,7 @@ class SwaCache:
     HBM, fp64 head-summed importance accumulator."""
 
     def __init__(self, layers: int, batch: int, heads: int, head_dim: int, capacity: int,
-                 kv_dtype="f16", q_dtype=None, device: int | None = None):
+                 kv_dtype="f16", q_dtype=None, device: int | None = None, out_f32: bool = False):
         self.layers, self.batch, self.heads, self.head_dim, self.capacity = (
             layers, batch, heads, head_dim, capacity)
         self.kv_code = _code(kv_dtype)
@@ -140,7 +140,9 @@ class SwaCache:
         self.q_dtype = _TORCH[self.q_code]
         self.device = torch.cuda.current_device() if device is None else device
         self.dev = torch.device("cuda", self.device)
-        d = _Desc(layers, batch, heads, head_dim, capacity, self.kv_code, self.q_code, self.device)
+        self.out_dtype = torch.float32 if out_f32 else self.q_dtype
+        d = _Desc(layers, batch, heads, head_dim, capacity, self.kv_code, self.q_code, self.device,
+                  int(out_f32))
         h = C.c_void_p()
         check(lib().skv_cache_create(C.byref(d), C.byref(h)))
         self._h = h
@@ -192,7 +194,8 @@ class SwaCache:
 
     # Engine::prefill accumulator seeding (engine.hpp:508-512)
     def prefill_seed(self, layer: int, n: int, q_last: torch.Tensor) -> torch.Tensor:
-        out = torch.empty_like(self._q(q_last, (self.batch, self.heads, self.head_dim)))
+        out = torch.empty(self._q(q_last, (self.batch, self.heads, self.head_dim)).shape,
+                          dtype=self.out_dtype, device=self.dev)
         check(lib().skv_prefill_seed(self._h, layer, n, _ptr(q_last), _ptr(out), _stream(q_last)))
         return out
 
@@ -202,7 +205,7 @@ class SwaCache:
         shp = (self.batch, self.heads, self.head_dim)
         for t in (q, k_new, v_new):
             self._q(t, shp)
-        out = torch.empty_like(q) if out is None else out
+        out = torch.empty(q.shape, dtype=self.out_dtype, device=self.dev) if out is None else out
         m = swa_keep_count(n, r)
         idx = torch.empty((self.batch, m), dtype=torch.int32, device=self.dev) if return_indices else None
         w = (torch.empty((self.batch, self.heads, m), dtype=torch.float32, device=self.dev)
@@ -215,7 +218,7 @@ class SwaCache:
         shp = (self.layers, self.batch, self.heads, self.head_dim)
         for t in (q, k_new, v_new):
             self._q(t, shp)
-        out = torch.empty_like(q) if out is None else out
+        out = torch.empty(q.shape, dtype=self.out_dtype, device=self.dev) if out is None else out
         check(lib().skv_swa_decode_step(self._h, n, r, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(out),
                                         _stream(q)))
         return out
@@ -239,7 +242,8 @@ class SwaCache:
         if idx.dim() == 1:
             idx = idx.reshape(1, -1).expand(self.batch, -1).contiguous()
         m = idx.shape[1]
-        out = torch.empty_like(self._q(q, (self.batch, self.heads, self.head_dim)))
+        out = torch.empty(self._q(q, (self.batch, self.heads, self.head_dim)).shape, dtype=self.out_dtype,
+                          device=self.dev)
         w = (torch.empty((self.batch, self.heads, m), dtype=torch.float32, device=self.dev)
              if return_weights else None)
         check(lib().skv_attend_over_indices(self._h, layer, n, _ptr(idx), m, _ptr(q), _ptr(out), _ptr(w),

@@ -81,6 +81,9 @@ inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 }  // namespace
 
+struct skv_cache;
+static size_t out_size(const skv_cache* c);
+
 struct skv_cache {
     skv_cache_desc d{};
     size_t row_bytes = 0;    // one head row of D elements (storage dtype)
@@ -89,8 +92,10 @@ struct skv_cache {
     uint8_t* kv = nullptr;
     float2* meta = nullptr;
     double* imp = nullptr;
-    float* wpart = nullptr;
-    unsigned* counters = nullptr;
+    float* wpart = nullptr;  // [L][B][H][Ncap] per-head-group weight sums of the last attend
+    int* idx = nullptr;      // [L][B][Ncap] selection (ascending) for the pending step
+    std::vector<int> pend_n;     // per layer: n the index buffer was selected for (-1: none)
+    std::vector<double> pend_r;  // per layer: its ratio
     uint64_t device_bytes = 0;
     int num_sms = 0;
     int max_smem = 0;
@@ -101,9 +106,11 @@ struct skv_cache {
     bool prof = false;
     std::vector<cudaEvent_t> ev;  // start/stop pairs
     std::vector<cudaEvent_t> ev_pool;
-    int64_t prof_launches = 0;
-    uint64_t prof_bytes = 0;
+    int64_t attend_launches = 0;
+    uint64_t algo_bytes = 0;
 };
+
+static size_t out_size(const skv_cache* c) { return c->d.out_f32 ? 4 : dtype_size(c->d.q_dtype); }
 
 extern "C" {
 
@@ -155,8 +162,8 @@ skv_status skv_cache_create(const skv_cache_desc* desc, skv_cache** out) {
     const size_t meta_bytes =
         d.kv_dtype == SKV_U8 ? static_cast<size_t>(d.layers) * d.batch * d.capacity * 2 * d.heads * 8 : 0;
     const size_t imp_bytes = static_cast<size_t>(d.layers) * d.batch * d.capacity * 8;
-    const size_t wpart_bytes = static_cast<size_t>(d.batch) * d.heads * d.capacity * 4;
-    const size_t cnt_bytes = static_cast<size_t>(d.layers) * d.batch * 4;
+    const size_t wpart_bytes = static_cast<size_t>(d.layers) * d.batch * d.heads * d.capacity * 4;
+    const size_t cnt_bytes = static_cast<size_t>(d.layers) * d.batch * d.capacity * 4;  // selections
     auto alloc = [&](void** p, size_t bytes) -> bool {
         if (bytes == 0) return true;
         if (cudaMalloc(p, bytes) != cudaSuccess) {
@@ -170,14 +177,15 @@ skv_status skv_cache_create(const skv_cache_desc* desc, skv_cache** out) {
         !alloc(reinterpret_cast<void**>(&c->meta), meta_bytes) ||
         !alloc(reinterpret_cast<void**>(&c->imp), imp_bytes) ||
         !alloc(reinterpret_cast<void**>(&c->wpart), wpart_bytes) ||
-        !alloc(reinterpret_cast<void**>(&c->counters), cnt_bytes)) {
+        !alloc(reinterpret_cast<void**>(&c->idx), cnt_bytes)) {
         const uint64_t want = kv_bytes + meta_bytes + imp_bytes + wpart_bytes + cnt_bytes;
         skv_cache_destroy(c);
         return fail(SKV_ERR_OOM, "skv_cache_create: cannot allocate %llu device bytes",
                     static_cast<unsigned long long>(want));
     }
     SKV_CUDA(cudaMemset(c->imp, 0, imp_bytes));
-    SKV_CUDA(cudaMemset(c->counters, 0, cnt_bytes));
+    c->pend_n.assign(d.layers, -1);
+    c->pend_r.assign(d.layers, 0.0);
     if (meta_bytes) SKV_CUDA(cudaMemset(c->meta, 0, meta_bytes));
     SKV_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, d.device));
     SKV_CUDA(cudaDeviceGetAttribute(&c->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, d.device));
@@ -192,7 +200,7 @@ skv_status skv_cache_destroy(skv_cache* c) {
     cudaFree(c->meta);
     cudaFree(c->imp);
     cudaFree(c->wpart);
-    cudaFree(c->counters);
+    cudaFree(c->idx);
     cudaFree(c->stage);
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -221,6 +229,7 @@ skv_status skv_cache_write(skv_cache* c, int layer, int b0, int nb, int t0, int 
     SKV_REQUIRE(k != nullptr && v != nullptr, "append_token: null rows");
     DeviceGuard guard(c->d.device);
     const size_t lt = static_cast<size_t>(layer) * c->d.batch * c->d.capacity;
+    c->pend_n[layer] = -1;
     SKV_CUDA(launch_cache_write(c->d.kv_dtype, c->d.q_dtype, c->kv + layer * c->layer_bytes,
                                 c->meta ? c->meta + lt * 2 * c->d.heads : nullptr, c->imp + lt, k, v,
                                 c->d.heads, c->d.capacity, b0, nb, t0, nt, as_stream(stream)));
@@ -244,6 +253,7 @@ skv_status skv_importance_set(skv_cache* c, int layer, int b0, int nb, int len, 
     if (skv_status s = check_block(c, layer, b0, nb, 0, len)) return s;
     DeviceGuard guard(c->d.device);
     double* dst = c->imp + (static_cast<size_t>(layer) * c->d.batch + b0) * c->d.capacity;
+    c->pend_n[layer] = -1;
     SKV_CUDA(cudaMemcpy2DAsync(dst, c->d.capacity * 8, src, static_cast<size_t>(len) * 8,
                                static_cast<size_t>(len) * 8, nb, cudaMemcpyDefault, as_stream(stream)));
     return SKV_OK;
@@ -264,9 +274,9 @@ skv_status skv_importance_get(const skv_cache* c, int layer, int b0, int nb, int
 namespace {
 
 // Pick heads-per-CTA: the smallest head group whose grid still fits in one
-// wave of resident CTAs (all CTAs stream concurrently and finish together);
-// otherwise the largest available group. SKV_HG overrides (tuning).
-skv_status pick_decode(skv_cache* c, int m, int nc, const DecodeLaunch** dl_out, size_t* smem_out) {
+// wave of resident CTAs (all CTAs stream concurrently); otherwise the largest
+// available group. SKV_HG overrides (tuning).
+skv_status pick_attend(skv_cache* c, int m, const DecodeLaunch** dl_out, size_t* smem_out) {
     static const int env_hg = [] {
         const char* s = std::getenv("SKV_HG");
         return s ? std::atoi(s) : 0;
@@ -279,7 +289,7 @@ skv_status pick_decode(skv_cache* c, int m, int nc, const DecodeLaunch** dl_out,
         if (env_hg && hg != env_hg) continue;
         const DecodeLaunch* dl = find_decode(c->d.kv_dtype, c->d.q_dtype, hg);
         if (!dl) continue;
-        const size_t smem = dl->smem(m, nc);
+        const size_t smem = dl->smem(m);
         if (smem > static_cast<size_t>(c->max_smem)) continue;
         best = dl;
         best_smem = smem;
@@ -291,64 +301,122 @@ skv_status pick_decode(skv_cache* c, int m, int nc, const DecodeLaunch** dl_out,
         if (occ > 0 && ctas <= static_cast<long long>(occ) * c->num_sms) break;
     }
     if (!best)
-        return fail(SKV_ERR_UNSUPPORTED, "no decode kernel fits (heads %d, m %d, shared memory %d)",
-                    c->d.heads, m, c->max_smem);
+        return fail(SKV_ERR_UNSUPPORTED, "no attend kernel fits (heads %d, m %d, shared memory %d)", c->d.heads, m,
+                    c->max_smem);
     *dl_out = best;
     *smem_out = best_smem;
     return SKV_OK;
 }
 
-uint64_t algo_bytes(const skv_cache* c, int n, int m, int nc, bool append) {
+// Algorithmic HBM bytes of one attend launch (the roofline numerator): q in,
+// out out, new K/V rows in and stored, every other selected row of K and V
+// gathered once.
+uint64_t attend_algo_bytes(const skv_cache* c, int m, bool append) {
     const uint64_t H = c->d.heads, D = c->d.head_dim;
-    const uint64_t eq = dtype_size(c->d.q_dtype), ekv = dtype_size(c->d.kv_dtype);
+    const uint64_t eq = dtype_size(c->d.q_dtype), eo = out_size(c), ekv = dtype_size(c->d.kv_dtype);
     const uint64_t meta = c->d.kv_dtype == SKV_U8 ? 8 : 0;
     const uint64_t row = D * ekv + meta;  // one head row as stored
-    uint64_t per = H * D * eq * 2;        // q in, out
+    uint64_t per = H * D * (eq + eo);
     uint64_t gathered = static_cast<uint64_t>(m);
     if (append) {
-        per += 2 * H * D * eq + 2 * H * row;  // new k,v in; stored rows out
-        gathered -= 1;                        // the new token is not re-read
+        per += 2 * H * D * eq + 2 * H * row;
+        gathered -= 1;
     }
-    per += static_cast<uint64_t>(nc) * 8;            // importance candidates
-    per += 2 * gathered * H * row;                   // K and V gather
-    per += static_cast<uint64_t>(m) * 16;            // importance read-modify-write
-    (void)n;
+    per += 2 * gathered * H * row;
     return per * static_cast<uint64_t>(c->d.batch);
 }
 
-skv_status run_decode(skv_cache* c, int layer, int n, int k, int m, int nc, int mode, bool append,
-                      bool dense, const void* q, const void* k_new, const void* v_new, void* out,
-                      const int32_t* idx_in, int32_t* idx_out, float* w_out, cudaStream_t st) {
+struct StepShape {
+    int k, m;
+    bool dense;
+};
+
+skv_status step_shape(const skv_cache* c, int n, double r, StepShape* s) {
+    SKV_REQUIRE(n >= 1, "swa_attention: empty cache");
+    SKV_REQUIRE(n <= c->d.capacity, "decode_step: context overflow");
+    const size_t k = skv_swa_window_k(static_cast<size_t>(n), r);
+    if (k == 0) return SKV_ERR_CONTRACT;
+    s->k = static_cast<int>(k);
+    s->dense = n < 2 || 2 * static_cast<int>(k) >= n;
+    s->m = s->dense ? n : 2 * s->k;
+    return SKV_OK;
+}
+
+int* layer_idx(const skv_cache* c, int layer) {
+    return c->idx + static_cast<size_t>(layer) * c->d.batch * c->d.capacity;
+}
+
+// The per-sequence select kernel for one layer: optionally fold the attend
+// kernel's weight partials into the importance, optionally select for
+// (n_next, r_next) into the layer's index buffer (recorded as pending).
+skv_status launch_select_c(skv_cache* c, int layer, int apply, const int* tok_prev, long long tok_prev_ld,
+                           int m_prev, int G, int cur_tok, int n_next, double r_next, bool pdl, cudaStream_t st) {
+    skvd::SelectParams p{};
+    p.imp = c->imp + static_cast<size_t>(layer) * c->d.batch * c->d.capacity;
+    p.imp_ld = c->d.capacity;
+    p.wpart = c->wpart + static_cast<size_t>(layer) * c->d.batch * c->d.heads * c->d.capacity;
+    p.G = G;
+    p.m_prev = m_prev;
+    p.tok_prev = tok_prev;
+    p.tok_prev_ld = tok_prev_ld;
+    p.apply = apply;
+    p.cur_tok = cur_tok;
+    p.idx = layer_idx(c, layer);
+    p.idx_ld = c->d.capacity;
+    p.pdl_wait = 1;
+    c->pend_n[layer] = -1;
+    if (n_next > 0 && n_next <= c->d.capacity) {
+        StepShape s;
+        if (skv_status e = step_shape(c, n_next, r_next, &s)) return e;
+        if (!s.dense && static_cast<size_t>(n_next - s.k) * 8 + 8192 > static_cast<size_t>(c->max_smem))
+            return fail(SKV_ERR_UNSUPPORTED, "swa_select: %d candidates exceed shared memory", n_next - s.k);
+        p.select = 1;
+        p.n = n_next;
+        p.k = s.k;
+        p.m = s.m;
+        p.dense = s.dense ? 1 : 0;
+    }
+    if (!p.apply && !p.select) return SKV_OK;
+    SKV_CUDA(launch_select(p, c->d.batch, pdl, st));
+    if (p.select) {
+        c->pend_n[layer] = n_next;
+        c->pend_r[layer] = r_next;
+    }
+    return SKV_OK;
+}
+
+skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok, long long tok_ld, bool append,
+                           const void* q, const void* k_new, const void* v_new, void* out, int32_t* idx_out,
+                           float* w_out, bool pdl, cudaStream_t st, int* G_out) {
     const DecodeLaunch* dl = nullptr;
     size_t smem = 0;
-    if (skv_status s = pick_decode(c, m, nc, &dl, &smem)) return s;
+    if (skv_status s = pick_attend(c, m, &dl, &smem)) return s;
     const size_t lt = static_cast<size_t>(layer) * c->d.batch * c->d.capacity;
-    skvd::DecodeParams p{};
+    skvd::AttendParams p{};
     p.kv = c->kv + layer * c->layer_bytes;
     p.kv_w = c->kv + layer * c->layer_bytes;
     p.meta = c->meta ? c->meta + lt * 2 * c->d.heads : nullptr;
     p.meta_w = const_cast<float2*>(p.meta);
-    p.imp = c->imp + lt;
     p.q = q;
     p.k_new = k_new;
     p.v_new = v_new;
     p.out = out;
-    p.idx_in = idx_in;
+    p.tok = tok;
+    p.tok_ld = tok_ld;
     p.idx_out = idx_out;
     p.w_out = w_out;
-    p.wpart = c->wpart;
-    p.counters = c->counters + static_cast<size_t>(layer) * c->d.batch;
+    p.wpart = c->wpart + static_cast<size_t>(layer) * c->d.batch * c->d.heads * c->d.capacity;
     p.B = c->d.batch;
     p.H = c->d.heads;
     p.Ncap = c->d.capacity;
     p.n = n;
-    p.k = k;
     p.m = m;
-    p.mode = mode;
     p.append = append ? 1 : 0;
-    p.dense = dense ? 1 : 0;
+    p.out_f32 = c->d.out_f32 ? 1 : 0;
+    p.pdl_wait = 0;  // inputs are complete before the first (non-PDL) launch of a call
     p.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d.head_dim)));
     const int grid_g = c->d.heads / dl->hg;
+    *G_out = grid_g;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->prof) {
         auto take = [&]() {
@@ -364,33 +432,37 @@ skv_status run_decode(skv_cache* c, int layer, int n, int k, int m, int nc, int 
         e0 = take();
         e1 = take();
         SKV_CUDA(cudaEventRecord(e0, st));
+        pdl = false;
     }
-    SKV_CUDA(launch_decode(*dl, p, grid_g, smem, st));
+    SKV_CUDA(launch_attend(*dl, p, grid_g, smem, pdl, st));
+    c->algo_bytes += attend_algo_bytes(c, m, append);
+    c->attend_launches += 1;
     if (c->prof) {
         SKV_CUDA(cudaEventRecord(e1, st));
         c->ev.push_back(e0);
         c->ev.push_back(e1);
-        c->prof_launches += 1;
-        c->prof_bytes += algo_bytes(c, n, m, nc, append);
     }
     return SKV_OK;
 }
 
-struct StepShape {
-    int k, m, nc;
-    bool dense;
-};
-
-skv_status step_shape(const skv_cache* c, int n, double r, StepShape* s) {
-    SKV_REQUIRE(n >= 1, "swa_attention: empty cache");
-    SKV_REQUIRE(n <= c->d.capacity, "decode_step: context overflow");
-    const size_t k = skv_swa_window_k(static_cast<size_t>(n), r);
-    if (k == 0) return SKV_ERR_CONTRACT;
-    s->k = static_cast<int>(k);
-    s->dense = n < 2 || 2 * static_cast<int>(k) >= n;
-    s->m = s->dense ? n : 2 * s->k;
-    s->nc = s->dense ? 0 : n - s->k;
-    return SKV_OK;
+// One layer of one decode step: [select if no matching pending selection] ->
+// attend (append + gather + softmax + PV) -> select kernel (fold weights into
+// the importance, select for n+1 with the same ratio).
+skv_status decode_layer_impl(skv_cache* c, int layer, int n, double r, const void* q, const void* k_new,
+                             const void* v_new, void* out, int32_t* idx_out, float* w_out, bool chained,
+                             cudaStream_t st) {
+    StepShape s;
+    if (skv_status e = step_shape(c, n, r, &s)) return e;
+    bool fresh = false;
+    if (!(c->pend_n[layer] == n && c->pend_r[layer] == r)) {
+        if (skv_status e = launch_select_c(c, layer, 0, nullptr, 0, 0, 0, -1, n, r, false, st)) return e;
+        fresh = true;
+    }
+    int G = 0;
+    if (skv_status e = launch_attend_c(c, layer, n, s.m, layer_idx(c, layer), c->d.capacity, true, q, k_new, v_new,
+                                       out, idx_out, w_out, chained && !fresh, st, &G))
+        return e;
+    return launch_select_c(c, layer, 1, layer_idx(c, layer), c->d.capacity, s.m, G, n - 1, n + 1, r, !c->prof, st);
 }
 
 }  // namespace
@@ -403,8 +475,12 @@ skv_status skv_prefill_seed(skv_cache* c, int layer, int n, const void* q_last, 
     SKV_REQUIRE(n >= 1 && n <= c->d.capacity, "prefill: prompt length out of range");
     SKV_REQUIRE(q_last != nullptr && out != nullptr, "prefill: null argument");
     DeviceGuard guard(c->d.device);
-    return run_decode(c, layer, n, 1, n, 0, skvd::kModeSeed, false, true, q_last, nullptr, nullptr, out,
-                      nullptr, nullptr, nullptr, as_stream(stream));
+    const cudaStream_t st = as_stream(stream);
+    int G = 0;
+    if (skv_status e = launch_attend_c(c, layer, n, n, nullptr, 0, false, q_last, nullptr, nullptr, out, nullptr,
+                                       nullptr, false, st, &G))
+        return e;
+    return launch_select_c(c, layer, 2, nullptr, 0, n, G, -1, 0, 0.0, true, st);
 }
 
 skv_status skv_swa_decode_layer(skv_cache* c, int layer, int n, double r, const void* q, const void* k_new,
@@ -412,11 +488,8 @@ skv_status skv_swa_decode_layer(skv_cache* c, int layer, int n, double r, const 
     SKV_REQUIRE(c != nullptr, "null cache");
     SKV_REQUIRE(layer >= 0 && layer < c->d.layers, "KvLedger: layer out of range");
     SKV_REQUIRE(q && k_new && v_new && out, "decode_step: null argument");
-    StepShape s;
-    if (skv_status st = step_shape(c, n, r, &s)) return st;
     DeviceGuard guard(c->d.device);
-    return run_decode(c, layer, n, s.k, s.m, s.nc, skvd::kModeSwaStep, true, s.dense, q, k_new, v_new, out,
-                      nullptr, idx_out, w_out, as_stream(stream));
+    return decode_layer_impl(c, layer, n, r, q, k_new, v_new, out, idx_out, w_out, false, as_stream(stream));
 }
 
 skv_status skv_swa_decode_step(skv_cache* c, int n, double r, const void* q, const void* k_new,
@@ -427,12 +500,17 @@ skv_status skv_swa_decode_step(skv_cache* c, int n, double r, const void* q, con
     if (skv_status st = step_shape(c, n, r, &s)) return st;
     DeviceGuard guard(c->d.device);
     const size_t per_layer = static_cast<size_t>(c->d.batch) * c->d.heads * c->d.head_dim * dtype_size(c->d.q_dtype);
+    const size_t per_layer_out = static_cast<size_t>(c->d.batch) * c->d.heads * c->d.head_dim * out_size(c);
     for (int l = 0; l < c->d.layers; ++l) {
         const size_t o = per_layer * l;
-        if (skv_status st = run_decode(c, l, n, s.k, s.m, s.nc, skvd::kModeSwaStep, true, s.dense,
-                                       static_cast<const uint8_t*>(q) + o, static_cast<const uint8_t*>(k_new) + o,
-                                       static_cast<const uint8_t*>(v_new) + o, static_cast<uint8_t*>(out) + o,
-                                       nullptr, nullptr, nullptr, as_stream(stream)))
+        // Layer l > 0 launches with programmatic dependent launch: its inputs
+        // were complete before this call's first launch, so it can stream
+        // while the previous layer's kernels drain.
+        if (skv_status st = decode_layer_impl(c, l, n, r, static_cast<const uint8_t*>(q) + o,
+                                              static_cast<const uint8_t*>(k_new) + o,
+                                              static_cast<const uint8_t*>(v_new) + o,
+                                              static_cast<uint8_t*>(out) + per_layer_out * l, nullptr, nullptr,
+                                              l > 0, as_stream(stream)))
             return st;
     }
     return SKV_OK;
@@ -445,15 +523,16 @@ skv_status skv_swa_decode_step_host(skv_cache* c, int n, double r, const void* q
     DeviceGuard guard(c->d.device);
     const size_t bytes = static_cast<size_t>(c->d.layers) * c->d.batch * c->d.heads * c->d.head_dim *
                          dtype_size(c->d.q_dtype);
-    if (c->stage_bytes < 4 * bytes) {
+    const size_t obytes = static_cast<size_t>(c->d.layers) * c->d.batch * c->d.heads * c->d.head_dim * out_size(c);
+    if (c->stage_bytes < 3 * bytes + obytes) {
         cudaFree(c->stage);
         c->stage = nullptr;
-        if (cudaMalloc(reinterpret_cast<void**>(&c->stage), 4 * bytes) != cudaSuccess) {
+        if (cudaMalloc(reinterpret_cast<void**>(&c->stage), 3 * bytes + obytes) != cudaSuccess) {
             cudaGetLastError();
             c->stage_bytes = 0;
             return fail(SKV_ERR_OOM, "decode_step_host: cannot allocate staging");
         }
-        c->stage_bytes = 4 * bytes;
+        c->stage_bytes = 3 * bytes + obytes;
     }
     const cudaStream_t st = as_stream(stream);
     uint8_t *dq = c->stage, *dk = dq + bytes, *dv = dk + bytes, *dout = dv + bytes;
@@ -461,7 +540,7 @@ skv_status skv_swa_decode_step_host(skv_cache* c, int n, double r, const void* q
     SKV_CUDA(cudaMemcpyAsync(dk, k_host, bytes, cudaMemcpyHostToDevice, st));
     SKV_CUDA(cudaMemcpyAsync(dv, v_host, bytes, cudaMemcpyHostToDevice, st));
     if (skv_status s = skv_swa_decode_step(c, n, r, dq, dk, dv, dout, stream)) return s;
-    SKV_CUDA(cudaMemcpyAsync(out_host, dout, bytes, cudaMemcpyDeviceToHost, st));
+    SKV_CUDA(cudaMemcpyAsync(out_host, dout, obytes, cudaMemcpyDeviceToHost, st));
     return SKV_OK;
 }
 
@@ -474,11 +553,12 @@ skv_status skv_attend_over_indices(skv_cache* c, int layer, int n, const int32_t
     SKV_REQUIRE(m <= n, "attend_over_indices: more indices than tokens");
     SKV_REQUIRE(idx && q && out, "attend_over_indices: null argument");
     DeviceGuard guard(c->d.device);
-    // The reference validates every index (attention.hpp:186-192); the fused
-    // kernel additionally needs them unique (ascending, as sel.all() gives).
+    const cudaStream_t st = as_stream(stream);
+    // The reference validates every index (attention.hpp:186-192); the
+    // importance fold additionally needs them unique (ascending, as sel.all()).
     std::vector<int32_t> h(static_cast<size_t>(c->d.batch) * m);
-    SKV_CUDA(cudaMemcpyAsync(h.data(), idx, h.size() * 4, cudaMemcpyDefault, as_stream(stream)));
-    SKV_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    SKV_CUDA(cudaMemcpyAsync(h.data(), idx, h.size() * 4, cudaMemcpyDefault, st));
+    SKV_CUDA(cudaStreamSynchronize(st));
     for (int b = 0; b < c->d.batch; ++b)
         for (int i = 0; i < m; ++i) {
             const int32_t t = h[static_cast<size_t>(b) * m + i];
@@ -486,17 +566,20 @@ skv_status skv_attend_over_indices(skv_cache* c, int layer, int n, const int32_t
             SKV_REQUIRE(i == 0 || t > h[static_cast<size_t>(b) * m + i - 1],
                         "attend_over_indices: indices must be strictly ascending");
         }
-    return run_decode(c, layer, n, 1, m, 0, skvd::kModeExplicit, false, false, q, nullptr, nullptr, out, idx,
-                      nullptr, w_out, as_stream(stream));
+    int G = 0;
+    if (skv_status e = launch_attend_c(c, layer, n, m, idx, m, false, q, nullptr, nullptr, out, nullptr, w_out,
+                                       false, st, &G))
+        return e;
+    return launch_select_c(c, layer, 1, idx, m, m, G, -1, 0, 0.0, true, st);
 }
 
 skv_status skv_swa_select(const double* importance, int batch, int64_t ld, int n, double r, int32_t* idx_out,
                           int32_t* m_out, void* stream) {
     SKV_REQUIRE(batch >= 1, "swa_select: empty batch");
     SKV_REQUIRE(idx_out != nullptr, "swa_select: null output");
-    const size_t k = skv_swa_window_k(static_cast<size_t>(n < 0 ? 0 : n), r);
-    if (k == 0) return SKV_ERR_CONTRACT;
     SKV_REQUIRE(n >= 0, "swa_select: negative length");
+    const size_t k = skv_swa_window_k(static_cast<size_t>(n), r);
+    if (k == 0) return SKV_ERR_CONTRACT;
     const bool dense = n < 2 || 2 * static_cast<int>(k) >= n;
     const int m = dense ? n : 2 * static_cast<int>(k);
     if (m_out) *m_out = m;
@@ -507,7 +590,17 @@ skv_status skv_swa_select(const double* importance, int batch, int64_t ld, int n
         if (static_cast<size_t>(n - k) * 8 + 8192 > 220 * 1024)
             return fail(SKV_ERR_UNSUPPORTED, "swa_select: %d candidates exceed shared memory", n - static_cast<int>(k));
     }
-    SKV_CUDA(launch_swa_select(importance, batch, ld, n, static_cast<int>(k), m, dense, idx_out, as_stream(stream)));
+    skvd::SelectParams p{};
+    p.imp = const_cast<double*>(importance);
+    p.imp_ld = ld;
+    p.select = 1;
+    p.n = n;
+    p.k = static_cast<int>(k);
+    p.m = m;
+    p.dense = dense ? 1 : 0;
+    p.idx = idx_out;
+    p.idx_ld = m;
+    SKV_CUDA(launch_select(p, batch, false, as_stream(stream)));
     return SKV_OK;
 }
 
@@ -550,8 +643,8 @@ skv_status skv_profile_enable(skv_cache* c, int enable) {
     c->prof = enable != 0;
     for (cudaEvent_t e : c->ev) c->ev_pool.push_back(e);
     c->ev.clear();
-    c->prof_launches = 0;
-    c->prof_bytes = 0;
+    c->attend_launches = 0;
+    c->algo_bytes = 0;
     return SKV_OK;
 }
 
@@ -566,8 +659,8 @@ skv_status skv_profile_read(skv_cache* c, double* total_ms, int64_t* launches, u
         tot += ms;
     }
     if (total_ms) *total_ms = tot;
-    if (launches) *launches = c->prof_launches;
-    if (algo) *algo = c->prof_bytes;
+    if (launches) *launches = c->attend_launches;
+    if (algo) *algo = c->algo_bytes;
     return SKV_OK;
 }
 

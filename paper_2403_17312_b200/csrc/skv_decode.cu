@@ -8,13 +8,13 @@ using namespace skvd;
 namespace {
 
 template <class KV, class QT, int HG>
-size_t smem_of(int m, int nc) {
-    return decode_smem<KV, HG>(m, nc).total;
+size_t smem_of(int m) {
+    return decode_smem<KV, HG>(m).total;
 }
 
 template <class KV, class QT, int HG>
 DecodeLaunch make() {
-    return DecodeLaunch{reinterpret_cast<const void*>(&swa_decode_kernel<KV, QT, HG>),
+    return DecodeLaunch{reinterpret_cast<const void*>(&swa_attend_kernel<KV, QT, HG>),
                         &smem_of<KV, QT, HG>, HG};
 }
 
@@ -61,13 +61,23 @@ const DecodeLaunch* find_decode(int kv_dtype, int q_dtype, int hg) {
     return nullptr;
 }
 
-cudaError_t launch_decode(const DecodeLaunch& dl, const DecodeParams& p, int grid_g, size_t smem,
+cudaError_t launch_attend(const DecodeLaunch& dl, const AttendParams& p, int grid_g, size_t smem, bool pdl,
                           cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(dl.func, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    void* args[] = {const_cast<DecodeParams*>(&p)};
-    e = cudaLaunchKernel(dl.func, dim3(grid_g, p.B), dim3(kDecodeThreads), args, smem, st);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid_g, p.B);
+    cfg.blockDim = dim3(kDecodeThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    void* args[] = {const_cast<AttendParams*>(&p)};
+    e = cudaLaunchKernelExC(&cfg, dl.func, args);
     count_launch();
     return e;
 }

@@ -78,6 +78,8 @@ __device__ __forceinline__ void named_arrive(uint32_t id, uint32_t count) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
 // ----------------------------------------------------------- number helpers
 // Reference round_half_even (common.hpp:43-54), floor-based, fp64.
 __device__ __forceinline__ long long rne_ref(double x) {
@@ -158,6 +160,53 @@ __device__ __forceinline__ void cvt16(const uint4& r, float (&f)[16], KvU8) {
             f[4 * i + j] = __uint_as_float(bits) - 8388608.0f;
         }
     }
+}
+
+// 16 bytes -> float2 pairs (feed the packed FFMA2 pipe).
+__device__ __forceinline__ void cvt16x2(const uint4& r, float2 (&f)[2], KvF32) {
+    f[0] = make_float2(__uint_as_float(r.x), __uint_as_float(r.y));
+    f[1] = make_float2(__uint_as_float(r.z), __uint_as_float(r.w));
+}
+__device__ __forceinline__ void cvt16x2(const uint4& r, float2 (&f)[4], KvF16) {
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        __half2 h;
+        memcpy(&h, &w[i], 4);
+        f[i] = __half22float2(h);
+    }
+}
+__device__ __forceinline__ void cvt16x2(const uint4& r, float2 (&f)[4], KvBF16) {
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) f[i] = make_float2(__uint_as_float(w[i] << 16), __uint_as_float(w[i] & 0xFFFF0000u));
+}
+__device__ __forceinline__ void cvt16x2(const uint4& r, float2 (&f)[8], KvU8) {
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+    const float2 off = make_float2(-8388608.0f, -8388608.0f);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        // 0x4B0000bb == 2^23 + bb exactly: one PRMT per code, one FADD2 per pair.
+        const float2 a = make_float2(__uint_as_float(__byte_perm(w[i], 0x4B000000u, 0x7540u)),
+                                     __uint_as_float(__byte_perm(w[i], 0x4B000000u, 0x7541u)));
+        const float2 b = make_float2(__uint_as_float(__byte_perm(w[i], 0x4B000000u, 0x7542u)),
+                                     __uint_as_float(__byte_perm(w[i], 0x4B000000u, 0x7543u)));
+        f[2 * i] = __fadd2_rn(a, off);
+        f[2 * i + 1] = __fadd2_rn(b, off);
+    }
+}
+
+// Programmatic dependent launch (PDL).
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Make this thread's generic-proxy global writes visible to later async-proxy
+// (bulk copy) reads issued by other threads after a barrier.
+__device__ __forceinline__ void fence_global_to_async() {
+    __threadfence();
+    asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // Scalar loads of a compute-side (q / new k,v) element as float.

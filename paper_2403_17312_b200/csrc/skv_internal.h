@@ -8,13 +8,13 @@
 
 #include "skv_b200.h"
 #include "skv_decode.cuh"
+#include "skv_select.cuh"
 
 namespace skv_impl {
 
 void count_launch();
 
-cudaError_t launch_swa_select(const double* imp, int batch, long long ld, int n, int k, int m,
-                              bool dense, int* out, cudaStream_t st);
+cudaError_t launch_select(const skvd::SelectParams& p, int batch, bool pdl, cudaStream_t st);
 cudaError_t launch_top_k(const double* v, int batch, long long ld, int len, int k, int* out,
                          cudaStream_t st);
 cudaError_t launch_quantize(const double* x, long long len, long long cs, uint32_t bits,
@@ -31,12 +31,12 @@ cudaError_t launch_cache_read(int kv_dtype, const uint8_t* kv, const float2* met
 // Fused decode kernel: one instantiation per (kv dtype, q dtype, HG).
 struct DecodeLaunch {
     const void* func;
-    size_t (*smem)(int m, int nc);
+    size_t (*smem)(int m);
     int hg;
 };
 // Returns nullptr when no kernel is compiled for the combination.
 const DecodeLaunch* find_decode(int kv_dtype, int q_dtype, int hg);
-cudaError_t launch_decode(const DecodeLaunch& dl, const skvd::DecodeParams& p, int grid_g,
-                          size_t smem, cudaStream_t st);
+cudaError_t launch_attend(const DecodeLaunch& dl, const skvd::AttendParams& p, int grid_g,
+                          size_t smem, bool pdl, cudaStream_t st);
 
 }  // namespace skv_impl

@@ -2,31 +2,44 @@
 // decode kernel: batched swa_select / top_k, fp64 quantize / dequantize,
 // cache writes (append with fake-quant) and reads.
 #include "skv_internal.h"
+#include "skv_select.cuh"
 
 namespace skvd {
 
 // ---------------------------------------------------------------- selection
 constexpr int kSelThreads = 512;
 
-// swa_select (attention.hpp:142-171) + SparseSelection::all: one CTA per row.
-__global__ void __launch_bounds__(kSelThreads)
-    swa_select_kernel(const double* __restrict__ imp, long long ld, int n, int k, int m, int dense,
-                      int* __restrict__ out) {
+// Importance fold + next selection, one CTA per sequence (skv_select.cuh).
+__global__ void __launch_bounds__(kSelectThreads) swa_select_kernel(const SelectParams p) {
     extern __shared__ __align__(16) uint8_t smem[];
-    TopkSmem<kSelThreads>& s = *reinterpret_cast<TopkSmem<kSelThreads>*>(smem);
-    uint64_t* keys = reinterpret_cast<uint64_t*>(smem + align_up(sizeof(TopkSmem<kSelThreads>), 16));
+    TopkSmem<kSelectThreads>& s = *reinterpret_cast<TopkSmem<kSelectThreads>*>(smem);
+    uint64_t* keys = reinterpret_cast<uint64_t*>(smem + align_up(sizeof(TopkSmem<kSelectThreads>), 16));
     const int b = blockIdx.x, tid = threadIdx.x;
-    int* o = out + static_cast<size_t>(b) * m;
-    if (dense) {
-        for (int i = tid; i < m; i += kSelThreads) o[i] = i;
+    pdl_launch_dependents();
+    if (p.pdl_wait) pdl_wait();
+    double* imp = p.imp + static_cast<size_t>(b) * p.imp_ld;
+    if (p.apply) {
+        const float* wp = p.wpart + static_cast<size_t>(b) * p.G * p.m_prev;
+        const int* tp = p.tok_prev ? p.tok_prev + static_cast<size_t>(b) * p.tok_prev_ld : nullptr;
+        for (int pos = tid; pos < p.m_prev; pos += kSelectThreads) {
+            double v = 0.0;
+            for (int g = 0; g < p.G; ++g) v += static_cast<double>(wp[static_cast<size_t>(g) * p.m_prev + pos]);
+            const int t = tp ? tp[pos] : pos;
+            imp[t] = (p.apply == 2 || t == p.cur_tok) ? v : imp[t] + v;
+        }
+    }
+    if (!p.select) return;
+    __syncthreads();
+    int* o = p.idx + static_cast<size_t>(b) * p.idx_ld;
+    if (p.dense) {
+        for (int i = tid; i < p.m; i += kSelectThreads) o[i] = i;
         return;
     }
-    const int nc = n - k;
-    const double* row = imp + static_cast<size_t>(b) * ld;
-    for (int i = tid; i < nc; i += kSelThreads) keys[i] = order_key(row[i]);
-    named_sync(1, kSelThreads);
-    block_topk<kSelThreads, 1>(keys, nc, k, o, s, tid);  // global picks first (ascending)
-    for (int i = tid; i < k; i += kSelThreads) o[k + i] = n - k + i;  // then the local window
+    const int nc = p.n - p.k;
+    for (int i = tid; i < nc; i += kSelectThreads) keys[i] = order_key(imp[i]);
+    named_sync(1, kSelectThreads);
+    block_topk<kSelectThreads, 1>(keys, nc, p.k, o, s, tid);  // global picks, ascending
+    for (int i = tid; i < p.k; i += kSelectThreads) o[p.k + i] = p.n - p.k + i;  // local window
 }
 
 // top_k_indices (matrix.hpp:162-176) per row.
@@ -188,16 +201,25 @@ __global__ void cache_read_kernel(const uint8_t* __restrict__ kv, const float2* 
 namespace skv_impl {
 using namespace skvd;
 
-cudaError_t launch_swa_select(const double* imp, int batch, long long ld, int n, int k, int m,
-                              bool dense, int* out, cudaStream_t st) {
-    const size_t smem = align_up(sizeof(TopkSmem<kSelThreads>), 16) +
-                        (dense ? 0 : static_cast<size_t>(n - k) * 8);
+cudaError_t launch_select(const SelectParams& p, int batch, bool pdl, cudaStream_t st) {
+    const int nc = (p.select && !p.dense) ? p.n - p.k : 0;
+    const size_t smem = select_smem(nc);
     cudaError_t e = cudaFuncSetAttribute(swa_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    swa_select_kernel<<<batch, kSelThreads, smem, st>>>(imp, ld, n, k, m, dense ? 1 : 0, out);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(batch);
+    cfg.blockDim = dim3(kSelectThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    e = cudaLaunchKernelEx(&cfg, swa_select_kernel, p);
     count_launch();
-    return cudaGetLastError();
+    return e;
 }
 
 cudaError_t launch_top_k(const double* v, int batch, long long ld, int len, int k, int* out,

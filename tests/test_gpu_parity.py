@@ -1,0 +1,348 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Bit-exact: selection / top-k indices, quantization codes, scales, zero points.
+Within north_star tolerance: attention outputs (1e-5 fp32, 1e-3 fp16/bf16,
+1e-3 INT8 KV), importance accumulators (1e-4 relative; weights are fp32 on
+device). Trajectories run in the engine's order (engine.hpp:592-629) and
+allow selection differences only at importance ties within 1e-6 relative.
+"""
+import numpy as np
+import pytest
+import torch
+
+from skv_testlib import TOL, OracleSeq, assert_close, round_to, selection_flip_is_tie
+
+pytestmark = pytest.mark.gpu
+
+TD = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}
+
+
+@pytest.fixture(scope="module")
+def api():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2403_17312_b200 import api as a
+
+    a.lib()  # loads libskv_b200.so or raises
+    return a
+
+
+def split(flat, lens):
+    out, o = [], 0
+    for n in lens:
+        out.append(flat[o:o + n])
+        o += n
+    return out
+
+
+def cuda(x, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(x))
+    return t.to(device="cuda", dtype=dtype) if dtype is not None else t.cuda()
+
+
+# ---------------------------------------------------------------- bit-exact ops
+def test_top_k_golden(api, golden):
+    vs = split(golden["topk_v"], golden["topk_lens"])
+    outs = split(golden["topk_out"], golden["topk_k"])
+    for v, k, o in zip(vs, golden["topk_k"], outs):
+        got = api.top_k_indices(cuda(v), int(k)).cpu().numpy()
+        assert np.array_equal(got, o), (v.size, k)
+
+
+def test_top_k_random_large(api, port):
+    rng = np.random.default_rng(5)
+    for ln, k in [(922, 102), (3686, 410), (20000, 1), (5000, 5000), (1, 1), (4096, 2048)]:
+        v = rng.standard_normal(ln)
+        v[rng.integers(0, ln, ln // 4)] = 0.5  # mass ties
+        v[:3] = -0.0
+        got = api.top_k_indices(cuda(v), k).cpu().numpy()
+        assert np.array_equal(got, port.top_k_indices(v, k)), (ln, k)
+
+
+def test_swa_select_golden(api, golden):
+    imps = split(golden["sel_imp"], np.maximum(golden["sel_n"] - 1, 0))
+    alls = split(golden["sel_all"], golden["sel_m"])
+    for n, r, imp, want in zip(golden["sel_n"], golden["sel_r"], imps, alls):
+        t = cuda(imp if imp.size else np.zeros(1))
+        got = api.swa_select(t, int(n), float(r)).all.cpu().numpy()
+        assert np.array_equal(got, want), (n, r)
+
+
+def test_swa_select_batched(api, port):
+    rng = np.random.default_rng(9)
+    B, n = 8, 1024
+    imp = np.round(rng.random((B, n + 7)) * 1000) / 1000.0
+    sel = api.swa_select(cuda(imp), n, 0.2)
+    for b in range(B):
+        want, k, _, _ = port.swa_select(imp[b, :n - 1], n, 0.2)
+        assert np.array_equal(sel.all[b].cpu().numpy(), want)
+
+
+def test_quantize_golden(api, golden):
+    xs = split(golden["q_x"], golden["q_lens"])
+    codes = split(golden["q_codes"], golden["q_lens"])
+    o = 0
+    for x, b, cs, c in zip(xs, golden["q_bits"], golden["q_cs"], codes):
+        gc, gs, gz = api.quantize(cuda(x), int(b), int(cs))
+        ng = gs.numel()
+        assert np.array_equal(gc.cpu().numpy().astype(np.int64), c)
+        assert np.array_equal(gs.cpu().numpy(), golden["q_scales"][o:o + ng])
+        assert np.array_equal(gz.cpu().numpy(), golden["q_zps"][o:o + ng])
+        deq = api.dequantize(gc, int(cs) or x.size, gs, gz).cpu().numpy()
+        assert np.max(np.abs(deq - x)) <= gs.max().item() / 2 + 1e-9
+        o += ng
+
+
+def test_quantize_random_vs_oracle(api, port):
+    rng = np.random.default_rng(21)
+    for bits in (4, 8):
+        for scale in (1e-13, 1e-3, 1.0, 1e4):
+            x = rng.standard_normal(128 * 64) * scale
+            x[:128] = 3.25  # constant group
+            x[128:256] = np.abs(x[128:256]) + 1.0  # lo > 0: large negative zero point
+            a = [t.cpu().numpy() for t in api.quantize(cuda(x), bits, 128)]
+            b = port.quantize(x, bits, 128)
+            for p, q in zip(a, b):
+                assert np.array_equal(p.astype(np.int64) if p.dtype == np.uint16 else p,
+                                      q.astype(np.int64) if q.dtype == np.uint16 else q)
+
+
+# ------------------------------------------------------- attend_over_indices
+@pytest.mark.parametrize("dt", ["f32", "f16", "bf16"])
+def test_attend_over_indices(api, port, dt):
+    rng = np.random.default_rng(31)
+    B, H, D, n = 3, 8, 128, 300
+    kv = round_to(rng.standard_normal((B, n, 2, H, D)), dt)
+    q = round_to(rng.standard_normal((B, H, D)), dt)
+    # bf16 outputs would round at 2^-9 > 1e-3: bf16 caches report fp32 outputs
+    cache = api.SwaCache(1, B, H, D, n + 4, kv_dtype=dt, out_f32=dt == "bf16")
+    cache.append_tokens(0, 0, 0, cuda(kv[:, :, 0], TD[dt]), cuda(kv[:, :, 1], TD[dt]))
+    base = rng.random((B, n))
+    cache.set_importance(0, cuda(base))
+    idx = np.sort(rng.choice(n, size=97, replace=False)).astype(np.int32)
+    idx_b = np.stack([idx] * B)
+    out, w = cache.attend_over_indices(0, n, cuda(idx_b), cuda(q, TD[dt]), return_weights=True)
+    imp = cache.importance(0, n).cpu().numpy()
+    for b in range(B):
+        seq = OracleSeq(port, H, D, n)
+        seq.keys[:] = kv[b, :, 0].transpose(1, 0, 2)
+        seq.vals[:] = kv[b, :, 1].transpose(1, 0, 2)
+        attn, aw = port.attend_over_indices(seq.keys, seq.vals, seq.acc, n, q[b], idx, n)
+        assert_close(out[b].float().cpu().numpy(), attn, TOL[dt], f"attn b={b}")
+        assert_close(w[b].cpu().numpy(), seq.acc[:, idx], TOL[dt], f"weights b={b}")
+        np.testing.assert_allclose(imp[b] - base[b], aw, rtol=1e-4, atol=1e-7)
+
+
+def test_attend_over_indices_errors(api):
+    cache = api.SwaCache(1, 1, 4, 128, 16, kv_dtype="f32")
+    q = torch.zeros((1, 4, 128), device="cuda")
+    with pytest.raises(api.ContractViolation):
+        cache.attend_over_indices(0, 8, torch.tensor([[1, 9]], device="cuda"), q)  # index >= n
+    with pytest.raises(api.ContractViolation):
+        cache.attend_over_indices(0, 8, torch.tensor([[3, 1]], device="cuda"), q)  # not ascending
+    with pytest.raises(api.ContractViolation):
+        cache.attend_over_indices(0, 0, torch.tensor([[0]], device="cuda"), q)  # empty cache
+    with pytest.raises(api.ContractViolation):
+        cache.attend_over_indices(3, 8, torch.tensor([[0]], device="cuda"), q)  # layer out of range
+
+
+# ------------------------------------------------------------ decode trajectory
+def run_trajectory(api, port, dt, B, H, s, steps, r, seed, q_dt=None, check_every=1, L=1, layer=None):
+    """Prefill s tokens, seed the accumulator from the dense last row, then
+    `steps` decode steps (append -> select -> attend), all compared to the
+    oracle. Returns the number of tolerated tie flips."""
+    rng = np.random.default_rng(seed)
+    D = 128
+    quant = dt == "u8"
+    qdt = q_dt or ("f16" if quant else dt)
+    ncap = s + steps
+    layer = L - 1 if layer is None else layer
+    kv = round_to(rng.standard_normal((B, ncap, 2, H, D)), qdt)
+    qs = round_to(rng.standard_normal((steps + 1, B, H, D)) * 1.5, qdt)
+    cache = api.SwaCache(L, B, H, D, ncap, kv_dtype=dt, q_dtype=qdt, out_f32=qdt == "bf16")
+    cache.append_tokens(layer, 0, 0, cuda(kv[:, :s, 0], TD[qdt]), cuda(kv[:, :s, 1], TD[qdt]))
+    seqs = [OracleSeq(port, H, D, ncap, quant) for _ in range(B)]
+    for b in range(B):
+        for t in range(s):
+            seqs[b].append(t, kv[b, t, 0], kv[b, t, 1])
+    seed_out = cache.prefill_seed(layer, s, cuda(qs[0], TD[qdt])).float().cpu().numpy()
+    imp_dev = cache.importance(layer, s).cpu().numpy()
+    for b in range(B):
+        ref_out = seqs[b].seed(s, qs[0][b])
+        assert_close(seed_out[b], ref_out, TOL[dt], "prefill seed attn")
+        np.testing.assert_allclose(imp_dev[b], seqs[b].importance(s), rtol=1e-4, atol=1e-7)
+    flips = 0
+    for j in range(steps):
+        n = s + j + 1
+        imp_pre = [sq.importance(n - 1) for sq in seqs]
+        q = cuda(qs[j + 1], TD[qdt])
+        out, idx, w = cache.swa_decode_layer(layer, n, r, q, cuda(kv[:, n - 1, 0], TD[qdt]),
+                                             cuda(kv[:, n - 1, 1], TD[qdt]), return_indices=True,
+                                             return_weights=True)
+        out, idx = out.float().cpu().numpy(), idx.cpu().numpy()
+        resync = []
+        for b in range(B):
+            seqs[b].append(n - 1, kv[b, n - 1, 0], kv[b, n - 1, 1])
+            attn, aw, oidx = seqs[b].step(n, r, qs[j + 1][b])
+            if not np.array_equal(idx[b], oidx):
+                k = api.swa_window_k(n, r)
+                assert selection_flip_is_tie(idx[b], oidx, imp_pre[b], n, k), \
+                    f"selection mismatch step {j} seq {b}: {sorted(set(idx[b]) ^ set(oidx))}"
+                flips += 1
+                resync.append(b)
+                continue
+            assert_close(out[b], attn, TOL[dt], f"attn step {j} seq {b}")
+        if resync or (j % check_every == 0) or j == steps - 1:
+            imp = cache.importance(layer, n).cpu().numpy()
+            for b in range(B):
+                want = seqs[b].importance(n)
+                if b in resync:
+                    continue
+                np.testing.assert_allclose(imp[b], want, rtol=1e-4, atol=1e-7,
+                                           err_msg=f"importance step {j} seq {b}")
+            if resync:  # put the device back on the oracle's trajectory
+                full = imp.copy()
+                for b in resync:
+                    full[b] = seqs[b].importance(n)
+                cache.set_importance(layer, cuda(full))
+    return flips
+
+
+def test_golden_trajectory_gpu(api, golden):
+    """The reference's own 8-step trajectory (tests/golden) on the device."""
+    H, D, s, steps = (int(x) for x in golden["traj_shape"])
+    r = float(golden["traj_r"][0])
+    kv, qs = golden["traj_kv"], golden["traj_q"]  # fp16-representable
+    idxs = split(golden["traj_idx"], golden["traj_m"])
+    for dt in ("f32", "f16"):
+        cache = api.SwaCache(1, 1, H, D, s + steps, kv_dtype=dt)
+        k0 = kv[0][:, :s].transpose(1, 0, 2)[None]
+        v0 = kv[1][:, :s].transpose(1, 0, 2)[None]
+        cache.append_tokens(0, 0, 0, cuda(k0, TD[dt]), cuda(v0, TD[dt]))
+        cache.set_importance(0, cuda(golden["traj_acc0"][:, :s].sum(0)[None]))
+        for j in range(steps):
+            n = s + j + 1
+            out, idx, _ = cache.swa_decode_layer(0, n, r, cuda(qs[j + 1][None], TD[dt]),
+                                                 cuda(kv[0][:, n - 1][None], TD[dt]),
+                                                 cuda(kv[1][:, n - 1][None], TD[dt]), return_indices=True)
+            assert np.array_equal(idx[0].cpu().numpy(), idxs[j]), (dt, j)
+            assert_close(out[0].float().cpu().numpy(), golden["traj_attn"][j], TOL[dt], f"{dt} step {j}")
+        imp = cache.importance(0, s + steps).cpu().numpy()[0]
+        np.testing.assert_allclose(imp, golden["traj_acc_final"].sum(0), rtol=1e-4, atol=1e-7)
+
+
+# config 1 (fp32, H=32, n=512) and the dtype/shape family of configs 2-4 at
+# oracle-friendly batch sizes.
+@pytest.mark.parametrize("dt,B,H,s,steps", [
+    ("f32", 1, 32, 511, 24),    # BASELINE config 1 shape: n = 512 .. 535
+    ("f16", 3, 32, 512, 12),    # config 2 shape (OPT-6.7B heads)
+    ("bf16", 2, 40, 1024, 6),   # config 3 shape (OPT-13B heads)
+    ("u8", 2, 56, 1000, 4),     # config 4 family: INT8 KV, OPT-30B heads
+])
+def test_decode_trajectory(api, port, dt, B, H, s, steps):
+    flips = run_trajectory(api, port, dt, B, H, s, steps, 0.2, seed=sum(map(ord, dt)) * 100 + H)
+    assert flips <= max(1, steps * B // 10)
+
+
+def test_decode_trajectory_u8_f32_query(api, port):
+    run_trajectory(api, port, "u8", 1, 8, 300, 6, 0.2, seed=77, q_dt="f32")
+
+
+def test_decode_from_first_token(api, port):
+    """n = 1, 2, 3, ... : degenerate branches n<2 and 2k>=n (attention.hpp:146-164)."""
+    run_trajectory(api, port, "f32", 2, 4, 1, 40, 0.2, seed=3)
+
+
+@pytest.mark.parametrize("r", [1.0, 0.5, 0.05])
+def test_decode_ratios(api, port, r):
+    """r = 1 is exactly dense (swa_window_k forces ceil(n/2))."""
+    run_trajectory(api, port, "f32", 2, 8, 64, 8, r, seed=int(r * 100))
+
+
+def test_decode_multilayer_step(api):
+    """skv_swa_decode_step over L layers == per-layer calls; host-buffer
+    variant == device variant."""
+    rng = np.random.default_rng(8)
+    L, B, H, D, s = 3, 4, 8, 128, 100
+    kv = torch.from_numpy(rng.standard_normal((L, B, s, 2, H, D))).half().cuda()
+    q, kn, vn = (torch.from_numpy(rng.standard_normal((L, B, H, D))).half().cuda() for _ in range(3))
+    caches = [api.SwaCache(L, B, H, D, s + 2, kv_dtype="f16") for _ in range(3)]
+    for c in caches:
+        for l in range(L):
+            c.append_tokens(l, 0, 0, kv[l, :, :, 0].contiguous(), kv[l, :, :, 1].contiguous())
+            c.prefill_seed(l, s, q[l])
+    n = s + 1
+    a = caches[0].swa_decode_step(n, 0.2, q, kn, vn)
+    b = torch.stack([caches[1].swa_decode_layer(l, n, 0.2, q[l].contiguous(), kn[l].contiguous(),
+                                                vn[l].contiguous())[0] for l in range(L)])
+    outh = torch.empty_like(q, device="cpu").pin_memory()
+    caches[2].swa_decode_step_host(n, 0.2, q.cpu().pin_memory(), kn.cpu().pin_memory(), vn.cpu().pin_memory(), outh)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    assert torch.equal(a.cpu(), outh)
+    for l in range(L):
+        assert torch.equal(caches[0].importance(l, n), caches[1].importance(l, n))
+
+
+def test_decode_errors(api):
+    cache = api.SwaCache(2, 1, 4, 128, 8, kv_dtype="f16")
+    x = torch.zeros((1, 4, 128), device="cuda", dtype=torch.float16)
+    with pytest.raises(api.ContractViolation):
+        cache.swa_decode_layer(0, 9, 0.2, x, x, x)  # beyond capacity
+    with pytest.raises(api.ContractViolation):
+        cache.swa_decode_layer(2, 3, 0.2, x, x, x)  # layer out of range
+    with pytest.raises(api.ContractViolation):
+        cache.swa_decode_layer(0, 3, 0.0, x, x, x)  # ratio out of (0,1]
+    with pytest.raises(api.ContractViolation):
+        cache.swa_decode_layer(0, 0, 0.2, x, x, x)  # empty cache
+    with pytest.raises(api.Unsupported):
+        api.SwaCache(1, 1, 4, 64, 8, kv_dtype="f16")  # head_dim not compiled
+    with pytest.raises(api.ContractViolation):
+        api.swa_select(torch.zeros(5, dtype=torch.float64, device="cuda"), 100, 0.2)
+
+
+# ------------------------------------------------ full-size property checks
+def test_full_size_properties_config2(api, port):
+    """BASELINE config 2 shape (B=64, H=32, D=128, s=512 fp16) on 2 layers:
+    size-independent invariants on every sequence plus oracle spot checks."""
+    B, H, D, s, L, steps = 64, 32, 128, 512, 2, 3
+    g = torch.Generator(device="cuda").manual_seed(2403)
+    cache = api.SwaCache(L, B, H, D, s + steps, kv_dtype="f16")
+    kv = torch.randn((L, B, s, 2, H, D), generator=g, device="cuda").half()
+    q0 = torch.randn((L, B, H, D), generator=g, device="cuda").half()
+    for l in range(L):
+        cache.append_tokens(l, 0, 0, kv[l, :, :, 0].contiguous(), kv[l, :, :, 1].contiguous())
+        cache.prefill_seed(l, s, q0[l].contiguous())
+    tot = [cache.importance(l, s).sum(1) for l in range(L)]
+    for l in range(L):  # seeded importance = H heads of probability mass
+        torch.testing.assert_close(tot[l], torch.full_like(tot[l], H), rtol=1e-5, atol=0)
+    for j in range(steps):
+        n = s + j + 1
+        k = api.swa_window_k(n, 0.2)
+        for l in range(L):
+            q, kn, vn = (torch.randn((B, H, D), generator=g, device="cuda").half() for _ in range(3))
+            out, idx, w = cache.swa_decode_layer(l, n, 0.2, q, kn, vn, return_indices=True, return_weights=True)
+            m = idx.shape[1]
+            assert m == 2 * k
+            assert bool((idx[:, 1:] > idx[:, :-1]).all())                       # ascending, unique
+            assert torch.equal(idx[:, k:], torch.arange(n - k, n, device="cuda", dtype=torch.int32).expand(B, k))
+            assert bool((idx[:, :k] < n - k).all())                             # globals outside window
+            torch.testing.assert_close(w.sum(-1), torch.ones((B, H), device="cuda"), rtol=2e-6, atol=2e-6)
+            imp = cache.importance(l, n).sum(1)
+            torch.testing.assert_close(imp, tot[l] + H, rtol=1e-6, atol=1e-6)  # mass checksum
+            tot[l] = imp
+            # torch fp32 reference from the cache contents and the kernel's own selection
+            kvr = cache.read(l, 0, B, 0, n)  # [B, n, 2, H, D]
+            gi = idx.long()
+            ks = torch.gather(kvr[:, :, 0], 1, gi[:, :, None, None].expand(B, m, H, D))
+            vs = torch.gather(kvr[:, :, 1], 1, gi[:, :, None, None].expand(B, m, H, D))
+            logits = torch.einsum("bhd,bmhd->bhm", q.float(), ks) / np.sqrt(D)
+            p = torch.softmax(logits, -1)
+            ref = torch.einsum("bhm,bmhd->bhd", p, vs)
+            assert_close(out.float().cpu().numpy(), ref.cpu().numpy(), TOL["f16"], "torch fp32 reference")
+            assert_close(w.cpu().numpy(), p.cpu().numpy(), TOL["f16"], "weights")
+    # the selection itself is the oracle's on the device importance
+    n = s + steps + 1
+    imp = cache.importance(0, n - 1).cpu().numpy()
+    sel = api.swa_select(cuda(imp), n, 0.2).all.cpu().numpy()
+    for b in (0, 17, 63):
+        assert np.array_equal(sel[b], port.swa_select(imp[b], n, 0.2)[0])
