@@ -140,6 +140,13 @@ skv_status skv_dequantize(const uint16_t* codes, size_t len, size_t channel_size
                           const double* scales, const int64_t* zero_points, double* out,
                           void* stream);
 
+/* ---- device memory helpers for hosts without the CUDA headers (the C++
+ * mirror include/skv/b200.hpp uses these). skv_copy is cudaMemcpyDefault
+ * (any direction, UVA) on `stream`, then synchronizes that stream. */
+skv_status skv_device_alloc(int device, size_t bytes, void** out);
+skv_status skv_device_free(void* ptr);
+skv_status skv_copy(void* dst, const void* src, size_t bytes, void* stream);
+
 /* ---- measurement hooks (bench.py) ----------------------------------------
  * While enabled, every decode-kernel launch on a cache is bracketed by CUDA
  * events on its own stream; skv_profile_read sums the measured durations. */

@@ -77,6 +77,9 @@ def _declare(lib):
         "skv_top_k_indices": (I, [P, I, I64, I, I, P, P]),
         "skv_quantize": (I, [P, SZ, C.c_uint32, SZ, P, P, P, P]),
         "skv_dequantize": (I, [P, SZ, SZ, P, P, P, P]),
+        "skv_device_alloc": (I, [I, SZ, P]),
+        "skv_device_free": (I, [P]),
+        "skv_copy": (I, [P, P, SZ, P]),
         "skv_profile_enable": (I, [P, I]),
         "skv_profile_read": (I, [P, P, P, P]),
     }

@@ -637,6 +637,31 @@ skv_status skv_dequantize(const uint16_t* codes, size_t len, size_t channel_size
     return SKV_OK;
 }
 
+skv_status skv_device_alloc(int device, size_t bytes, void** out) {
+    SKV_REQUIRE(out != nullptr, "skv_device_alloc: null output");
+    DeviceGuard guard(device);
+    *out = nullptr;
+    if (bytes == 0) return SKV_OK;
+    if (cudaMalloc(out, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(SKV_ERR_OOM, "skv_device_alloc: cannot allocate %llu bytes", static_cast<unsigned long long>(bytes));
+    }
+    return SKV_OK;
+}
+
+skv_status skv_device_free(void* ptr) {
+    if (ptr) SKV_CUDA(cudaFree(ptr));
+    return SKV_OK;
+}
+
+skv_status skv_copy(void* dst, const void* src, size_t bytes, void* stream) {
+    if (bytes == 0) return SKV_OK;
+    SKV_REQUIRE(dst && src, "skv_copy: null pointer");
+    SKV_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, as_stream(stream)));
+    SKV_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    return SKV_OK;
+}
+
 skv_status skv_profile_enable(skv_cache* c, int enable) {
     SKV_REQUIRE(c != nullptr, "null cache");
     DeviceGuard guard(c->d.device);

@@ -1,0 +1,48 @@
+"""Multi-GPU plumbing for the SWA decode path: batch sharding.
+
+Selection is per (sequence, layer) (attention.hpp:235-244), so sequences are
+independent: each rank owns a contiguous slice of the batch and runs the
+decode path on it with no collective. Collectives are used only for
+measurement (max-over-ranks time) and, when a caller wants the whole batch's
+outputs on every rank, one all-gather of the attention outputs.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(global_batch: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous slice [b0, b0 + nb) of `global_batch` sequences for `rank`;
+    the first global_batch % world ranks take one extra sequence."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside world {world}")
+    if global_batch < 0:
+        raise ValueError("negative batch")
+    base, rem = divmod(global_batch, world)
+    b0 = rank * base + min(rank, rem)
+    return b0, base + (1 if rank < rem else 0)
+
+
+def max_over_ranks(value: float, device=None) -> float:
+    """The slowest rank's time: what a multi-GPU step costs."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def gather_batch(local: torch.Tensor, global_batch: int) -> torch.Tensor:
+    """All-gather per-rank [nb, ...] slices (shard_range order) into the
+    global [global_batch, ...] tensor on every rank. Pads uneven shards."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return local
+    world = dist.get_world_size()
+    width = -(-global_batch // world)
+    pad = torch.zeros((width,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad)
+    out = [parts[r][: shard_range(global_batch, world, r)[1]] for r in range(world)]
+    return torch.cat(out, 0)

@@ -1,0 +1,22 @@
+"""The C++ drop-in (include/skv/b200.hpp) against the unmodified reference,
+both called with the reference's own types (tests/cpp/test_shim.cpp). The
+binary is built where /root/reference exists (build()) and travels to the GPU
+box."""
+import os
+import subprocess
+
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+BIN = os.path.join(HERE, "cpp", "build", "test_shim")
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_matches_reference():
+    if not os.path.exists(BIN):
+        if os.path.isdir("/root/reference/proj/include"):
+            subprocess.run(["make", "-s", "-C", os.path.join(HERE, "cpp")], check=True)
+        else:
+            pytest.skip("reference headers absent and no prebuilt tests/cpp/build/test_shim")
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ALL OK" in r.stdout, r.stdout + r.stderr

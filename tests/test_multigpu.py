@@ -1,0 +1,98 @@
+"""Multi-rank host logic (gloo, world size 2, CPU): batch sharding of the SWA
+decode path has no data-path collective -- every rank decodes its own
+sequences -- so the union of the per-rank results must equal the whole-batch
+result, and the timing reduction is a max over ranks. The per-rank compute in
+this CPU test is the oracle (the GPU kernels are covered by the -m gpu tests).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2403_17312_b200.shard import gather_batch, max_over_ranks, shard_range
+
+
+def test_shard_range_partitions():
+    for B in (0, 1, 7, 64, 128, 129):
+        for world in (1, 2, 3, 4, 8):
+            spans = [shard_range(B, world, r) for r in range(world)]
+            assert sum(nb for _, nb in spans) == B
+            pos = 0
+            for b0, nb in spans:
+                assert b0 == pos
+                pos += nb
+            assert max(nb for _, nb in spans) - min(nb for _, nb in spans) <= 1
+    with pytest.raises(ValueError):
+        shard_range(8, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, B, result_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import Oracle
+        from skv_testlib import OracleSeq
+
+        port_ = Oracle("port")
+        H, D, s, steps, r = 2, 128, 40, 4, 0.2
+        rng = np.random.default_rng(5)  # same global data on every rank
+        kv = rng.standard_normal((B, s + steps, 2, H, D))
+        qs = rng.standard_normal((steps + 1, B, H, D))
+        b0, nb = shard_range(B, world, rank)
+        outs = np.zeros((steps, nb, H, D))
+        idxs = []
+        for i, b in enumerate(range(b0, b0 + nb)):
+            seq = OracleSeq(port_, H, D, s + steps)
+            for t in range(s):
+                seq.append(t, kv[b, t, 0], kv[b, t, 1])
+            seq.seed(s, qs[0, b])
+            for j in range(steps):
+                n = s + j + 1
+                seq.append(n - 1, kv[b, n - 1, 0], kv[b, n - 1, 1])
+                attn, _, idx = seq.step(n, r, qs[j + 1, b])
+                outs[j, i] = attn
+                idxs.append(idx)
+        gathered = [gather_batch(torch.from_numpy(outs[j]), B).numpy() for j in range(steps)]
+        slowest = max_over_ranks(1.0 + rank)
+        if rank == 0:
+            np.savez(result_path, out=np.stack(gathered), slowest=slowest)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("B", [4, 5])
+def test_batch_sharded_decode_equals_whole_batch(tmp_path, B, port):
+    from skv_testlib import OracleSeq
+
+    world = 2
+    res = str(tmp_path / "r.npz")
+    mp.start_processes(_worker, args=(world, _free_port(), B, res), nprocs=world, start_method="spawn")
+    got = np.load(res)
+    assert got["slowest"] == 2.0  # max over ranks
+    H, D, s, steps, r = 2, 128, 40, 4, 0.2
+    rng = np.random.default_rng(5)
+    kv = rng.standard_normal((B, s + steps, 2, H, D))
+    qs = rng.standard_normal((steps + 1, B, H, D))
+    for b in range(B):
+        seq = OracleSeq(port, H, D, s + steps)
+        for t in range(s):
+            seq.append(t, kv[b, t, 0], kv[b, t, 1])
+        seq.seed(s, qs[0, b])
+        for j in range(steps):
+            n = s + j + 1
+            seq.append(n - 1, kv[b, n - 1, 0], kv[b, n - 1, 1])
+            attn, _, _ = seq.step(n, r, qs[j + 1, b])
+            assert np.array_equal(got["out"][j, b], attn)
