@@ -193,11 +193,11 @@ def main():
     g = torch.Generator(device="cuda").manual_seed(2403_17312 + args.config * 1000 + rank)
     for l in range(L):
         chunk = max(1, min(B, (1 << 30) // (s * H * D * 2)))
-        for b0 in range(0, B, chunk):
-            nb = min(chunk, B - b0)
+        for c0 in range(0, B, chunk):
+            nb = min(chunk, B - c0)
             kp = torch.randn((nb, s, H, D), generator=g, device="cuda", dtype=qdt)
             vp = torch.randn((nb, s, H, D), generator=g, device="cuda", dtype=qdt)
-            cache.append_tokens(l, b0, 0, kp, vp)
+            cache.append_tokens(l, c0, 0, kp, vp)
             del kp, vp
         cache.prefill_seed(l, s, torch.randn((B, H, D), generator=g, device="cuda", dtype=qdt))
     pool = min(W + K, 8)
