@@ -140,6 +140,35 @@ skv_status skv_dequantize(const uint16_t* codes, size_t len, size_t channel_size
                           const double* scales, const int64_t* zero_points, double* out,
                           void* stream);
 
+/* ---- KV residency bookkeeping for the three-phase schedule ----------------
+ * SchedulePlan (scheduler.hpp:28-39) + the workload lengths step_actions reads
+ * from CostParams (input_len s, output_len n). */
+typedef struct skv_plan {
+    double alpha, beta;
+    int64_t p1, p2;
+    int32_t recompute_enabled;
+    int64_t input_len, output_len;
+} skv_plan;
+/* Attach (or with NULL detach) a plan. While attached, every decode step also
+ * runs step_actions + apply_actions for the NEXT step on the device ledger
+ * right after selecting it (so the lists are ready before that step runs). */
+skv_status skv_cache_set_plan(skv_cache* cache, const skv_plan* plan);
+/* KvLedger tiers per token (memsim.hpp:72): 0 Device, 1 Host, 2 Deleted,
+ * 255 not stored. src/dst: [nb][len] bytes (host or device). skv_cache_write
+ * marks written tokens Device (store_new). */
+skv_status skv_ledger_set(skv_cache* cache, int layer, int b0, int nb, int len, const uint8_t* src, void* stream);
+skv_status skv_ledger_get(const skv_cache* cache, int layer, int b0, int nb, int len, uint8_t* dst, void* stream);
+/* step_actions (scheduler.hpp:320-381) for step j of `layer`, every
+ * sequence, with selection `selected` (device [B][m], ascending; k its
+ * window). apply != 0 also applies them (engine.hpp:686-716). lists_out
+ * (nullable): [B][4][capacity] offload, delete, reload, recompute;
+ * counts_out (nullable): [B][4]. Both any memory; enqueued on `stream`. */
+skv_status skv_step_actions(skv_cache* cache, int layer, int j, const int32_t* selected, int m, int k, int apply,
+                            int32_t* lists_out, int32_t* counts_out, void* stream);
+/* The action lists of the last step_actions run on `layer` (same layout). */
+skv_status skv_last_actions(const skv_cache* cache, int layer, int32_t* lists_out, int32_t* counts_out,
+                            void* stream);
+
 /* ---- device memory helpers for hosts without the CUDA headers (the C++
  * mirror include/skv/b200.hpp uses these). skv_copy is cudaMemcpyDefault
  * (any direction, UVA) on `stream`, then synchronizes that stream. */

@@ -77,6 +77,11 @@ def _declare(lib):
         "skv_top_k_indices": (I, [P, I, I64, I, I, P, P]),
         "skv_quantize": (I, [P, SZ, C.c_uint32, SZ, P, P, P, P]),
         "skv_dequantize": (I, [P, SZ, SZ, P, P, P, P]),
+        "skv_cache_set_plan": (I, [P, P]),
+        "skv_ledger_set": (I, [P, I, I, I, I, P, P]),
+        "skv_ledger_get": (I, [P, I, I, I, I, P, P]),
+        "skv_step_actions": (I, [P, I, I, P, I, I, I, P, P, P]),
+        "skv_last_actions": (I, [P, I, P, P, P]),
         "skv_device_alloc": (I, [I, SZ, P]),
         "skv_device_free": (I, [P]),
         "skv_copy": (I, [P, P, SZ, P]),

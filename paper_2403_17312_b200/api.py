@@ -125,6 +125,11 @@ class _Desc(C.Structure):
                 ("q_dtype", C.c_int32), ("device", C.c_int32), ("out_f32", C.c_int32)]
 
 
+class _Plan(C.Structure):
+    _fields_ = [("alpha", C.c_double), ("beta", C.c_double), ("p1", C.c_int64), ("p2", C.c_int64),
+                ("recompute_enabled", C.c_int32), ("input_len", C.c_int64), ("output_len", C.c_int64)]
+
+
 class SwaCache:
     """Device-resident decode state: the reference's AttentionState
     (attention.hpp:45-86) for `layers` x `batch` sequences, K/V token-major in
@@ -249,6 +254,46 @@ class SwaCache:
         check(lib().skv_attend_over_indices(self._h, layer, n, _ptr(idx), m, _ptr(q), _ptr(out), _ptr(w),
                                             _stream(q)))
         return out, w
+
+    # ---- three-phase schedule bookkeeping (memsim.hpp:77-215, scheduler.hpp:320-381)
+    def set_plan(self, alpha: float, beta: float, p1: int, p2: int, input_len: int, output_len: int,
+                 recompute_enabled: bool = True):
+        pl = _Plan(alpha, beta, p1, p2, int(recompute_enabled), input_len, output_len)
+        check(lib().skv_cache_set_plan(self._h, C.byref(pl)))
+
+    def clear_plan(self):
+        check(lib().skv_cache_set_plan(self._h, None))
+
+    def set_tiers(self, layer: int, tiers: torch.Tensor, b0: int = 0):
+        # tiers: uint8 [nb, len] (0 device, 1 host, 2 deleted, 255 absent)
+        t = tiers.to(device=self.dev, dtype=torch.uint8).contiguous()
+        check(lib().skv_ledger_set(self._h, layer, b0, t.shape[0], t.shape[1], _ptr(t), _stream(t)))
+
+    def tiers(self, layer: int, length: int, b0: int = 0, nb: int | None = None) -> torch.Tensor:
+        nb = self.batch - b0 if nb is None else nb
+        out = torch.empty((nb, length), dtype=torch.uint8, device=self.dev)
+        check(lib().skv_ledger_get(self._h, layer, b0, nb, length, _ptr(out), _stream(out)))
+        return out
+
+    def _lists(self, lists: torch.Tensor, counts: torch.Tensor):
+        names = ("offload", "delete", "reload", "recompute")
+        lists, counts = lists.cpu(), counts.cpu()
+        return [{nm: lists[b, i, :counts[b, i]].tolist() for i, nm in enumerate(names)} for b in range(self.batch)]
+
+    def step_actions(self, layer: int, j: int, selected: torch.Tensor, k: int, apply: bool = True):
+        # step_actions for every sequence; selected: int32 [B, m] ascending
+        sel = selected.to(device=self.dev, dtype=torch.int32).contiguous()
+        lists = torch.empty((self.batch, 4, self.capacity), dtype=torch.int32, device=self.dev)
+        counts = torch.empty((self.batch, 4), dtype=torch.int32, device=self.dev)
+        check(lib().skv_step_actions(self._h, layer, j, _ptr(sel), sel.shape[1], k, int(apply), _ptr(lists),
+                                     _ptr(counts), _stream(sel)))
+        return self._lists(lists, counts)
+
+    def last_actions(self, layer: int):
+        lists = torch.empty((self.batch, 4, self.capacity), dtype=torch.int32, device=self.dev)
+        counts = torch.empty((self.batch, 4), dtype=torch.int32, device=self.dev)
+        check(lib().skv_last_actions(self._h, layer, _ptr(lists), _ptr(counts), _stream(lists)))
+        return self._lists(lists, counts)
 
     # measurement hooks
     def profile(self, enable: bool):

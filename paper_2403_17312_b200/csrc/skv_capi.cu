@@ -94,6 +94,12 @@ struct skv_cache {
     double* imp = nullptr;
     float* wpart = nullptr;  // [L][B][H][Ncap] per-head-group weight sums of the last attend
     int* idx = nullptr;      // [L][B][Ncap] selection (ascending) for the pending step
+    uint8_t* tiers = nullptr;  // [L][B][Ncap] KvLedger tiers: 0 device, 1 host, 2 deleted, 255 absent
+    int* act_lists = nullptr;  // [L][B][4][Ncap] last step_actions lists
+    int* act_counts = nullptr; // [L][B][4]
+    bool has_plan = false;
+    skv_plan plan{};
+    std::vector<long long> ledger_j;  // per layer: last step whose actions were applied (-1: none)
     std::vector<int> pend_n;     // per layer: n the index buffer was selected for (-1: none)
     std::vector<double> pend_r;  // per layer: its ratio
     uint64_t device_bytes = 0;
@@ -164,6 +170,9 @@ skv_status skv_cache_create(const skv_cache_desc* desc, skv_cache** out) {
     const size_t imp_bytes = static_cast<size_t>(d.layers) * d.batch * d.capacity * 8;
     const size_t wpart_bytes = static_cast<size_t>(d.layers) * d.batch * d.heads * d.capacity * 4;
     const size_t cnt_bytes = static_cast<size_t>(d.layers) * d.batch * d.capacity * 4;  // selections
+    const size_t tier_bytes = static_cast<size_t>(d.layers) * d.batch * d.capacity;
+    const size_t list_bytes = static_cast<size_t>(d.layers) * d.batch * 4 * d.capacity * 4;
+    const size_t acnt_bytes = static_cast<size_t>(d.layers) * d.batch * 4 * 4;
     auto alloc = [&](void** p, size_t bytes) -> bool {
         if (bytes == 0) return true;
         if (cudaMalloc(p, bytes) != cudaSuccess) {
@@ -177,15 +186,22 @@ skv_status skv_cache_create(const skv_cache_desc* desc, skv_cache** out) {
         !alloc(reinterpret_cast<void**>(&c->meta), meta_bytes) ||
         !alloc(reinterpret_cast<void**>(&c->imp), imp_bytes) ||
         !alloc(reinterpret_cast<void**>(&c->wpart), wpart_bytes) ||
-        !alloc(reinterpret_cast<void**>(&c->idx), cnt_bytes)) {
-        const uint64_t want = kv_bytes + meta_bytes + imp_bytes + wpart_bytes + cnt_bytes;
+        !alloc(reinterpret_cast<void**>(&c->idx), cnt_bytes) ||
+        !alloc(reinterpret_cast<void**>(&c->tiers), tier_bytes) ||
+        !alloc(reinterpret_cast<void**>(&c->act_lists), list_bytes) ||
+        !alloc(reinterpret_cast<void**>(&c->act_counts), acnt_bytes)) {
+        const uint64_t want = kv_bytes + meta_bytes + imp_bytes + wpart_bytes + cnt_bytes + tier_bytes + list_bytes +
+                              acnt_bytes;
         skv_cache_destroy(c);
         return fail(SKV_ERR_OOM, "skv_cache_create: cannot allocate %llu device bytes",
                     static_cast<unsigned long long>(want));
     }
     SKV_CUDA(cudaMemset(c->imp, 0, imp_bytes));
+    SKV_CUDA(cudaMemset(c->tiers, 0xFF, tier_bytes));
+    SKV_CUDA(cudaMemset(c->act_counts, 0, acnt_bytes));
     c->pend_n.assign(d.layers, -1);
     c->pend_r.assign(d.layers, 0.0);
+    c->ledger_j.assign(d.layers, -1);
     if (meta_bytes) SKV_CUDA(cudaMemset(c->meta, 0, meta_bytes));
     SKV_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, d.device));
     SKV_CUDA(cudaDeviceGetAttribute(&c->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, d.device));
@@ -201,6 +217,9 @@ skv_status skv_cache_destroy(skv_cache* c) {
     cudaFree(c->imp);
     cudaFree(c->wpart);
     cudaFree(c->idx);
+    cudaFree(c->tiers);
+    cudaFree(c->act_lists);
+    cudaFree(c->act_counts);
     cudaFree(c->stage);
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -231,7 +250,7 @@ skv_status skv_cache_write(skv_cache* c, int layer, int b0, int nb, int t0, int 
     const size_t lt = static_cast<size_t>(layer) * c->d.batch * c->d.capacity;
     c->pend_n[layer] = -1;
     SKV_CUDA(launch_cache_write(c->d.kv_dtype, c->d.q_dtype, c->kv + layer * c->layer_bytes,
-                                c->meta ? c->meta + lt * 2 * c->d.heads : nullptr, c->imp + lt, k, v,
+                                c->meta ? c->meta + lt * 2 * c->d.heads : nullptr, c->imp + lt, c->tiers + lt, k, v,
                                 c->d.heads, c->d.capacity, b0, nb, t0, nt, as_stream(stream)));
     return SKV_OK;
 }
@@ -445,6 +464,41 @@ skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok
     return SKV_OK;
 }
 
+// phase_of_step (scheduler.hpp:52-60)
+int phase_of(const skv_plan& pl, long long j) {
+    if (j < pl.p1) return 1;
+    if (j < pl.p2 || !pl.recompute_enabled) return 2;
+    return 3;
+}
+
+// step_actions + apply_actions for step j of one layer on the device ledger,
+// with the given (ascending) selection.
+skv_status launch_ledger_c(skv_cache* c, int layer, long long j, const int* sel, long long sel_ld, int m, int k,
+                           bool apply, bool store_current, bool pdl, cudaStream_t st) {
+    const skv_plan& pl = c->plan;
+    skvd::LedgerParams p{};
+    const size_t lt = static_cast<size_t>(layer) * c->d.batch * c->d.capacity;
+    p.tiers = c->tiers + lt;
+    p.tier_ld = c->d.capacity;
+    p.sel = sel;
+    p.sel_ld = sel_ld;
+    p.m = m;
+    p.k = k;
+    p.existing = static_cast<int>(pl.input_len + j);
+    p.phase = phase_of(pl, j);
+    p.target = static_cast<long long>(std::ceil(pl.alpha * static_cast<double>(p.existing)));
+    p.beta = pl.beta;
+    p.lists = c->act_lists + lt * 4;
+    p.list_ld = c->d.capacity;
+    p.counts = c->act_counts + static_cast<size_t>(layer) * c->d.batch * 4;
+    p.apply = apply ? 1 : 0;
+    p.store_current = store_current ? 1 : 0;
+    SKV_REQUIRE(p.existing < c->d.capacity, "step_actions: step beyond the cache capacity");
+    SKV_CUDA(launch_ledger(p, c->d.batch, pdl, st));
+    if (apply) c->ledger_j[layer] = j;
+    return SKV_OK;
+}
+
 // One layer of one decode step: [select if no matching pending selection] ->
 // attend (append + gather + softmax + PV) -> select kernel (fold weights into
 // the importance, select for n+1 with the same ratio).
@@ -457,12 +511,33 @@ skv_status decode_layer_impl(skv_cache* c, int layer, int n, double r, const voi
     if (!(c->pend_n[layer] == n && c->pend_r[layer] == r)) {
         if (skv_status e = launch_select_c(c, layer, 0, nullptr, 0, 0, 0, -1, n, r, false, st)) return e;
         fresh = true;
+        if (c->has_plan) {  // this step's bookkeeping (normally done right after the previous step)
+            const long long j = static_cast<long long>(n) - 1 - c->plan.input_len;
+            if (j >= 0 && j < c->plan.output_len && c->ledger_j[layer] != j)
+                if (skv_status e = launch_ledger_c(c, layer, j, layer_idx(c, layer), c->d.capacity, s.m, s.k, true,
+                                                   true, false, st))
+                    return e;
+        }
     }
     int G = 0;
     if (skv_status e = launch_attend_c(c, layer, n, s.m, layer_idx(c, layer), c->d.capacity, true, q, k_new, v_new,
                                        out, idx_out, w_out, chained && !fresh, st, &G))
         return e;
-    return launch_select_c(c, layer, 1, layer_idx(c, layer), c->d.capacity, s.m, G, n - 1, n + 1, r, !c->prof, st);
+    if (skv_status e = launch_select_c(c, layer, 1, layer_idx(c, layer), c->d.capacity, s.m, G, n - 1, n + 1, r,
+                                       !c->prof, st))
+        return e;
+    if (c->has_plan && c->pend_n[layer] == n + 1) {
+        // the next step's KV residency actions (scheduler.hpp:320-381) on the
+        // device ledger, from the selection just made, then its store_new
+        const long long j_next = static_cast<long long>(n) - c->plan.input_len;
+        if (j_next >= 0 && j_next < c->plan.output_len) {
+            StepShape sn;
+            if (skv_status e = step_shape(c, n + 1, r, &sn)) return e;
+            return launch_ledger_c(c, layer, j_next, layer_idx(c, layer), c->d.capacity, sn.m, sn.k, true, true,
+                                   !c->prof, st);
+        }
+    }
+    return SKV_OK;
 }
 
 }  // namespace
@@ -634,6 +709,79 @@ skv_status skv_dequantize(const uint16_t* codes, size_t len, size_t channel_size
     SKV_REQUIRE(codes && scales && zero_points && out, "dequantize: null argument");
     SKV_CUDA(launch_dequantize(codes, static_cast<long long>(len), static_cast<long long>(channel_size), scales,
                                reinterpret_cast<const long long*>(zero_points), out, as_stream(stream)));
+    return SKV_OK;
+}
+
+skv_status skv_cache_set_plan(skv_cache* c, const skv_plan* plan) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    if (plan == nullptr) {
+        c->has_plan = false;
+        return SKV_OK;
+    }
+    // validate_plan (scheduler.hpp:26-35)
+    const skv_plan& p = *plan;
+    SKV_REQUIRE(p.input_len >= 0 && p.output_len >= 0, "plan: negative workload");
+    if (p.p1 == p.p2) {
+        SKV_REQUIRE(p.p1 == p.output_len, "plan: degenerate plans must have p1 == p2 == n");
+    } else {
+        SKV_REQUIRE(p.p1 < p.p2 && p.p2 <= p.output_len, "plan: requires 0 <= p1 < p2 <= n");
+        SKV_REQUIRE(p.alpha > 0.0 && p.alpha < 1.0, "plan: alpha out of (0,1)");
+        SKV_REQUIRE(p.beta > 0.0 && p.beta < 1.0, "plan: beta out of (0,1)");
+    }
+    c->plan = p;
+    c->has_plan = true;
+    for (auto& j : c->ledger_j) j = -1;
+    return SKV_OK;
+}
+
+skv_status skv_ledger_set(skv_cache* c, int layer, int b0, int nb, int len, const uint8_t* src, void* stream) {
+    if (skv_status s = check_block(c, layer, b0, nb, 0, len)) return s;
+    DeviceGuard guard(c->d.device);
+    uint8_t* dst = c->tiers + (static_cast<size_t>(layer) * c->d.batch + b0) * c->d.capacity;
+    SKV_CUDA(cudaMemcpy2DAsync(dst, c->d.capacity, src, len, len, nb, cudaMemcpyDefault, as_stream(stream)));
+    return SKV_OK;
+}
+
+skv_status skv_ledger_get(const skv_cache* c, int layer, int b0, int nb, int len, uint8_t* dst, void* stream) {
+    if (skv_status s = check_block(c, layer, b0, nb, 0, len)) return s;
+    DeviceGuard guard(c->d.device);
+    const uint8_t* src = c->tiers + (static_cast<size_t>(layer) * c->d.batch + b0) * c->d.capacity;
+    SKV_CUDA(cudaMemcpy2DAsync(dst, len, src, c->d.capacity, len, nb, cudaMemcpyDefault, as_stream(stream)));
+    return SKV_OK;
+}
+
+skv_status skv_step_actions(skv_cache* c, int layer, int j, const int32_t* selected, int m, int k, int apply,
+                            int32_t* lists_out, int32_t* counts_out, void* stream) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    SKV_REQUIRE(c->has_plan, "step_actions: no plan attached (skv_cache_set_plan)");
+    SKV_REQUIRE(layer >= 0 && layer < c->d.layers, "KvLedger: layer out of range");
+    SKV_REQUIRE(j >= 0 && j < c->plan.output_len, "step_actions: step beyond output length");
+    SKV_REQUIRE(selected != nullptr && m >= 0 && k >= 1, "step_actions: bad selection");
+    DeviceGuard guard(c->d.device);
+    const cudaStream_t st = as_stream(stream);
+    if (skv_status e = launch_ledger_c(c, layer, j, selected, m, m, k, apply != 0, false, false, st)) return e;
+    const size_t lt = static_cast<size_t>(layer) * c->d.batch;
+    if (lists_out)
+        SKV_CUDA(cudaMemcpyAsync(lists_out, c->act_lists + lt * 4 * c->d.capacity,
+                                 static_cast<size_t>(c->d.batch) * 4 * c->d.capacity * 4, cudaMemcpyDefault, st));
+    if (counts_out)
+        SKV_CUDA(cudaMemcpyAsync(counts_out, c->act_counts + lt * 4, static_cast<size_t>(c->d.batch) * 16,
+                                 cudaMemcpyDefault, st));
+    return SKV_OK;
+}
+
+skv_status skv_last_actions(const skv_cache* c, int layer, int32_t* lists_out, int32_t* counts_out, void* stream) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    SKV_REQUIRE(layer >= 0 && layer < c->d.layers, "KvLedger: layer out of range");
+    DeviceGuard guard(c->d.device);
+    const cudaStream_t st = as_stream(stream);
+    const size_t lt = static_cast<size_t>(layer) * c->d.batch;
+    if (lists_out)
+        SKV_CUDA(cudaMemcpyAsync(lists_out, c->act_lists + lt * 4 * c->d.capacity,
+                                 static_cast<size_t>(c->d.batch) * 4 * c->d.capacity * 4, cudaMemcpyDefault, st));
+    if (counts_out)
+        SKV_CUDA(cudaMemcpyAsync(counts_out, c->act_counts + lt * 4, static_cast<size_t>(c->d.batch) * 16,
+                                 cudaMemcpyDefault, st));
     return SKV_OK;
 }
 

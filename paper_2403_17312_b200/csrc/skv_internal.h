@@ -9,12 +9,14 @@
 #include "skv_b200.h"
 #include "skv_decode.cuh"
 #include "skv_select.cuh"
+#include "skv_ledger.cuh"
 
 namespace skv_impl {
 
 void count_launch();
 
 cudaError_t launch_select(const skvd::SelectParams& p, int batch, bool pdl, cudaStream_t st);
+cudaError_t launch_ledger(const skvd::LedgerParams& p, int batch, bool pdl, cudaStream_t st);
 cudaError_t launch_top_k(const double* v, int batch, long long ld, int len, int k, int* out,
                          cudaStream_t st);
 cudaError_t launch_quantize(const double* x, long long len, long long cs, uint32_t bits,
@@ -23,7 +25,7 @@ cudaError_t launch_dequantize(const uint16_t* codes, long long len, long long cs
                               const double* scales, const long long* zps, double* out,
                               cudaStream_t st);
 cudaError_t launch_cache_write(int kv_dtype, int q_dtype, uint8_t* kv, float2* meta, double* imp,
-                               const void* k, const void* v, int H, int Ncap, int b0, int nb,
+                               uint8_t* tiers, const void* k, const void* v, int H, int Ncap, int b0, int nb,
                                int t0, int nt, cudaStream_t st);
 cudaError_t launch_cache_read(int kv_dtype, const uint8_t* kv, const float2* meta, float* out,
                               int H, int Ncap, int b0, int nb, int t0, int nt, cudaStream_t st);

@@ -3,11 +3,155 @@
 // cache writes (append with fake-quant) and reads.
 #include "skv_internal.h"
 #include "skv_select.cuh"
+#include "skv_ledger.cuh"
 
 namespace skvd {
 
 // ---------------------------------------------------------------- selection
 constexpr int kSelThreads = 512;
+
+
+// ------------------------------------------------------------------- ledger
+// Block-wide exclusive sum-scan of a u64; *total gets the block total.
+template <int NT>
+__device__ __forceinline__ uint64_t block_excl_scan(uint64_t v, uint64_t* warp_tot, uint64_t* total, int tid) {
+    const int lane = tid & 31, warp = tid >> 5;
+    const uint64_t inc = warp_incl_scan_u64(v, lane);
+    if (lane == 31) warp_tot[warp] = inc;
+    __syncthreads();
+    uint64_t base = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) {
+        base += w < warp ? warp_tot[w] : 0;
+        tot += warp_tot[w];
+    }
+    __syncthreads();
+    *total = tot;
+    return base + inc - v;
+}
+
+// step_actions (scheduler.hpp:320-381) + apply_actions (engine.hpp:686-716)
+// for one layer, one CTA per sequence. See skv_ledger.cuh.
+__global__ void __launch_bounds__(kLedgerThreads) ledger_step_kernel(const LedgerParams p) {
+    constexpr int NT = kLedgerThreads;
+    constexpr uint64_t M21 = (1ull << 21) - 1;
+    __shared__ uint64_t wt[NT / 32];
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int b = blockIdx.x, tid = threadIdx.x;
+    pdl_launch_dependents();
+    pdl_wait();  // the selection comes from the preceding select kernel
+    const int ntok = p.existing;
+    uint8_t* tg = p.tiers + static_cast<size_t>(b) * p.tier_ld;
+    int* lists = p.lists + static_cast<size_t>(b) * 4 * p.list_ld;
+    int* cnt = p.counts + static_cast<size_t>(b) * 4;
+    if (p.phase == 1) {
+        if (tid < 4) cnt[tid] = 0;
+        if (tid == 0 && p.store_current) tg[ntok] = kTierDevice;
+        return;
+    }
+    uint8_t* t8 = smem;          // pre-action tiers [ntok]
+    uint8_t* act = smem + ntok;  // bit0 offload, bit1 delete, bit2 reload/recompute
+    for (int i = tid; i < ntok; i += NT) {
+        t8[i] = tg[i];
+        act[i] = 0;
+    }
+    __syncthreads();
+    const int n_tot = ntok + 1;
+    const int nonlocal = n_tot > p.k ? n_tot - p.k : 0;
+    const int per = (ntok + NT - 1) / NT;
+    const int beg = min(tid * per, ntok), end = min(beg + per, ntok);
+
+    // device / host counts and device-before-window count, packed 3 x 21 bits
+    uint64_t dv = 0, hs = 0, dnl = 0;
+    for (int i = beg; i < end; ++i) {
+        dv += t8[i] == kTierDevice;
+        hs += t8[i] == kTierHost;
+        dnl += (t8[i] == kTierDevice) && i < nonlocal;
+    }
+    uint64_t tot;
+    const uint64_t ex = block_excl_scan<NT>((dv << 42) | (hs << 21) | dnl, wt, &tot, tid);
+    const long long nh = static_cast<long long>((tot >> 21) & M21);
+    const long long ndnl = static_cast<long long>(tot & M21);
+    const long long to_off = p.target > nh ? p.target - nh : 0;
+    const long long n_off = to_off < ndnl ? to_off : ndnl;
+    // offload: the oldest to_off device tokens, stopping at the local window
+    long long drank = static_cast<long long>(ex >> 42);
+    for (int i = beg; i < end; ++i) {
+        if (t8[i] != kTierDevice) continue;
+        if (i < nonlocal && drank < to_off) {
+            lists[drank] = i;
+            act[i] |= 1;
+        }
+        ++drank;
+    }
+    __syncthreads();
+    // Phase III: delete the oldest ceil(beta * host_after) of host U offloaded
+    long long n_del = 0;
+    const long long host_after = nh + n_off;
+    if (p.phase == 3 && host_after > 0) {
+        const long long to_del = static_cast<long long>(ceil(p.beta * static_cast<double>(host_after)));
+        uint64_t hc = 0;
+        for (int i = beg; i < end; ++i) hc += (t8[i] == kTierHost) || (act[i] & 1);
+        uint64_t htot;
+        long long hrank = static_cast<long long>(block_excl_scan<NT>(hc, wt, &htot, tid));
+        for (int i = beg; i < end; ++i) {
+            if (!((t8[i] == kTierHost) || (act[i] & 1))) continue;
+            if (hrank < to_del) {
+                lists[p.list_ld + hrank] = i;
+                act[i] |= 2;
+            }
+            ++hrank;
+        }
+        n_del = to_del < host_after ? to_del : host_after;
+        __syncthreads();
+    }
+    // selected tokens: reload (host or just offloaded) / recompute (deleted)
+    const int* sel = p.sel + static_cast<size_t>(b) * p.sel_ld;
+    const int sper = (p.m + NT - 1) / NT;
+    const int sbeg = min(tid * sper, p.m), send = min(sbeg + sper, p.m);
+    uint64_t rl = 0, rc = 0;
+    for (int q = sbeg; q < send; ++q) {
+        const int t = sel[q];
+        if (t < 0 || t >= ntok || t8[t] == kTierAbsent) continue;  // the current token
+        const bool rec = (act[t] & 2) || t8[t] == kTierDeleted;
+        rc += rec;
+        rl += !rec && (t8[t] == kTierHost || (act[t] & 1));
+    }
+    uint64_t stot;
+    const uint64_t sex = block_excl_scan<NT>((rl << 32) | rc, wt, &stot, tid);
+    long long rlr = static_cast<long long>(sex >> 32), rcr = static_cast<long long>(sex & 0xffffffffu);
+    for (int q = sbeg; q < send; ++q) {
+        const int t = sel[q];
+        if (t < 0 || t >= ntok || t8[t] == kTierAbsent) continue;
+        const bool rec = (act[t] & 2) || t8[t] == kTierDeleted;
+        if (rec) {
+            lists[3 * p.list_ld + rcr++] = t;
+            act[t] |= 4;
+        } else if (t8[t] == kTierHost || (act[t] & 1)) {
+            lists[2 * p.list_ld + rlr++] = t;
+            act[t] |= 4;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        cnt[0] = static_cast<int>(n_off);
+        cnt[1] = static_cast<int>(n_del);
+        cnt[2] = static_cast<int>(stot >> 32);
+        cnt[3] = static_cast<int>(stot & 0xffffffffu);
+    }
+    if (p.apply) {
+        for (int i = tid; i < ntok; i += NT) {
+            const uint8_t a = act[i];
+            if (!a) continue;
+            uint8_t t = t8[i];
+            if (a & 1) t = kTierHost;
+            if (a & 2) t = kTierDeleted;
+            if (a & 4) t = kTierDevice;
+            tg[i] = t;
+        }
+        if (tid == 0 && p.store_current) tg[ntok] = kTierDevice;
+    }
+}
 
 // Importance fold + next selection, one CTA per sequence (skv_select.cuh).
 __global__ void __launch_bounds__(kSelectThreads) swa_select_kernel(const SelectParams p) {
@@ -113,7 +257,7 @@ __global__ void dequantize_kernel(const uint16_t* __restrict__ codes, long long 
 // fake-quant). One warp per (b, t, kv, head) row of D elements.
 template <class QT, class KV>
 __global__ void cache_write_kernel(uint8_t* __restrict__ kv, float2* __restrict__ meta,
-                                   double* __restrict__ imp, const QT* __restrict__ k,
+                                   double* __restrict__ imp, uint8_t* __restrict__ tiers, const QT* __restrict__ k,
                                    const QT* __restrict__ v, int H, int Ncap, int b0, int nb, int t0,
                                    int nt) {
     constexpr int D = kHeadDim;
@@ -166,7 +310,10 @@ __global__ void cache_write_kernel(uint8_t* __restrict__ kv, float2* __restrict_
             meta[(tok * 2 + which) * H + h] =
                 make_float2(static_cast<float>(scale), static_cast<float>(-scale * static_cast<double>(zp)));
     }
-    if (lane == 0 && h == 0 && which == 0) imp[tok] = 0.0;
+    if (lane == 0 && h == 0 && which == 0) {
+        imp[tok] = 0.0;
+        if (tiers) tiers[tok] = 0;  // KvLedger::store_new: new KV lands on device
+    }
 }
 
 // Cache read-back to fp32 [nb][nt][2][H][D].
@@ -222,6 +369,26 @@ cudaError_t launch_select(const SelectParams& p, int batch, bool pdl, cudaStream
     return e;
 }
 
+cudaError_t launch_ledger(const LedgerParams& p, int batch, bool pdl, cudaStream_t st) {
+    const size_t smem = static_cast<size_t>(p.existing > 0 ? p.existing : 0) * 2 + 16;
+    cudaError_t e = cudaFuncSetAttribute(ledger_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(batch);
+    cfg.blockDim = dim3(kLedgerThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    e = cudaLaunchKernelEx(&cfg, ledger_step_kernel, p);
+    count_launch();
+    return e;
+}
+
 cudaError_t launch_top_k(const double* v, int batch, long long ld, int len, int k, int* out,
                          cudaStream_t st) {
     const size_t smem = align_up(sizeof(TopkSmem<kSelThreads>), 16) + static_cast<size_t>(len) * 8;
@@ -253,31 +420,31 @@ cudaError_t launch_dequantize(const uint16_t* codes, long long len, long long cs
 }
 
 template <class QT, class KV>
-static cudaError_t write_t(uint8_t* kv, float2* meta, double* imp, const void* k, const void* v, int H,
-                           int Ncap, int b0, int nb, int t0, int nt, cudaStream_t st) {
+static cudaError_t write_t(uint8_t* kv, float2* meta, double* imp, uint8_t* tiers, const void* k, const void* v,
+                           int H, int Ncap, int b0, int nb, int t0, int nt, cudaStream_t st) {
     const long long rows = static_cast<long long>(nb) * nt * 2 * H;
     const int threads = 256;
     const long long blocks = (rows * 32 + threads - 1) / threads;
     cache_write_kernel<QT, KV><<<static_cast<unsigned>(blocks), threads, 0, st>>>(
-        kv, meta, imp, static_cast<const QT*>(k), static_cast<const QT*>(v), H, Ncap, b0, nb, t0, nt);
+        kv, meta, imp, tiers, static_cast<const QT*>(k), static_cast<const QT*>(v), H, Ncap, b0, nb, t0, nt);
     count_launch();
     return cudaGetLastError();
 }
 
 cudaError_t launch_cache_write(int kv_dtype, int q_dtype, uint8_t* kv, float2* meta, double* imp,
-                               const void* k, const void* v, int H, int Ncap, int b0, int nb, int t0,
-                               int nt, cudaStream_t st) {
+                               uint8_t* tiers, const void* k, const void* v, int H, int Ncap, int b0, int nb,
+                               int t0, int nt, cudaStream_t st) {
     switch (kv_dtype) {
     case SKV_F32:
-        return write_t<float, KvF32>(kv, meta, imp, k, v, H, Ncap, b0, nb, t0, nt, st);
+        return write_t<float, KvF32>(kv, meta, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
     case SKV_F16:
-        return write_t<__half, KvF16>(kv, meta, imp, k, v, H, Ncap, b0, nb, t0, nt, st);
+        return write_t<__half, KvF16>(kv, meta, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
     case SKV_BF16:
-        return write_t<__nv_bfloat16, KvBF16>(kv, meta, imp, k, v, H, Ncap, b0, nb, t0, nt, st);
+        return write_t<__nv_bfloat16, KvBF16>(kv, meta, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
     case SKV_U8:
-        if (q_dtype == SKV_F32) return write_t<float, KvU8>(kv, meta, imp, k, v, H, Ncap, b0, nb, t0, nt, st);
-        if (q_dtype == SKV_F16) return write_t<__half, KvU8>(kv, meta, imp, k, v, H, Ncap, b0, nb, t0, nt, st);
-        return write_t<__nv_bfloat16, KvU8>(kv, meta, imp, k, v, H, Ncap, b0, nb, t0, nt, st);
+        if (q_dtype == SKV_F32) return write_t<float, KvU8>(kv, meta, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
+        if (q_dtype == SKV_F16) return write_t<__half, KvU8>(kv, meta, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
+        return write_t<__nv_bfloat16, KvU8>(kv, meta, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
     }
     return cudaErrorInvalidValue;
 }
