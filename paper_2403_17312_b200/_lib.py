@@ -15,7 +15,7 @@ import threading
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-SO_PATH = os.path.join(PKG, "libskv_b200.so")
+SO_PATH = os.environ.get("SKV_LIB") or os.path.join(PKG, "libskv_b200.so")
 
 _lock = threading.Lock()
 _lib = None

@@ -158,15 +158,17 @@ skv_status skv_cache_create(const skv_cache_desc* desc, skv_cache** out) {
     if (!ok_pair || dtype_size(d.kv_dtype) == 0)
         return fail(SKV_ERR_UNSUPPORTED, "skv_cache_create: kv_dtype %d with q_dtype %d", d.kv_dtype,
                     d.q_dtype);
+    if (d.kv_dtype == SKV_U8 && d.heads % 2 != 0)
+        return fail(SKV_ERR_UNSUPPORTED, "skv_cache_create: INT8 rows need an even head count (%d)", d.heads);
     DeviceGuard guard(d.device);
     skv_cache* c = new skv_cache();
     c->d = d;
-    c->row_bytes = static_cast<size_t>(d.head_dim) * dtype_size(d.kv_dtype);
+    // one stored head row; INT8 rows carry their (scale, bias) pair inline
+    c->row_bytes = static_cast<size_t>(d.head_dim) * dtype_size(d.kv_dtype) + (d.kv_dtype == SKV_U8 ? 8 : 0);
     c->tok_bytes = 2 * static_cast<size_t>(d.heads) * c->row_bytes;
     c->layer_bytes = static_cast<size_t>(d.batch) * d.capacity * c->tok_bytes;
     const size_t kv_bytes = c->layer_bytes * d.layers;
-    const size_t meta_bytes =
-        d.kv_dtype == SKV_U8 ? static_cast<size_t>(d.layers) * d.batch * d.capacity * 2 * d.heads * 8 : 0;
+    const size_t meta_bytes = 0;  // inline in the INT8 rows
     const size_t imp_bytes = static_cast<size_t>(d.layers) * d.batch * d.capacity * 8;
     const size_t wpart_bytes = static_cast<size_t>(d.layers) * d.batch * d.heads * d.capacity * 4;
     const size_t cnt_bytes = static_cast<size_t>(d.layers) * d.batch * d.capacity * 4;  // selections
@@ -249,8 +251,8 @@ skv_status skv_cache_write(skv_cache* c, int layer, int b0, int nb, int t0, int 
     DeviceGuard guard(c->d.device);
     const size_t lt = static_cast<size_t>(layer) * c->d.batch * c->d.capacity;
     c->pend_n[layer] = -1;
-    SKV_CUDA(launch_cache_write(c->d.kv_dtype, c->d.q_dtype, c->kv + layer * c->layer_bytes,
-                                c->meta ? c->meta + lt * 2 * c->d.heads : nullptr, c->imp + lt, c->tiers + lt, k, v,
+    SKV_CUDA(launch_cache_write(c->d.kv_dtype, c->d.q_dtype, c->kv + layer * c->layer_bytes, c->imp + lt,
+                                c->tiers + lt, k, v,
                                 c->d.heads, c->d.capacity, b0, nb, t0, nt, as_stream(stream)));
     return SKV_OK;
 }
@@ -261,8 +263,8 @@ skv_status skv_cache_read(const skv_cache* c, int layer, int b0, int nb, int t0,
     SKV_REQUIRE(out != nullptr, "skv_cache_read: null output");
     DeviceGuard guard(c->d.device);
     const size_t lt = static_cast<size_t>(layer) * c->d.batch * c->d.capacity;
-    SKV_CUDA(launch_cache_read(c->d.kv_dtype, c->kv + layer * c->layer_bytes,
-                               c->meta ? c->meta + lt * 2 * c->d.heads : nullptr, out, c->d.heads,
+    (void)lt;
+    SKV_CUDA(launch_cache_read(c->d.kv_dtype, c->kv + layer * c->layer_bytes, out, c->d.heads,
                                c->d.capacity, b0, nb, t0, nt, as_stream(stream)));
     return SKV_OK;
 }
@@ -414,8 +416,6 @@ skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok
     skvd::AttendParams p{};
     p.kv = c->kv + layer * c->layer_bytes;
     p.kv_w = c->kv + layer * c->layer_bytes;
-    p.meta = c->meta ? c->meta + lt * 2 * c->d.heads : nullptr;
-    p.meta_w = const_cast<float2*>(p.meta);
     p.q = q;
     p.k_new = k_new;
     p.v_new = v_new;

@@ -35,15 +35,23 @@ namespace skvd {
 constexpr int kHeadDim = 128;
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumerThreads = kConsumerWarps * 32;
-constexpr int kDecodeThreads = kConsumerThreads + 32;
+// Bulk-copy issue is serial per warp (ELECT + R2UR + UBLKCP per copy), so the
+// gather is issued by one producer warp per SM sub-partition.
+constexpr int kProducerWarps = 4;
+constexpr int kDecodeThreads = kConsumerThreads + kProducerWarps * 32;
 constexpr int kBarConsumers = 1;  // named barrier: consumer warps only
 constexpr int kBarAppend = 2;     // named barrier: consumers arrive, producer syncs
 
+// Bytes of one stored head row: D elements, plus the inline (scale, bias)
+// pair for INT8 rows.
+template <class KV>
+__host__ __device__ constexpr int kv_row_bytes() {
+    return kHeadDim * KV::E + (KV::QUANT ? 8 : 0);
+}
+
 struct AttendParams {
-    const uint8_t* kv;   // layer base [B][Ncap][2][H][D] elements of KV::T
+    const uint8_t* kv;   // layer base [B][Ncap][2][H] rows of ROWE bytes (D elements [+ meta])
     uint8_t* kv_w;       // same storage (the append)
-    const float2* meta;  // layer base [B][Ncap][2][H] (scale, bias) when quantized
-    float2* meta_w;
     const void* q;       // [B][H][D] compute dtype
     const void* k_new;   // [B][H][D] (append mode)
     const void* v_new;   // [B][H][D]
@@ -68,7 +76,8 @@ struct DecodeCfg {
     static constexpr int LR = D / VE;    // lanes per head row
     static constexpr int RPW = 32 / LR;  // row groups per warp
     static constexpr int SLOTS = kConsumerWarps * RPW;
-    static constexpr int ROWE = D * E;   // bytes per head row
+    static constexpr int META = QUANT ? 8 : 0;  // INT8 rows carry (scale, bias) inline
+    static constexpr int ROWE = D * E + META;   // bytes per head row
     static constexpr int ROWB = HG * ROWE;
     static constexpr int TMIN = SLOTS / HG > 0 ? SLOTS / HG : 1;  // tokens per stage for RS = 1
     static constexpr int T0 = SKV_STAGE_BYTES / ROWB > 32 ? 32 : SKV_STAGE_BYTES / ROWB;
@@ -76,16 +85,15 @@ struct DecodeCfg {
     static constexpr int RS = T * HG / SLOTS;  // rows per slot per stage
     static constexpr int S = SKV_STAGES;
     static constexpr int STAGEB = T * ROWB;
-    static constexpr int METAB = QUANT ? T * HG * 8 : 0;
     static_assert(SLOTS % HG == 0, "head group must tile the consumer slots");
     static_assert(T * HG % SLOTS == 0 && RS >= 1 && RS <= LR, "stage rows must tile the slots");
     static_assert(T <= 32, "one producer lane per token row");
-    static_assert(!QUANT || HG >= 2, "quantized rows need >= 16-byte meta copies");
+    static_assert(!QUANT || HG % 2 == 0, "136-byte INT8 rows: an even head group keeps copies 16-byte sized");
     static_assert(SLOTS * D * 4 <= S * STAGEB, "reduction scratch aliases the ring");
 };
 
 struct DecodeSmem {
-    size_t ring, meta, bars, tok, wts, flag, total;
+    size_t ring, bars, tok, wts, flag, total;
 };
 
 // Shared-memory carve-up; identical on host (launch size) and device.
@@ -95,9 +103,7 @@ __host__ __device__ inline DecodeSmem decode_smem(int m) {
     DecodeSmem s;
     size_t o = 0;
     s.ring = o;
-    o += static_cast<size_t>(C::S) * C::STAGEB;
-    s.meta = o;
-    o = align_up(o + static_cast<size_t>(C::S) * C::METAB, 16);
+    o = align_up(o + static_cast<size_t>(C::S) * C::STAGEB, 16);
     s.bars = o;
     o += 2 * C::S * 8;
     s.tok = o;
@@ -145,7 +151,7 @@ __global__ void __launch_bounds__(kDecodeThreads)
     using C = DecodeCfg<KV, HG>;
     constexpr int D = C::D, VE = C::VE, V2 = C::V2, LR = C::LR, RPW = C::RPW, SLOTS = C::SLOTS;
     constexpr int ROWE = C::ROWE, ROWB = C::ROWB, T = C::T, S = C::S, RS = C::RS;
-    constexpr int STAGEB = C::STAGEB, METAB = C::METAB;
+    constexpr int STAGEB = C::STAGEB;
     constexpr bool QUANT = C::QUANT;
 
     extern __shared__ __align__(128) uint8_t smem[];
@@ -155,7 +161,6 @@ __global__ void __launch_bounds__(kDecodeThreads)
     const DecodeSmem L = decode_smem<KV, HG>(m);
 
     uint8_t* ring = smem + L.ring;
-    float2* metaR = reinterpret_cast<float2*>(smem + L.meta);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
     uint64_t* empty = full + S;
     int* tok = reinterpret_cast<int*>(smem + L.tok);
@@ -167,11 +172,10 @@ __global__ void __launch_bounds__(kDecodeThreads)
 
     const size_t TOKB = static_cast<size_t>(2) * H * ROWE;  // bytes per token (K and V planes)
     const uint8_t* kvb = p.kv + static_cast<size_t>(b) * p.Ncap * TOKB + static_cast<size_t>(g) * ROWB;
-    const float2* metab = QUANT ? p.meta + static_cast<size_t>(b) * p.Ncap * 2 * H + g * HG : nullptr;
 
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], kProducerWarps);
             mbar_init(&empty[s], kConsumerWarps);
         }
         fence_barrier_init();
@@ -186,8 +190,11 @@ __global__ void __launch_bounds__(kDecodeThreads)
 
     const int nchunks = (m + T - 1) / T;
 
-    if (warp == kConsumerWarps) {
-        // ================================================== producer warp
+    if (warp >= kConsumerWarps) {
+        // ================================================= producer warps
+        // Producer warp pw issues the rows i = pw, pw + P, ... of every stage
+        // and posts its own byte count on the stage's full barrier.
+        const int pw = warp - kConsumerWarps;
         const uint64_t pol = policy_evict_first();
         // The appended token (position m-1) is copied from the step's input row
         // (non-quantized storage) or, once the consumers have stored its codes,
@@ -205,22 +212,19 @@ __global__ void __launch_bounds__(kDecodeThreads)
             if (u >= S) mbar_wait(&empty[stage], ((u / S) - 1) & 1);
             const bool has_cur = p.append && base + cnt == m;
             if (has_cur && !synced) {
-                if (QUANT) named_sync(kBarAppend, kConsumerThreads + 32);
+                if (QUANT) named_sync(kBarAppend, kDecodeThreads);
                 else if (p.pdl_wait) pdl_wait();
                 synced = true;
             }
-            if (lane == 0) mbar_arrive_expect_tx(&full[stage], cnt * (ROWB + (QUANT ? HG * 8 : 0)));
+            const int mine = cnt > pw ? (cnt - pw + kProducerWarps - 1) / kProducerWarps : 0;
+            if (lane == 0) mbar_arrive_expect_tx(&full[stage], mine * ROWB);
             __syncwarp();
-            if (lane < cnt) {
-                const int t = tok[base + lane];
+            if (lane < mine) {
+                const int i = pw + lane * kProducerWarps;
+                const int t = tok[base + i];
                 const uint8_t* src = kvb + static_cast<size_t>(t) * TOKB + vsel * H * ROWE;
-                if (!QUANT && has_cur && lane == cnt - 1) src = vsel ? vnew : knew;
-                bulk_g2s(ring + stage * STAGEB + lane * ROWB, src, ROWB, &full[stage], pol);
-                if constexpr (QUANT) {
-                    const float2* msrc = metab + static_cast<size_t>(t) * 2 * H + vsel * H;
-                    bulk_g2s(reinterpret_cast<uint8_t*>(metaR) + stage * METAB + lane * HG * 8, msrc,
-                             HG * 8, &full[stage], pol);
-                }
+                if (!QUANT && has_cur && i == cnt - 1) src = vsel ? vnew : knew;
+                bulk_g2s(ring + stage * STAGEB + i * ROWB, src, ROWB, &full[stage], pol);
             }
         }
         return;
@@ -281,13 +285,14 @@ __global__ void __launch_bounds__(kDecodeThreads)
                     c = c < 0 ? 0 : (c > 255 ? 255 : c);
                     packed |= static_cast<uint32_t>(c) << (8 * i);
                 }
-                reinterpret_cast<uint32_t*>(p.kv_w + tok_off + kv * H * ROWE + h * ROWE)[lane] = packed;
+                uint8_t* row = p.kv_w + tok_off + kv * H * ROWE + h * ROWE;
+                reinterpret_cast<uint32_t*>(row)[lane] = packed;
                 if (lane == 0)
-                    p.meta_w[(static_cast<size_t>(b) * p.Ncap + (n - 1)) * 2 * H + kv * H + g * HG + h] =
+                    *reinterpret_cast<float2*>(row + D) =
                         make_float2(static_cast<float>(scale), static_cast<float>(-scale * static_cast<double>(zp)));
             }
             fence_global_to_async();
-            named_arrive(kBarAppend, kConsumerThreads + 32);
+            named_arrive(kBarAppend, kDecodeThreads);
         }
     }
 
@@ -310,6 +315,16 @@ __global__ void __launch_bounds__(kDecodeThreads)
     }
     const uint32_t lane_off = static_cast<uint32_t>(slot * ROWE + c * 16);
     const float scale = p.scale;
+    // 16-byte vector at p; INT8 rows are 136 bytes, so only 8-byte aligned
+    auto ld16 = [](const uint8_t* q) -> uint4 {
+        if constexpr (QUANT) {
+            const uint2 a = *reinterpret_cast<const uint2*>(q);
+            const uint2 bb = *reinterpret_cast<const uint2*>(q + 8);
+            return make_uint4(a.x, a.y, bb.x, bb.y);
+        } else {
+            return *reinterpret_cast<const uint4*>(q);
+        }
+    };
 
     // ---- pass 1: logits = (q . k) * scale  (attention.hpp:204-212)
     for (int u = 0; u < nchunks; ++u) {
@@ -320,7 +335,7 @@ __global__ void __launch_bounds__(kDecodeThreads)
         const uint8_t* st = ring + stage * STAGEB + lane_off;
         uint4 raw[RS];
 #pragma unroll
-        for (int i = 0; i < RS; ++i) raw[i] = *reinterpret_cast<const uint4*>(st + i * SLOTS * ROWE);
+        for (int i = 0; i < RS; ++i) raw[i] = ld16(st + i * SLOTS * ROWE);
         float part[RS];
 #pragma unroll
         for (int i = 0; i < RS; ++i) {
@@ -338,7 +353,7 @@ __global__ void __launch_bounds__(kDecodeThreads)
             const int t = r / HG;
             float logit;
             if constexpr (QUANT) {
-                const float2 ms = metaR[stage * (METAB / 8) + r];
+                const float2 ms = *reinterpret_cast<const float2*>(ring + stage * STAGEB + r * ROWE + D);
                 logit = fmaf(ms.x, dot, ms.y * qsum) * scale;
             } else {
                 logit = dot * scale;
@@ -401,7 +416,7 @@ __global__ void __launch_bounds__(kDecodeThreads)
         if (rows == T * HG) {
             uint4 raw[RS];
 #pragma unroll
-            for (int i = 0; i < RS; ++i) raw[i] = *reinterpret_cast<const uint4*>(st + i * SLOTS * ROWE);
+            for (int i = 0; i < RS; ++i) raw[i] = ld16(st + i * SLOTS * ROWE);
 #pragma unroll
             for (int i = 0; i < RS; ++i) {
                 const int r = slot + i * SLOTS;
@@ -409,7 +424,7 @@ __global__ void __launch_bounds__(kDecodeThreads)
                 float2 vf[V2];
                 cvt16x2(raw[i], vf, KV{});
                 if constexpr (QUANT) {
-                    const float2 ms = metaR[stage * (METAB / 8) + r];
+                    const float2 ms = *reinterpret_cast<const float2*>(ring + stage * STAGEB + r * ROWE + D);
                     const float a = w * ms.x;
                     const float2 a2 = make_float2(a, a);
 #pragma unroll
@@ -428,9 +443,9 @@ __global__ void __launch_bounds__(kDecodeThreads)
                 if (r < rows) {
                     const float w = wh[base + r / HG];
                     float2 vf[V2];
-                    cvt16x2(*reinterpret_cast<const uint4*>(st + i * SLOTS * ROWE), vf, KV{});
+                    cvt16x2(ld16(st + i * SLOTS * ROWE), vf, KV{});
                     if constexpr (QUANT) {
-                        const float2 ms = metaR[stage * (METAB / 8) + r];
+                        const float2 ms = *reinterpret_cast<const float2*>(ring + stage * STAGEB + r * ROWE + D);
                         const float a = w * ms.x;
                         const float2 a2 = make_float2(a, a);
 #pragma unroll

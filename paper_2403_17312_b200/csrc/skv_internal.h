@@ -24,11 +24,11 @@ cudaError_t launch_quantize(const double* x, long long len, long long cs, uint32
 cudaError_t launch_dequantize(const uint16_t* codes, long long len, long long cs,
                               const double* scales, const long long* zps, double* out,
                               cudaStream_t st);
-cudaError_t launch_cache_write(int kv_dtype, int q_dtype, uint8_t* kv, float2* meta, double* imp,
-                               uint8_t* tiers, const void* k, const void* v, int H, int Ncap, int b0, int nb,
-                               int t0, int nt, cudaStream_t st);
-cudaError_t launch_cache_read(int kv_dtype, const uint8_t* kv, const float2* meta, float* out,
-                              int H, int Ncap, int b0, int nb, int t0, int nt, cudaStream_t st);
+cudaError_t launch_cache_write(int kv_dtype, int q_dtype, uint8_t* kv, double* imp, uint8_t* tiers,
+                               const void* k, const void* v, int H, int Ncap, int b0, int nb, int t0, int nt,
+                               cudaStream_t st);
+cudaError_t launch_cache_read(int kv_dtype, const uint8_t* kv, float* out, int H, int Ncap, int b0, int nb,
+                              int t0, int nt, cudaStream_t st);
 
 // Fused decode kernel: one instantiation per (kv dtype, q dtype, HG).
 struct DecodeLaunch {

@@ -256,8 +256,7 @@ __global__ void dequantize_kernel(const uint16_t* __restrict__ codes, long long 
 // AttentionState::append_token for a block of tokens (+ engine head_rows
 // fake-quant). One warp per (b, t, kv, head) row of D elements.
 template <class QT, class KV>
-__global__ void cache_write_kernel(uint8_t* __restrict__ kv, float2* __restrict__ meta,
-                                   double* __restrict__ imp, uint8_t* __restrict__ tiers, const QT* __restrict__ k,
+__global__ void cache_write_kernel(uint8_t* __restrict__ kv, double* __restrict__ imp, uint8_t* __restrict__ tiers, const QT* __restrict__ k,
                                    const QT* __restrict__ v, int H, int Ncap, int b0, int nb, int t0,
                                    int nt) {
     constexpr int D = kHeadDim;
@@ -271,7 +270,7 @@ __global__ void cache_write_kernel(uint8_t* __restrict__ kv, float2* __restrict_
     const int bb = static_cast<int>(row / (2LL * H * nt));
     const QT* src = (which ? v : k) + ((static_cast<size_t>(bb) * nt + t) * H + h) * D;
     const size_t tok = static_cast<size_t>(b0 + bb) * Ncap + (t0 + t);
-    uint8_t* dst = kv + ((tok * 2 + which) * H + h) * static_cast<size_t>(D) * KV::E;
+    uint8_t* dst = kv + ((tok * 2 + which) * H + h) * static_cast<size_t>(kv_row_bytes<KV>());
     if constexpr (!KV::QUANT) {
         using T = typename KV::T;
         T* d = reinterpret_cast<T*>(dst);
@@ -307,7 +306,7 @@ __global__ void cache_write_kernel(uint8_t* __restrict__ kv, float2* __restrict_
         }
         reinterpret_cast<uint32_t*>(dst)[lane] = packed;
         if (lane == 0)
-            meta[(tok * 2 + which) * H + h] =
+            *reinterpret_cast<float2*>(dst + D) =
                 make_float2(static_cast<float>(scale), static_cast<float>(-scale * static_cast<double>(zp)));
     }
     if (lane == 0 && h == 0 && which == 0) {
@@ -318,8 +317,7 @@ __global__ void cache_write_kernel(uint8_t* __restrict__ kv, float2* __restrict_
 
 // Cache read-back to fp32 [nb][nt][2][H][D].
 template <class KV>
-__global__ void cache_read_kernel(const uint8_t* __restrict__ kv, const float2* __restrict__ meta,
-                                  float* __restrict__ out, int H, int Ncap, int b0, int nb, int t0,
+__global__ void cache_read_kernel(const uint8_t* __restrict__ kv, float* __restrict__ out, int H, int Ncap, int b0, int nb, int t0,
                                   int nt) {
     constexpr int D = kHeadDim;
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -332,13 +330,13 @@ __global__ void cache_read_kernel(const uint8_t* __restrict__ kv, const float2* 
     const int t = static_cast<int>((r / (2 * H)) % nt);
     const int bb = static_cast<int>(r / (2LL * H * nt));
     const size_t tok = static_cast<size_t>(b0 + bb) * Ncap + (t0 + t);
-    const size_t at = ((tok * 2 + which) * H + h) * D + d;
+    const uint8_t* row = kv + ((tok * 2 + which) * H + h) * static_cast<size_t>(kv_row_bytes<KV>());
     if constexpr (KV::QUANT) {
-        const float2 ms = meta[(tok * 2 + which) * H + h];
-        out[i] = fmaf(ms.x, static_cast<float>(kv[at]), ms.y);
+        const float2 ms = *reinterpret_cast<const float2*>(row + D);
+        out[i] = fmaf(ms.x, static_cast<float>(row[d]), ms.y);
     } else {
         using T = typename KV::T;
-        out[i] = to_f(reinterpret_cast<const T*>(kv)[at]);
+        out[i] = to_f(reinterpret_cast<const T*>(row)[d]);
     }
 }
 
@@ -420,53 +418,53 @@ cudaError_t launch_dequantize(const uint16_t* codes, long long len, long long cs
 }
 
 template <class QT, class KV>
-static cudaError_t write_t(uint8_t* kv, float2* meta, double* imp, uint8_t* tiers, const void* k, const void* v,
+static cudaError_t write_t(uint8_t* kv, double* imp, uint8_t* tiers, const void* k, const void* v,
                            int H, int Ncap, int b0, int nb, int t0, int nt, cudaStream_t st) {
     const long long rows = static_cast<long long>(nb) * nt * 2 * H;
     const int threads = 256;
     const long long blocks = (rows * 32 + threads - 1) / threads;
     cache_write_kernel<QT, KV><<<static_cast<unsigned>(blocks), threads, 0, st>>>(
-        kv, meta, imp, tiers, static_cast<const QT*>(k), static_cast<const QT*>(v), H, Ncap, b0, nb, t0, nt);
+        kv, imp, tiers, static_cast<const QT*>(k), static_cast<const QT*>(v), H, Ncap, b0, nb, t0, nt);
     count_launch();
     return cudaGetLastError();
 }
 
-cudaError_t launch_cache_write(int kv_dtype, int q_dtype, uint8_t* kv, float2* meta, double* imp,
-                               uint8_t* tiers, const void* k, const void* v, int H, int Ncap, int b0, int nb,
-                               int t0, int nt, cudaStream_t st) {
+cudaError_t launch_cache_write(int kv_dtype, int q_dtype, uint8_t* kv, double* imp, uint8_t* tiers,
+                               const void* k, const void* v, int H, int Ncap, int b0, int nb, int t0, int nt,
+                               cudaStream_t st) {
     switch (kv_dtype) {
     case SKV_F32:
-        return write_t<float, KvF32>(kv, meta, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
+        return write_t<float, KvF32>(kv, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
     case SKV_F16:
-        return write_t<__half, KvF16>(kv, meta, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
+        return write_t<__half, KvF16>(kv, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
     case SKV_BF16:
-        return write_t<__nv_bfloat16, KvBF16>(kv, meta, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
+        return write_t<__nv_bfloat16, KvBF16>(kv, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
     case SKV_U8:
-        if (q_dtype == SKV_F32) return write_t<float, KvU8>(kv, meta, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
-        if (q_dtype == SKV_F16) return write_t<__half, KvU8>(kv, meta, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
-        return write_t<__nv_bfloat16, KvU8>(kv, meta, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
+        if (q_dtype == SKV_F32) return write_t<float, KvU8>(kv, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
+        if (q_dtype == SKV_F16) return write_t<__half, KvU8>(kv, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
+        return write_t<__nv_bfloat16, KvU8>(kv, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
     }
     return cudaErrorInvalidValue;
 }
 
 template <class KV>
-static cudaError_t read_t(const uint8_t* kv, const float2* meta, float* out, int H, int Ncap, int b0,
-                          int nb, int t0, int nt, cudaStream_t st) {
+static cudaError_t read_t(const uint8_t* kv, float* out, int H, int Ncap, int b0, int nb, int t0, int nt,
+                          cudaStream_t st) {
     const long long total = static_cast<long long>(nb) * nt * 2 * H * kHeadDim;
     const int threads = 256;
     cache_read_kernel<KV><<<static_cast<unsigned>((total + threads - 1) / threads), threads, 0, st>>>(
-        kv, meta, out, H, Ncap, b0, nb, t0, nt);
+        kv, out, H, Ncap, b0, nb, t0, nt);
     count_launch();
     return cudaGetLastError();
 }
 
-cudaError_t launch_cache_read(int kv_dtype, const uint8_t* kv, const float2* meta, float* out, int H,
-                              int Ncap, int b0, int nb, int t0, int nt, cudaStream_t st) {
+cudaError_t launch_cache_read(int kv_dtype, const uint8_t* kv, float* out, int H, int Ncap, int b0, int nb,
+                              int t0, int nt, cudaStream_t st) {
     switch (kv_dtype) {
-    case SKV_F32: return read_t<KvF32>(kv, meta, out, H, Ncap, b0, nb, t0, nt, st);
-    case SKV_F16: return read_t<KvF16>(kv, meta, out, H, Ncap, b0, nb, t0, nt, st);
-    case SKV_BF16: return read_t<KvBF16>(kv, meta, out, H, Ncap, b0, nb, t0, nt, st);
-    case SKV_U8: return read_t<KvU8>(kv, meta, out, H, Ncap, b0, nb, t0, nt, st);
+    case SKV_F32: return read_t<KvF32>(kv, out, H, Ncap, b0, nb, t0, nt, st);
+    case SKV_F16: return read_t<KvF16>(kv, out, H, Ncap, b0, nb, t0, nt, st);
+    case SKV_BF16: return read_t<KvBF16>(kv, out, H, Ncap, b0, nb, t0, nt, st);
+    case SKV_U8: return read_t<KvU8>(kv, out, H, Ncap, b0, nb, t0, nt, st);
     }
     return cudaErrorInvalidValue;
 }
