@@ -182,6 +182,17 @@ skv_status skv_copy(void* dst, const void* src, size_t bytes, void* stream);
 skv_status skv_profile_enable(skv_cache* cache, int enable);
 skv_status skv_profile_read(skv_cache* cache, double* total_ms, int64_t* launches,
                             uint64_t* algo_bytes);
+/* Steady-state attend timing: `reps` x L attend launches back to back
+ * (chained with programmatic dependent launch, as inside a decode step, no
+ * select kernels) at length n, which must be the pending step of every layer.
+ * Re-appends token n-1 with the given rows; importance is not touched.
+ * *total_ms = event time around the whole chain. */
+skv_status skv_profile_attend_chain(skv_cache* cache, int n, double r, const void* q, const void* k_new,
+                                    const void* v_new, void* out, int reps, double* total_ms, void* stream);
+/* Launch shape of the last attend launch: heads per CTA, CTAs, dynamic shared
+ * memory bytes, resident CTAs per SM. */
+skv_status skv_attend_config(const skv_cache* cache, int32_t* heads_per_cta, int32_t* grid,
+                             int32_t* smem_bytes, int32_t* ctas_per_sm);
 
 #ifdef __cplusplus
 }

@@ -87,6 +87,8 @@ def _declare(lib):
         "skv_copy": (I, [P, P, SZ, P]),
         "skv_profile_enable": (I, [P, I]),
         "skv_profile_read": (I, [P, P, P, P]),
+        "skv_profile_attend_chain": (I, [P, I, D, P, P, P, P, I, P, P]),
+        "skv_attend_config": (I, [P, P, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -299,6 +299,17 @@ class SwaCache:
     def profile(self, enable: bool):
         check(lib().skv_profile_enable(self._h, int(enable)))
 
+    def attend_chain_ms(self, n: int, r: float, q, k_new, v_new, out, reps: int = 3) -> float:
+        ms = C.c_double()
+        check(lib().skv_profile_attend_chain(self._h, n, r, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(out), reps,
+                                             C.byref(ms), _stream(q)))
+        return ms.value
+
+    def attend_config(self) -> dict:
+        v = [C.c_int32() for _ in range(4)]
+        check(lib().skv_attend_config(self._h, *[C.byref(x) for x in v]))
+        return dict(zip(("heads_per_cta", "grid", "smem_bytes", "ctas_per_sm"), (x.value for x in v)))
+
     def profile_read(self):
         ms, n, b = C.c_double(), C.c_int64(), C.c_uint64()
         check(lib().skv_profile_read(self._h, C.byref(ms), C.byref(n), C.byref(b)))

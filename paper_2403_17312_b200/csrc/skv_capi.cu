@@ -114,6 +114,8 @@ struct skv_cache {
     std::vector<cudaEvent_t> ev_pool;
     int64_t attend_launches = 0;
     uint64_t algo_bytes = 0;
+    int last_hg = 0, last_grid = 0, last_occ = 0;
+    size_t last_smem = 0;
 };
 
 static size_t out_size(const skv_cache* c) { return c->d.out_f32 ? 4 : dtype_size(c->d.q_dtype); }
@@ -318,6 +320,7 @@ skv_status pick_attend(skv_cache* c, int m, const DecodeLaunch** dl_out, size_t*
                                       static_cast<int>(smem)));
         int occ = 0;
         SKV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dl->func, skvd::kDecodeThreads, smem));
+        c->last_occ = occ;
         const long long ctas = static_cast<long long>(c->d.batch) * (c->d.heads / hg);
         if (occ > 0 && ctas <= static_cast<long long>(occ) * c->num_sms) break;
     }
@@ -436,6 +439,9 @@ skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok
     p.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d.head_dim)));
     const int grid_g = c->d.heads / dl->hg;
     *G_out = grid_g;
+    c->last_hg = dl->hg;
+    c->last_grid = grid_g * c->d.batch;
+    c->last_smem = smem;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->prof) {
         auto take = [&]() {
@@ -818,6 +824,58 @@ skv_status skv_profile_enable(skv_cache* c, int enable) {
     c->ev.clear();
     c->attend_launches = 0;
     c->algo_bytes = 0;
+    return SKV_OK;
+}
+
+skv_status skv_attend_config(const skv_cache* c, int32_t* heads_per_cta, int32_t* grid, int32_t* smem_bytes,
+                             int32_t* ctas_per_sm) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    if (heads_per_cta) *heads_per_cta = c->last_hg;
+    if (grid) *grid = c->last_grid;
+    if (smem_bytes) *smem_bytes = static_cast<int32_t>(c->last_smem);
+    if (ctas_per_sm) *ctas_per_sm = c->last_occ;
+    return SKV_OK;
+}
+
+skv_status skv_profile_attend_chain(skv_cache* c, int n, double r, const void* q, const void* k_new,
+                                    const void* v_new, void* out, int reps, double* total_ms, void* stream) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    SKV_REQUIRE(reps >= 1 && q && k_new && v_new && out && total_ms, "profile_attend_chain: bad argument");
+    StepShape s;
+    if (skv_status e = step_shape(c, n, r, &s)) return e;
+    for (int l = 0; l < c->d.layers; ++l)
+        SKV_REQUIRE(c->pend_n[l] == n && c->pend_r[l] == r, "profile_attend_chain: no pending selection for n");
+    DeviceGuard guard(c->d.device);
+    const cudaStream_t st = as_stream(stream);
+    const bool prof = c->prof;
+    c->prof = false;
+    const size_t per_layer = static_cast<size_t>(c->d.batch) * c->d.heads * c->d.head_dim * dtype_size(c->d.q_dtype);
+    const size_t per_layer_out = static_cast<size_t>(c->d.batch) * c->d.heads * c->d.head_dim * out_size(c);
+    cudaEvent_t e0, e1;
+    SKV_CUDA(cudaEventCreate(&e0));
+    SKV_CUDA(cudaEventCreate(&e1));
+    SKV_CUDA(cudaEventRecord(e0, st));
+    for (int rep = 0; rep < reps; ++rep)
+        for (int l = 0; l < c->d.layers; ++l) {
+            int G = 0;
+            if (skv_status e = launch_attend_c(c, l, n, s.m, layer_idx(c, l), c->d.capacity, true,
+                                               static_cast<const uint8_t*>(q) + per_layer * l,
+                                               static_cast<const uint8_t*>(k_new) + per_layer * l,
+                                               static_cast<const uint8_t*>(v_new) + per_layer * l,
+                                               static_cast<uint8_t*>(out) + per_layer_out * l, nullptr, nullptr,
+                                               rep + l > 0, st, &G)) {
+                c->prof = prof;
+                return e;
+            }
+        }
+    SKV_CUDA(cudaEventRecord(e1, st));
+    SKV_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    SKV_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    c->prof = prof;
+    *total_ms = ms;
     return SKV_OK;
 }
 
