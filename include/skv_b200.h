@@ -140,6 +140,25 @@ skv_status skv_dequantize(const uint16_t* codes, size_t len, size_t channel_size
                           const double* scales, const int64_t* zero_points, double* out,
                           void* stream);
 
+/* ---- attention variants (AttentionVariant, attention.hpp:15-21) -----------
+ * Engine::variant_selection (engine.hpp:531-569) for the decode entry points:
+ * DENSE = swa_select at r = 1; SWA (default); LOCAL = the last
+ * swa_keep_count(n, r) tokens; STRIDED = every stride-th token phased onto
+ * n-1 (stride 0: ceil(n / swa_keep_count(n, r))). */
+typedef enum skv_variant {
+    SKV_VARIANT_DENSE = 0,
+    SKV_VARIANT_SWA = 1,
+    SKV_VARIANT_LOCAL = 2,
+    SKV_VARIANT_STRIDED = 3
+} skv_variant;
+skv_status skv_cache_set_variant(skv_cache* cache, int variant, int stride);
+/* Selection size m (and its window k) of a step at length n for the cache's
+ * variant: what idx_out / w_out of skv_swa_decode_layer hold. */
+skv_status skv_selection_size(const skv_cache* cache, int n, double r, int32_t* m, int32_t* k);
+/* attention_sparsity(new_aw_row, 0.01) (attention.hpp:275-310) of each
+ * sequence's last decode step of `layer`; dst [nb] fp64 (host or device). */
+skv_status skv_sparsity_get(const skv_cache* cache, int layer, int b0, int nb, double* dst, void* stream);
+
 /* ---- KV residency bookkeeping for the three-phase schedule ----------------
  * SchedulePlan (scheduler.hpp:28-39) + the workload lengths step_actions reads
  * from CostParams (input_len s, output_len n). */

@@ -207,6 +207,41 @@ class Oracle:
                                                _p(aw, _D)))
         return attn, aw
 
+    def local_attention_mask(self, n: int, window: int) -> np.ndarray:
+        f = self._f("local_attention_mask")
+        f.restype = _SZ
+        out = np.zeros(max(n, 1), np.int64)
+        c = f(_SZ(n), _SZ(window), _p(out, _I64))
+        if window < 1:
+            raise ContractViolation("local_attention_mask: window must be >= 1")
+        return out[:c]
+
+    def strided_attention_mask(self, n: int, stride: int) -> np.ndarray:
+        f = self._f("strided_attention_mask")
+        f.restype = _SZ
+        out = np.zeros(max(n, 1), np.int64)
+        c = f(_SZ(n), _SZ(stride), _p(out, _I64))
+        if stride < 1:
+            raise ContractViolation("strided_attention_mask: stride must be >= 1")
+        return out[:c]
+
+    def variant_selection(self, variant: str, n: int, r: float, stride: int = 0):
+        # engine.hpp:531-569 -> (all ascending, k); importance-free variants only
+        if variant == "local":
+            w = self.swa_keep_count(n, r)
+            out = self.local_attention_mask(n, w)
+            return out, out.size
+        if stride == 0:
+            budget = self.swa_keep_count(n, r)
+            stride = max(1, (n + budget - 1) // budget)
+        return self.strided_attention_mask(n, stride), 1
+
+    def attention_sparsity(self, aw, rel: float = 0.01, causal: bool = False) -> float:
+        aw = np.ascontiguousarray(np.atleast_2d(aw), np.float64)
+        f = self._f("attention_sparsity")
+        f.restype = _D
+        return f(_SZ(aw.shape[0]), _SZ(aw.shape[1]), _p(aw, _D), _D(rel), C.c_int(int(causal)))
+
     # ---- quant.hpp ------------------------------------------------------
     def quantize(self, x, bits: int = 8, channel_size: int = 0):
         x = np.ascontiguousarray(x, np.float64)

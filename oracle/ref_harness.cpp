@@ -166,6 +166,36 @@ int ref_swa_attention(size_t H, size_t D, size_t n, size_t ncap, const double* k
     });
 }
 
+// attention.hpp:247-269
+size_t ref_local_attention_mask(size_t n, size_t window, int64_t* out) {
+    size_t c = 0;
+    guarded([&] {
+        const skv::IndexList l = skv::local_attention_mask(n, window);
+        copy_idx(l, out);
+        c = l.size();
+    });
+    return c;
+}
+size_t ref_strided_attention_mask(size_t n, size_t stride, int64_t* out) {
+    size_t c = 0;
+    guarded([&] {
+        const skv::IndexList l = skv::strided_attention_mask(n, stride);
+        copy_idx(l, out);
+        c = l.size();
+    });
+    return c;
+}
+// attention.hpp:275-310
+double ref_attention_sparsity(size_t rows, size_t cols, const double* aw, double rel, int causal) {
+    double r = -1.0;
+    guarded([&] {
+        skv::Matrix m(rows, cols);
+        std::memcpy(m.data.data(), aw, rows * cols * sizeof(double));
+        r = skv::attention_sparsity(m, rel, causal != 0);
+    });
+    return r;
+}
+
 // matrix.hpp:137-158
 int ref_softmax_rows(size_t rows, size_t cols, const double* in, double* out) {
     return guarded([&] {

@@ -260,6 +260,76 @@ int oc_swa_attention(size_t H, size_t D, size_t n, size_t ncap, const double* ke
                                   attn, new_aw_row);
 }
 
+/* ---- attention.hpp:247-256 ----------------------------------------------- */
+size_t oc_local_attention_mask(size_t n, size_t window, int64_t* out) {
+    if (window < 1) {
+        fail(OC_CONTRACT, "local_attention_mask: window must be >= 1");
+        return 0;
+    }
+    const size_t w = window < n ? window : n;
+    size_t c = 0;
+    for (size_t i = n - w; i < n; ++i) out[c++] = (int64_t)i;
+    return c;
+}
+
+/* ---- attention.hpp:258-269 ----------------------------------------------- */
+size_t oc_strided_attention_mask(size_t n, size_t stride, int64_t* out) {
+    if (stride < 1) {
+        fail(OC_CONTRACT, "strided_attention_mask: stride must be >= 1");
+        return 0;
+    }
+    if (n == 0) return 0;
+    const size_t phase = (n - 1) % stride;
+    size_t c = 0;
+    for (size_t i = phase; i < n; i += stride) out[c++] = (int64_t)i;
+    return c;
+}
+
+/* ---- engine.hpp:545-566 (Local = 2, Strided = 3); result = sel.all() ------ */
+size_t oc_variant_selection(int variant, size_t n_tot, double r, size_t stride, int64_t* out, size_t* k_out) {
+    if (variant == 2) {
+        const size_t w = oc_swa_keep_count(n_tot, r);
+        const size_t c = oc_local_attention_mask(n_tot, w, out);
+        if (k_out) *k_out = c;
+        return c;
+    }
+    if (stride == 0) {
+        const size_t budget = oc_swa_keep_count(n_tot, r);
+        stride = (n_tot + budget - 1) / budget;
+        if (stride < 1) stride = 1;
+    }
+    /* local = {n_tot-1}, global = mask minus n_tot-1; all() sorts them back */
+    const size_t c = oc_strided_attention_mask(n_tot, stride, out);
+    if (k_out) *k_out = 1;
+    return c;
+}
+
+/* ---- attention.hpp:275-310 ----------------------------------------------- */
+double oc_attention_sparsity(size_t rows, size_t cols, const double* aw, double rel, int causal) {
+    const long long offset = (long long)cols - (long long)rows;
+    size_t counted = 0, sparse = 0;
+    for (size_t i = 0; i < rows; ++i) {
+        double mx = 0.0;
+        size_t cells = 0;
+        for (size_t j = 0; j < cols; ++j) {
+            if (causal && (long long)j > (long long)i + offset) continue;
+            if (mx < aw[i * cols + j]) mx = aw[i * cols + j];
+            ++cells;
+        }
+        counted += cells;
+        if (mx == 0.0) {
+            sparse += cells;
+            continue;
+        }
+        const double thr = rel * mx;
+        for (size_t j = 0; j < cols; ++j) {
+            if (causal && (long long)j > (long long)i + offset) continue;
+            if (aw[i * cols + j] < thr) ++sparse;
+        }
+    }
+    return counted == 0 ? 0.0 : (double)sparse / (double)counted;
+}
+
 /* ---- matrix.hpp:137-158 -------------------------------------------------- */
 int oc_softmax_rows(size_t rows, size_t cols, const double* in, double* out) {
     if (rows == 0 || cols == 0) return fail(OC_CONTRACT, "softmax_rows: empty matrix");

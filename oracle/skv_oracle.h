@@ -79,6 +79,14 @@ int oc_swa_attention(size_t H, size_t D, size_t n, size_t ncap, const double* ke
                      double r, double* attn, double* new_aw_row, int64_t* idx_out,
                      size_t* m_out);
 
+/* attention.hpp:247-256 / 258-269: index lists of the baseline variants. */
+size_t oc_local_attention_mask(size_t n, size_t window, int64_t* out);
+size_t oc_strided_attention_mask(size_t n, size_t stride, int64_t* out);
+/* engine.hpp:531-569 for Local / Strided (stride 0 = derive from ratio). */
+size_t oc_variant_selection(int variant, size_t n_tot, double r, size_t stride, int64_t* out, size_t* k_out);
+/* attention.hpp:275-310 */
+double oc_attention_sparsity(size_t rows, size_t cols, const double* aw, double rel, int causal);
+
 /* matrix.hpp:137-158 */
 int oc_softmax_rows(size_t rows, size_t cols, const double* in, double* out);
 

@@ -211,7 +211,7 @@ class SwaCache:
         for t in (q, k_new, v_new):
             self._q(t, shp)
         out = torch.empty(q.shape, dtype=self.out_dtype, device=self.dev) if out is None else out
-        m = swa_keep_count(n, r)
+        m = self.selection_size(n, r)[0]
         idx = torch.empty((self.batch, m), dtype=torch.int32, device=self.dev) if return_indices else None
         w = (torch.empty((self.batch, self.heads, m), dtype=torch.float32, device=self.dev)
              if return_weights else None)
@@ -254,6 +254,23 @@ class SwaCache:
         check(lib().skv_attend_over_indices(self._h, layer, n, _ptr(idx), m, _ptr(q), _ptr(out), _ptr(w),
                                             _stream(q)))
         return out, w
+
+    # ---- attention variants (attention.hpp:15-21, engine.hpp:531-569)
+    VARIANTS = {"dense": 0, "swa": 1, "local": 2, "strided": 3}
+
+    def set_variant(self, variant: str = "swa", stride: int = 0):
+        check(lib().skv_cache_set_variant(self._h, self.VARIANTS[variant], stride))
+
+    def selection_size(self, n: int, r: float):
+        m, k = C.c_int32(), C.c_int32()
+        check(lib().skv_selection_size(self._h, n, r, C.byref(m), C.byref(k)))
+        return m.value, k.value
+
+    def sparsity(self, layer: int) -> torch.Tensor:
+        # attention_sparsity of each sequence's last step row (attention.hpp:275-310)
+        out = torch.empty(self.batch, dtype=torch.float64, device=self.dev)
+        check(lib().skv_sparsity_get(self._h, layer, 0, self.batch, _ptr(out), _stream(out)))
+        return out
 
     # ---- three-phase schedule bookkeeping (memsim.hpp:77-215, scheduler.hpp:320-381)
     def set_plan(self, alpha: float, beta: float, p1: int, p2: int, input_len: int, output_len: int,

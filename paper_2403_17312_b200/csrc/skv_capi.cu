@@ -97,6 +97,8 @@ struct skv_cache {
     uint8_t* tiers = nullptr;  // [L][B][Ncap] KvLedger tiers: 0 device, 1 host, 2 deleted, 255 absent
     int* act_lists = nullptr;  // [L][B][4][Ncap] last step_actions lists
     int* act_counts = nullptr; // [L][B][4]
+    double* sparsity = nullptr;  // [L][B] attention_sparsity of the last step's row
+    int variant = SKV_VARIANT_SWA, stride = 0;  // SparsityConfig (attention.hpp:15-21)
     bool has_plan = false;
     skv_plan plan{};
     std::vector<long long> ledger_j;  // per layer: last step whose actions were applied (-1: none)
@@ -177,6 +179,7 @@ skv_status skv_cache_create(const skv_cache_desc* desc, skv_cache** out) {
     const size_t tier_bytes = static_cast<size_t>(d.layers) * d.batch * d.capacity;
     const size_t list_bytes = static_cast<size_t>(d.layers) * d.batch * 4 * d.capacity * 4;
     const size_t acnt_bytes = static_cast<size_t>(d.layers) * d.batch * 4 * 4;
+    const size_t sp_bytes = static_cast<size_t>(d.layers) * d.batch * 8;
     auto alloc = [&](void** p, size_t bytes) -> bool {
         if (bytes == 0) return true;
         if (cudaMalloc(p, bytes) != cudaSuccess) {
@@ -193,7 +196,8 @@ skv_status skv_cache_create(const skv_cache_desc* desc, skv_cache** out) {
         !alloc(reinterpret_cast<void**>(&c->idx), cnt_bytes) ||
         !alloc(reinterpret_cast<void**>(&c->tiers), tier_bytes) ||
         !alloc(reinterpret_cast<void**>(&c->act_lists), list_bytes) ||
-        !alloc(reinterpret_cast<void**>(&c->act_counts), acnt_bytes)) {
+        !alloc(reinterpret_cast<void**>(&c->act_counts), acnt_bytes) ||
+        !alloc(reinterpret_cast<void**>(&c->sparsity), sp_bytes)) {
         const uint64_t want = kv_bytes + meta_bytes + imp_bytes + wpart_bytes + cnt_bytes + tier_bytes + list_bytes +
                               acnt_bytes;
         skv_cache_destroy(c);
@@ -203,6 +207,7 @@ skv_status skv_cache_create(const skv_cache_desc* desc, skv_cache** out) {
     SKV_CUDA(cudaMemset(c->imp, 0, imp_bytes));
     SKV_CUDA(cudaMemset(c->tiers, 0xFF, tier_bytes));
     SKV_CUDA(cudaMemset(c->act_counts, 0, acnt_bytes));
+    SKV_CUDA(cudaMemset(c->sparsity, 0, sp_bytes));
     c->pend_n.assign(d.layers, -1);
     c->pend_r.assign(d.layers, 0.0);
     c->ledger_j.assign(d.layers, -1);
@@ -224,6 +229,7 @@ skv_status skv_cache_destroy(skv_cache* c) {
     cudaFree(c->tiers);
     cudaFree(c->act_lists);
     cudaFree(c->act_counts);
+    cudaFree(c->sparsity);
     cudaFree(c->stage);
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -351,15 +357,35 @@ uint64_t attend_algo_bytes(const skv_cache* c, int m, bool append) {
 }
 
 struct StepShape {
-    int k, m;
+    int k, m, stride;
     bool dense;
 };
 
+// The selection shape of one step for the cache's variant
+// (Engine::variant_selection, engine.hpp:531-569).
 skv_status step_shape(const skv_cache* c, int n, double r, StepShape* s) {
     SKV_REQUIRE(n >= 1, "swa_attention: empty cache");
     SKV_REQUIRE(n <= c->d.capacity, "decode_step: context overflow");
+    s->stride = 0;
+    if (c->variant == SKV_VARIANT_DENSE) r = 1.0;  // swa_select(imp, n, 1.0)
     const size_t k = skv_swa_window_k(static_cast<size_t>(n), r);
     if (k == 0) return SKV_ERR_CONTRACT;
+    const int keep = static_cast<int>(std::min<size_t>(2 * k, static_cast<size_t>(n)));
+    if (c->variant == SKV_VARIANT_LOCAL) {  // local_attention_mask(n, keep)
+        s->m = keep;
+        s->k = keep;
+        s->dense = false;
+        return SKV_OK;
+    }
+    if (c->variant == SKV_VARIANT_STRIDED) {  // strided_attention_mask(n, stride)
+        const int stride = c->stride > 0 ? c->stride : std::max(1, (n + keep - 1) / keep);
+        const int phase = (n - 1) % stride;
+        s->stride = stride;
+        s->m = (n - 1 - phase) / stride + 1;
+        s->k = 1;
+        s->dense = false;
+        return SKV_OK;
+    }
     s->k = static_cast<int>(k);
     s->dense = n < 2 || 2 * static_cast<int>(k) >= n;
     s->m = s->dense ? n : 2 * s->k;
@@ -374,8 +400,11 @@ int* layer_idx(const skv_cache* c, int layer) {
 // kernel's weight partials into the importance, optionally select for
 // (n_next, r_next) into the layer's index buffer (recorded as pending).
 skv_status launch_select_c(skv_cache* c, int layer, int apply, const int* tok_prev, long long tok_prev_ld,
-                           int m_prev, int G, int cur_tok, int n_next, double r_next, bool pdl, cudaStream_t st) {
+                           int m_prev, int G, int cur_tok, int n_next, double r_next, bool pdl, cudaStream_t st,
+                           int sp_n = 0) {
     skvd::SelectParams p{};
+    p.sp_n = apply ? sp_n : 0;
+    p.sparsity = c->sparsity + static_cast<size_t>(layer) * c->d.batch;
     p.imp = c->imp + static_cast<size_t>(layer) * c->d.batch * c->d.capacity;
     p.imp_ld = c->d.capacity;
     p.wpart = c->wpart + static_cast<size_t>(layer) * c->d.batch * c->d.heads * c->d.capacity;
@@ -399,6 +428,8 @@ skv_status launch_select_c(skv_cache* c, int layer, int apply, const int* tok_pr
         p.k = s.k;
         p.m = s.m;
         p.dense = s.dense ? 1 : 0;
+        p.variant = c->variant == SKV_VARIANT_DENSE ? SKV_VARIANT_SWA : c->variant;
+        p.stride = s.stride;
     }
     if (!p.apply && !p.select) return SKV_OK;
     SKV_CUDA(launch_select(p, c->d.batch, pdl, st));
@@ -530,7 +561,7 @@ skv_status decode_layer_impl(skv_cache* c, int layer, int n, double r, const voi
                                        out, idx_out, w_out, chained && !fresh, st, &G))
         return e;
     if (skv_status e = launch_select_c(c, layer, 1, layer_idx(c, layer), c->d.capacity, s.m, G, n - 1, n + 1, r,
-                                       !c->prof, st))
+                                       !c->prof, st, n))
         return e;
     if (c->has_plan && c->pend_n[layer] == n + 1) {
         // the next step's KV residency actions (scheduler.hpp:320-381) on the
@@ -651,7 +682,7 @@ skv_status skv_attend_over_indices(skv_cache* c, int layer, int n, const int32_t
     if (skv_status e = launch_attend_c(c, layer, n, m, idx, m, false, q, nullptr, nullptr, out, nullptr, w_out,
                                        false, st, &G))
         return e;
-    return launch_select_c(c, layer, 1, idx, m, m, G, -1, 0, 0.0, true, st);
+    return launch_select_c(c, layer, 1, idx, m, m, G, -1, 0, 0.0, true, st, n);
 }
 
 skv_status skv_swa_select(const double* importance, int batch, int64_t ld, int n, double r, int32_t* idx_out,
@@ -681,6 +712,7 @@ skv_status skv_swa_select(const double* importance, int batch, int64_t ld, int n
     p.dense = dense ? 1 : 0;
     p.idx = idx_out;
     p.idx_ld = m;
+    p.variant = SKV_VARIANT_SWA;
     SKV_CUDA(launch_select(p, batch, false, as_stream(stream)));
     return SKV_OK;
 }
@@ -715,6 +747,34 @@ skv_status skv_dequantize(const uint16_t* codes, size_t len, size_t channel_size
     SKV_REQUIRE(codes && scales && zero_points && out, "dequantize: null argument");
     SKV_CUDA(launch_dequantize(codes, static_cast<long long>(len), static_cast<long long>(channel_size), scales,
                                reinterpret_cast<const long long*>(zero_points), out, as_stream(stream)));
+    return SKV_OK;
+}
+
+skv_status skv_cache_set_variant(skv_cache* c, int variant, int stride) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    SKV_REQUIRE(variant >= SKV_VARIANT_DENSE && variant <= SKV_VARIANT_STRIDED, "unknown attention variant");
+    SKV_REQUIRE(stride >= 0, "strided_attention_mask: stride must be >= 1");
+    c->variant = variant;
+    c->stride = stride;
+    for (auto& p : c->pend_n) p = -1;
+    return SKV_OK;
+}
+
+skv_status skv_selection_size(const skv_cache* c, int n, double r, int32_t* m, int32_t* k) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    StepShape s;
+    if (skv_status e = step_shape(c, n, r, &s)) return e;
+    if (m) *m = s.m;
+    if (k) *k = s.k;
+    return SKV_OK;
+}
+
+skv_status skv_sparsity_get(const skv_cache* c, int layer, int b0, int nb, double* dst, void* stream) {
+    if (skv_status s = check_block(c, layer, b0, nb, 0, 1)) return s;
+    SKV_REQUIRE(dst != nullptr, "sparsity: null output");
+    DeviceGuard guard(c->d.device);
+    SKV_CUDA(cudaMemcpyAsync(dst, c->sparsity + static_cast<size_t>(layer) * c->d.batch + b0,
+                             static_cast<size_t>(nb) * 8, cudaMemcpyDefault, as_stream(stream)));
     return SKV_OK;
 }
 

@@ -162,19 +162,63 @@ __global__ void __launch_bounds__(kSelectThreads) swa_select_kernel(const Select
     pdl_launch_dependents();
     if (p.pdl_wait) pdl_wait();
     double* imp = p.imp + static_cast<size_t>(b) * p.imp_ld;
+    __shared__ double red_max[kSelectThreads / 32];
+    __shared__ int red_cnt[kSelectThreads / 32];
     if (p.apply) {
         const float* wp = p.wpart + static_cast<size_t>(b) * p.G * p.m_prev;
         const int* tp = p.tok_prev ? p.tok_prev + static_cast<size_t>(b) * p.tok_prev_ld : nullptr;
+        double vmax = 0.0;
         for (int pos = tid; pos < p.m_prev; pos += kSelectThreads) {
             double v = 0.0;
             for (int g = 0; g < p.G; ++g) v += static_cast<double>(wp[static_cast<size_t>(g) * p.m_prev + pos]);
             const int t = tp ? tp[pos] : pos;
             imp[t] = (p.apply == 2 || t == p.cur_tok) ? v : imp[t] + v;
+            vmax = v > vmax ? v : vmax;
+        }
+        if (p.sp_n > 0) {
+            // attention_sparsity (attention.hpp:275-310) of the head-summed step
+            // row new_aw_row (length sp_n, zeros off-selection), threshold 0.01
+            const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double o = __shfl_xor_sync(0xffffffffu, vmax, off);
+                vmax = o > vmax ? o : vmax;
+            }
+            if (lane == 0) red_max[warp] = vmax;
+            __syncthreads();
+            double mx = 0.0;
+            for (int w = 0; w < kSelectThreads / 32; ++w) mx = red_max[w] > mx ? red_max[w] : mx;
+            const double thr = 0.01 * mx;
+            int below = 0;
+            for (int pos = tid; pos < p.m_prev; pos += kSelectThreads) {
+                double v = 0.0;
+                for (int g = 0; g < p.G; ++g) v += static_cast<double>(wp[static_cast<size_t>(g) * p.m_prev + pos]);
+                below += v < thr;
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) below += __shfl_xor_sync(0xffffffffu, below, off);
+            if (lane == 0) red_cnt[warp] = below;
+            __syncthreads();
+            if (tid == 0) {
+                int cnt = 0;
+                for (int w = 0; w < kSelectThreads / 32; ++w) cnt += red_cnt[w];
+                const int sparse = mx == 0.0 ? p.sp_n : cnt + (p.sp_n - p.m_prev);
+                p.sparsity[b] = static_cast<double>(sparse) / static_cast<double>(p.sp_n);
+            }
         }
     }
     if (!p.select) return;
     __syncthreads();
     int* o = p.idx + static_cast<size_t>(b) * p.idx_ld;
+    if (p.variant == 2) {  // local_attention_mask (attention.hpp:247-256): the last m tokens
+        for (int i = tid; i < p.m; i += kSelectThreads) o[i] = p.n - p.m + i;
+        return;
+    }
+    if (p.variant == 3) {  // strided_attention_mask (attention.hpp:258-269), phased onto n-1
+        const int phase = (p.n - 1) % p.stride;
+        for (int i = tid; i < p.m; i += kSelectThreads) o[i] = phase + i * p.stride;
+        return;
+    }
     if (p.dense) {
         for (int i = tid; i < p.m; i += kSelectThreads) o[i] = i;
         return;

@@ -30,6 +30,10 @@ struct SelectParams {
     int cur_tok;  // -1: none
     int select;   // compute a selection for (n, k, m, dense)
     int n, k, m, dense;
+    int variant;  // 1 swa (dense when `dense`), 2 local, 3 strided (engine.hpp:531-569)
+    int stride;   // strided only
+    int sp_n;           // > 0: attention_sparsity of the folded row (length sp_n) into sparsity[b]
+    double* sparsity;   // [B]
     int* idx;  // [B][idx_ld]
     long long idx_ld;
     int pdl_wait;

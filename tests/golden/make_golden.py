@@ -147,6 +147,26 @@ def main() -> None:
     g["sa_out"] = np.concatenate([np.concatenate([r_[7][nm] for nm in ("offload", "delete", "reload", "recompute")])
                                   for r_ in sa_rows]).astype(np.int64)
 
+    # attention.hpp:247-269 masks and 275-310 sparsity
+    mask_rows = []
+    for n in (1, 2, 5, 17, 100, 513):
+        for w in (1, 3, 50, 600):
+            mask_rows.append((0, n, w, ref.local_attention_mask(n, w)))
+        for st in (1, 2, 7, 50):
+            mask_rows.append((1, n, st, ref.strided_attention_mask(n, st)))
+    g["mask_meta"] = np.array([[a, b, c, len(m)] for a, b, c, m in mask_rows], np.int64)
+    g["mask_out"] = np.concatenate([m for *_, m in mask_rows]).astype(np.int64)
+    sp_in, sp_out = [], []
+    for rep in range(12):
+        a = rng.random((3, 40))
+        a[a < 0.6] = 0.0
+        if rep == 0:
+            a[:] = 0.0
+        sp_in.append(a)
+        sp_out.append([ref.attention_sparsity(a, 0.01, False), ref.attention_sparsity(a, 0.01, True)])
+    g["sp_in"] = np.stack(sp_in)
+    g["sp_out"] = np.array(sp_out)
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({os.path.getsize(OUT)} bytes)")
 

@@ -74,6 +74,14 @@ class OracleSeq:
     def step(self, n: int, r: float, q_hd: np.ndarray):
         return self.port.swa_attention(self.keys, self.vals, self.acc, q_hd, r, n)
 
+    def step_variant(self, n: int, r: float, q_hd: np.ndarray, variant: str, stride: int = 0):
+        """Engine::variant_selection (engine.hpp:531-569) + attend_over_indices."""
+        if variant in ("swa", "dense"):
+            return self.step(n, 1.0 if variant == "dense" else r, q_hd)
+        idx, _ = self.port.variant_selection(variant, n, r, stride)
+        attn, aw = self.port.attend_over_indices(self.keys, self.vals, self.acc, n - 1, q_hd, idx, n)
+        return attn, aw, idx
+
 
 def selection_flip_is_tie(gpu_idx, ora_idx, imp_pre: np.ndarray, n: int, k: int) -> bool:
     """True when the two selections differ only among global candidates whose

@@ -258,6 +258,42 @@ def test_decode_ratios(api, port, r):
     run_trajectory(api, port, "f32", 2, 8, 64, 8, r, seed=int(r * 100))
 
 
+@pytest.mark.parametrize("variant,stride", [("dense", 0), ("local", 0), ("strided", 0), ("strided", 5)])
+def test_decode_variants_and_sparsity(api, port, variant, stride):
+    """Dense / Local / Strided through the same kernels (engine.hpp:531-569),
+    plus the per-step attention_sparsity of the head-summed row
+    (engine.hpp:631-633, attention.hpp:275-310)."""
+    rng = np.random.default_rng(sum(map(ord, variant)) + stride)
+    B, H, D, s, steps, r = 2, 8, 128, 100, 6, 0.2
+    ncap = s + steps
+    kv = rng.standard_normal((B, ncap, 2, H, D))
+    qs = rng.standard_normal((steps + 1, B, H, D)) * 2.0
+    cache = api.SwaCache(1, B, H, D, ncap, kv_dtype="f32")
+    cache.set_variant(variant, stride)
+    cache.append_tokens(0, 0, 0, cuda(kv[:, :s, 0], torch.float32), cuda(kv[:, :s, 1], torch.float32))
+    cache.prefill_seed(0, s, cuda(qs[0], torch.float32))
+    seqs = [OracleSeq(port, H, D, ncap) for _ in range(B)]
+    for b in range(B):
+        for t in range(s):
+            seqs[b].append(t, kv[b, t, 0], kv[b, t, 1])
+        seqs[b].seed(s, qs[0][b])
+    for j in range(steps):
+        n = s + j + 1
+        out, idx, _ = cache.swa_decode_layer(0, n, r, cuda(qs[j + 1], torch.float32),
+                                             cuda(kv[:, n - 1, 0], torch.float32), cuda(kv[:, n - 1, 1], torch.float32),
+                                             return_indices=True)
+        sp = cache.sparsity(0).cpu().numpy()
+        imp = cache.importance(0, n).cpu().numpy()
+        for b in range(B):
+            seqs[b].append(n - 1, kv[b, n - 1, 0], kv[b, n - 1, 1])
+            attn, aw, oidx = seqs[b].step_variant(n, r, qs[j + 1][b], variant, stride)
+            assert np.array_equal(idx[b].cpu().numpy(), oidx), (variant, j, b)
+            assert_close(out[b].cpu().numpy(), attn, TOL["f32"], f"{variant} step {j}")
+            np.testing.assert_allclose(imp[b], seqs[b].importance(n), rtol=1e-4, atol=1e-7)
+            want_sp = port.attention_sparsity(aw[None, :], 0.01, False)
+            assert abs(sp[b] - want_sp) <= 1.0 / n + 1e-12, (variant, j, sp[b], want_sp)
+
+
 def test_decode_multilayer_step(api):
     """skv_swa_decode_step over L layers == per-layer calls; host-buffer
     variant == device variant."""
