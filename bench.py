@@ -151,6 +151,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--variant", default="swa", choices=["swa", "dense", "local", "strided"],
+                    help="attention variant (engine.hpp:531-569); dense = the full-KV decode baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no clocks/baseline/e2e)")
@@ -187,6 +189,7 @@ def main():
     ncap = s + W + K + min(K, 10) + e2e_steps + 1
     qdt = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[cfg["q"]]
     cache = api.SwaCache(L, B, H, D, ncap, kv_dtype=cfg["kv"], q_dtype=cfg["q"], device=local)
+    cache.set_variant(args.variant)
 
     # ---- prompt: random K/V for s tokens per layer, accumulator seeded from the
     # dense last row of the prompt (engine.hpp:508-512), all on device.
@@ -298,7 +301,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": elapsed_ms / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": cfg["kv"], "data": "synthetic (torch.randn K/V/q, seeded)",
-            "config": {"workload": cfg["name"], "per_gpu_batch": B, "global_batch": world * B, "layers": L,
+            "config": {"workload": cfg["name"], "variant": args.variant, "per_gpu_batch": B, "global_batch": world * B, "layers": L,
                        "heads": H, "head_dim": D, "ratio": RATIO, "n_range": [n_first, n_first + K - 1],
                        "parallelism": f"batch-sharded x{world} (no collective)", "rank0_batch_offset": b0,
                        "l2": "inputs larger than L2 (per-step KV gather >> 126 MB)"},

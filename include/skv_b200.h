@@ -168,6 +168,29 @@ typedef struct skv_plan {
     int32_t recompute_enabled;
     int64_t input_len, output_len;
 } skv_plan;
+/* CostParams (memsim.hpp:15-38): h, l, b, s, n, r, B (bytes/s), element
+ * bytes, device capacity (bytes), simulated MAC rate, recompute overhead. */
+typedef struct skv_cost_params {
+    int64_t hidden, layers, batch, input_len, output_len;
+    double ratio, bandwidth;
+    int32_t bytes_per_element;
+    uint64_t device_capacity;
+    double mac_rate, recompute_overhead;
+} skv_cost_params;
+/* PlanPrediction (scheduler.hpp:75-81) + per-phase PhasePrediction. */
+typedef struct skv_plan_prediction {
+    double total_seconds, prefill_compute_seconds;
+    double phase_compute[3], phase_transfer[3], phase_recompute[3];
+    int64_t phase_steps[3];
+    uint64_t peak_device_bytes;
+    int32_t feasible;
+} skv_plan_prediction;
+/* solve_plan (scheduler.hpp:207-303), host-side, offline: p1 from capacity,
+ * then greedy coordinate descent over (alpha, beta, p2). SKV_ERR_INFEASIBLE
+ * as InfeasiblePlan. input_len/output_len of the plan are NOT filled. */
+skv_status skv_solve_plan(const skv_cost_params* cost, skv_plan* plan, skv_plan_prediction* prediction);
+/* predict_plan (scheduler.hpp:174-186): the simulated objective of a plan. */
+skv_status skv_predict_plan(const skv_cost_params* cost, const skv_plan* plan, skv_plan_prediction* prediction);
 /* Attach (or with NULL detach) a plan. While attached, every decode step also
  * runs step_actions + apply_actions for the NEXT step on the device ledger
  * right after selecting it (so the lists are ready before that step runs). */

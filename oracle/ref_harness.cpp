@@ -290,6 +290,40 @@ int ref_step_actions(double alpha, double beta, size_t p1, size_t p2, int recomp
     });
 }
 
+// scheduler.hpp:207-303 solve_plan. plan_out = {alpha, beta, p1, p2};
+// pred_out = {total, prefill, compute[3], transfer[3], recompute[3], steps[3]}.
+int ref_solve_plan(size_t hidden, size_t layers, size_t batch, size_t input_len, size_t output_len,
+                   double ratio, double bandwidth, size_t bpe, uint64_t capacity, double mac_rate,
+                   double overhead, double* plan_out, double* pred_out) {
+    return guarded([&] {
+        skv::CostParams p;
+        p.hidden = hidden;
+        p.layers = layers;
+        p.batch = batch;
+        p.input_len = input_len;
+        p.output_len = output_len;
+        p.ratio = ratio;
+        p.bandwidth = bandwidth;
+        p.bytes_per_element = bpe;
+        p.device_capacity = capacity;
+        p.mac_rate = mac_rate;
+        p.recompute_overhead = overhead;
+        const skv::SchedulePlan plan = skv::solve_plan(p);
+        plan_out[0] = plan.alpha;
+        plan_out[1] = plan.beta;
+        plan_out[2] = static_cast<double>(plan.p1);
+        plan_out[3] = static_cast<double>(plan.p2);
+        pred_out[0] = plan.predicted_total_seconds;
+        pred_out[1] = plan.prefill_compute_seconds;
+        for (int i = 0; i < 3; ++i) {
+            pred_out[2 + i] = plan.phases[i].compute_seconds;
+            pred_out[5 + i] = plan.phases[i].transfer_seconds;
+            pred_out[8 + i] = plan.phases[i].recompute_seconds;
+            pred_out[11 + i] = static_cast<double>(plan.phases[i].steps);
+        }
+    });
+}
+
 // CPU timing arm: share-nothing threads, one AttentionState per worker. Each
 // work item = append one token then skv::swa_attention (one (sequence, layer)
 // decode step). Items run in rounds of up to 16 at n = n0 .. n0+15; between

@@ -130,6 +130,51 @@ class _Plan(C.Structure):
                 ("recompute_enabled", C.c_int32), ("input_len", C.c_int64), ("output_len", C.c_int64)]
 
 
+class _CostParams(C.Structure):
+    _fields_ = [("hidden", C.c_int64), ("layers", C.c_int64), ("batch", C.c_int64), ("input_len", C.c_int64),
+                ("output_len", C.c_int64), ("ratio", C.c_double), ("bandwidth", C.c_double),
+                ("bytes_per_element", C.c_int32), ("device_capacity", C.c_uint64), ("mac_rate", C.c_double),
+                ("recompute_overhead", C.c_double)]
+
+
+class _Prediction(C.Structure):
+    _fields_ = [("total_seconds", C.c_double), ("prefill_compute_seconds", C.c_double),
+                ("phase_compute", C.c_double * 3), ("phase_transfer", C.c_double * 3),
+                ("phase_recompute", C.c_double * 3), ("phase_steps", C.c_int64 * 3),
+                ("peak_device_bytes", C.c_uint64), ("feasible", C.c_int32)]
+
+
+def _cost(cost: dict) -> _CostParams:
+    return _CostParams(cost["hidden"], cost["layers"], cost.get("batch", 1), cost["input_len"], cost["output_len"],
+                       cost.get("ratio", 1.0), cost.get("bandwidth", 1.0), cost.get("bytes_per_element", 2),
+                       cost.get("device_capacity", 0), cost.get("mac_rate", 1e9), cost.get("recompute_overhead", 1.0))
+
+
+def _pred(p: _Prediction) -> dict:
+    return {"total_seconds": p.total_seconds, "prefill_compute_seconds": p.prefill_compute_seconds,
+            "phase_compute": list(p.phase_compute), "phase_transfer": list(p.phase_transfer),
+            "phase_recompute": list(p.phase_recompute), "phase_steps": list(p.phase_steps),
+            "peak_device_bytes": p.peak_device_bytes, "feasible": bool(p.feasible)}
+
+
+def solve_plan(cost: dict):
+    """solve_plan (scheduler.hpp:207-303) -> (plan dict, prediction dict).
+    cost keys follow CostParams (memsim.hpp:15-38)."""
+    pl, pr = _Plan(), _Prediction()
+    check(lib().skv_solve_plan(C.byref(_cost(cost)), C.byref(pl), C.byref(pr)))
+    plan = {"alpha": pl.alpha, "beta": pl.beta, "p1": pl.p1, "p2": pl.p2,
+            "recompute_enabled": bool(pl.recompute_enabled)}
+    return plan, _pred(pr)
+
+
+def predict_plan(cost: dict, plan: dict) -> dict:
+    """predict_plan (scheduler.hpp:174-186)."""
+    pl = _Plan(plan["alpha"], plan["beta"], plan["p1"], plan["p2"], int(plan.get("recompute_enabled", True)), 0, 0)
+    pr = _Prediction()
+    check(lib().skv_predict_plan(C.byref(_cost(cost)), C.byref(pl), C.byref(pr)))
+    return _pred(pr)
+
+
 class SwaCache:
     """Device-resident decode state: the reference's AttentionState
     (attention.hpp:45-86) for `layers` x `batch` sequences, K/V token-major in

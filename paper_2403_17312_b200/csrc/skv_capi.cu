@@ -22,6 +22,16 @@ using namespace skv_impl;
 namespace {
 
 thread_local std::string g_err;
+}  // namespace
+
+namespace skv_impl {
+skv_status fail_msg(skv_status s, const char* msg) {
+    g_err = msg;
+    return s;
+}
+}  // namespace skv_impl
+
+namespace {
 
 skv_status fail(skv_status s, const char* fmt, ...) {
     char buf[512];

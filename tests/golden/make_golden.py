@@ -167,6 +167,29 @@ def main() -> None:
     g["sp_in"] = np.stack(sp_in)
     g["sp_out"] = np.array(sp_out)
 
+    # scheduler.hpp:207-303 solve_plan on small workloads (capacity-constrained
+    # and not), via the reference itself
+    import ctypes as C
+    lib = ref.lib
+    plans = []
+    for rep in range(24):
+        hidden, layers, batch = int(rng.choice([16, 64])), int(rng.integers(1, 4)), int(rng.integers(1, 5))
+        s_len, out_len = int(rng.integers(4, 40)), int(rng.integers(2, 30))
+        bpe = int(rng.choice([1, 2]))
+        tb = 2 * bpe * batch * layers * hidden
+        cap = int(tb * (s_len + rng.integers(0, out_len + 4)))
+        if rep % 6 == 5:
+            cap = tb * s_len - 1  # prompt alone exceeds capacity -> InfeasiblePlan
+        ratio = float(rng.choice([0.2, 0.5, 1.0]))
+        bw, mac = float(rng.choice([1e3, 1e6, 1e9])), float(rng.choice([1e6, 1e9]))
+        ovh = float(rng.choice([1.0, 1.5]))
+        po, pr = (C.c_double * 4)(), (C.c_double * 14)()
+        rc = lib.ref_solve_plan(C.c_size_t(hidden), C.c_size_t(layers), C.c_size_t(batch), C.c_size_t(s_len),
+                                C.c_size_t(out_len), C.c_double(ratio), C.c_double(bw), C.c_size_t(bpe),
+                                C.c_uint64(cap), C.c_double(mac), C.c_double(ovh), po, pr)
+        plans.append([hidden, layers, batch, s_len, out_len, ratio, bw, bpe, cap, mac, ovh, rc] + list(po) + list(pr))
+    g["plan_rows"] = np.array(plans, np.float64)
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({os.path.getsize(OUT)} bytes)")
 
