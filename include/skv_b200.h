@@ -195,6 +195,12 @@ skv_status skv_predict_plan(const skv_cost_params* cost, const skv_plan* plan, s
  * runs step_actions + apply_actions for the NEXT step on the device ledger
  * right after selecting it (so the lists are ready before that step runs). */
 skv_status skv_cache_set_plan(skv_cache* cache, const skv_plan* plan);
+/* Host tier for Phase II/III: a pinned, device-mapped mirror of the KV
+ * layout. With it (and a plan) every decode step also MOVES the rows the
+ * ledger lists: offloads copy device -> host (and with `poison` overwrite the
+ * device row with NaN, so any read of a non-resident row shows up), reloads
+ * copy host -> device -- apply_actions (engine.hpp:686-716). */
+skv_status skv_cache_enable_host_tier(skv_cache* cache, int poison);
 /* KvLedger tiers per token (memsim.hpp:72): 0 Device, 1 Host, 2 Deleted,
  * 255 not stored. src/dst: [nb][len] bytes (host or device). skv_cache_write
  * marks written tokens Device (store_new). */

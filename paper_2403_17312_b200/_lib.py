@@ -78,6 +78,7 @@ def _declare(lib):
         "skv_quantize": (I, [P, SZ, C.c_uint32, SZ, P, P, P, P]),
         "skv_dequantize": (I, [P, SZ, SZ, P, P, P, P]),
         "skv_cache_set_plan": (I, [P, P]),
+        "skv_cache_enable_host_tier": (I, [P, I]),
         "skv_solve_plan": (I, [P, P, P]),
         "skv_predict_plan": (I, [P, P, P]),
         "skv_cache_set_variant": (I, [P, I, I]),

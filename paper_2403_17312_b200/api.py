@@ -323,6 +323,9 @@ class SwaCache:
         pl = _Plan(alpha, beta, p1, p2, int(recompute_enabled), input_len, output_len)
         check(lib().skv_cache_set_plan(self._h, C.byref(pl)))
 
+    def enable_host_tier(self, poison: bool = False):
+        check(lib().skv_cache_enable_host_tier(self._h, int(poison)))
+
     def clear_plan(self):
         check(lib().skv_cache_set_plan(self._h, None))
 

@@ -108,6 +108,8 @@ struct skv_cache {
     int* act_lists = nullptr;  // [L][B][4][Ncap] last step_actions lists
     int* act_counts = nullptr; // [L][B][4]
     double* sparsity = nullptr;  // [L][B] attention_sparsity of the last step's row
+    uint8_t* host_kv = nullptr;  // host tier: mapped pinned mirror of the device layout (or null)
+    bool poison = false;         // offload overwrites device rows (checks residency)
     int variant = SKV_VARIANT_SWA, stride = 0;  // SparsityConfig (attention.hpp:15-21)
     bool has_plan = false;
     skv_plan plan{};
@@ -240,6 +242,7 @@ skv_status skv_cache_destroy(skv_cache* c) {
     cudaFree(c->act_lists);
     cudaFree(c->act_counts);
     cudaFree(c->sparsity);
+    if (c->host_kv) cudaFreeHost(c->host_kv);
     cudaFree(c->stage);
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -546,6 +549,27 @@ skv_status launch_ledger_c(skv_cache* c, int layer, long long j, const int* sel,
     return SKV_OK;
 }
 
+// apply_actions data movement for one layer (engine.hpp:686-716): offload
+// then reload over the host tier, after the ledger kernel made the lists.
+skv_status launch_movement(skv_cache* c, int layer, bool pdl, cudaStream_t st) {
+    if (!c->host_kv) return SKV_OK;
+    skvd::MoveParams mp{};
+    const size_t lt = static_cast<size_t>(layer) * c->d.batch;
+    mp.dev = c->kv + layer * c->layer_bytes;
+    mp.host = c->host_kv + layer * c->layer_bytes;
+    mp.lists = c->act_lists + lt * 4 * c->d.capacity;
+    mp.counts = c->act_counts + lt * 4;
+    mp.list_ld = c->d.capacity;
+    mp.tok_bytes = static_cast<long long>(c->tok_bytes);
+    mp.seq_bytes = static_cast<long long>(c->tok_bytes) * c->d.capacity;
+    mp.poison = c->poison ? 1 : 0;
+    mp.which = 0;
+    SKV_CUDA(launch_move(mp, c->d.batch, c->d.capacity, pdl, st));
+    mp.which = 2;
+    SKV_CUDA(launch_move(mp, c->d.batch, c->d.capacity, true, st));
+    return SKV_OK;
+}
+
 // One layer of one decode step: [select if no matching pending selection] ->
 // attend (append + gather + softmax + PV) -> select kernel (fold weights into
 // the importance, select for n+1 with the same ratio).
@@ -560,10 +584,12 @@ skv_status decode_layer_impl(skv_cache* c, int layer, int n, double r, const voi
         fresh = true;
         if (c->has_plan) {  // this step's bookkeeping (normally done right after the previous step)
             const long long j = static_cast<long long>(n) - 1 - c->plan.input_len;
-            if (j >= 0 && j < c->plan.output_len && c->ledger_j[layer] != j)
+            if (j >= 0 && j < c->plan.output_len && c->ledger_j[layer] != j) {
                 if (skv_status e = launch_ledger_c(c, layer, j, layer_idx(c, layer), c->d.capacity, s.m, s.k, true,
                                                    true, false, st))
                     return e;
+                if (skv_status e = launch_movement(c, layer, true, st)) return e;
+            }
         }
     }
     int G = 0;
@@ -580,8 +606,10 @@ skv_status decode_layer_impl(skv_cache* c, int layer, int n, double r, const voi
         if (j_next >= 0 && j_next < c->plan.output_len) {
             StepShape sn;
             if (skv_status e = step_shape(c, n + 1, r, &sn)) return e;
-            return launch_ledger_c(c, layer, j_next, layer_idx(c, layer), c->d.capacity, sn.m, sn.k, true, true,
-                                   !c->prof, st);
+            if (skv_status e = launch_ledger_c(c, layer, j_next, layer_idx(c, layer), c->d.capacity, sn.m, sn.k,
+                                               true, true, !c->prof, st))
+                return e;
+            return launch_movement(c, layer, !c->prof, st);
         }
     }
     return SKV_OK;
@@ -757,6 +785,22 @@ skv_status skv_dequantize(const uint16_t* codes, size_t len, size_t channel_size
     SKV_REQUIRE(codes && scales && zero_points && out, "dequantize: null argument");
     SKV_CUDA(launch_dequantize(codes, static_cast<long long>(len), static_cast<long long>(channel_size), scales,
                                reinterpret_cast<const long long*>(zero_points), out, as_stream(stream)));
+    return SKV_OK;
+}
+
+skv_status skv_cache_enable_host_tier(skv_cache* c, int poison) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    DeviceGuard guard(c->d.device);
+    if (!c->host_kv) {
+        void* h = nullptr;
+        const size_t bytes = c->layer_bytes * c->d.layers;
+        if (cudaHostAlloc(&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(SKV_ERR_OOM, "host tier: cannot pin %llu bytes", static_cast<unsigned long long>(bytes));
+        }
+        c->host_kv = static_cast<uint8_t*>(h);
+    }
+    c->poison = poison != 0;
     return SKV_OK;
 }
 

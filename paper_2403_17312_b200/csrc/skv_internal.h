@@ -17,6 +17,7 @@ void count_launch();
 
 cudaError_t launch_select(const skvd::SelectParams& p, int batch, bool pdl, cudaStream_t st);
 cudaError_t launch_ledger(const skvd::LedgerParams& p, int batch, bool pdl, cudaStream_t st);
+cudaError_t launch_move(const skvd::MoveParams& p, int batch, int max_tokens, bool pdl, cudaStream_t st);
 cudaError_t launch_top_k(const double* v, int batch, long long ld, int len, int k, int* out,
                          cudaStream_t st);
 cudaError_t launch_quantize(const double* x, long long len, long long cs, uint32_t bits,

@@ -1,6 +1,8 @@
 // skv_kernels.cu -- sm_100a kernels behind the C ABI other than the fused
 // decode kernel: batched swa_select / top_k, fp64 quantize / dequantize,
 // cache writes (append with fake-quant) and reads.
+#include <algorithm>
+
 #include "skv_internal.h"
 #include "skv_select.cuh"
 #include "skv_ledger.cuh"
@@ -150,6 +152,31 @@ __global__ void __launch_bounds__(kLedgerThreads) ledger_step_kernel(const Ledge
             tg[i] = t;
         }
         if (tid == 0 && p.store_current) tg[ntok] = kTierDevice;
+    }
+}
+
+// Offload / reload the rows of one action list: grid (token chunk, sequence).
+// 16-byte vectors; the host side is mapped pinned memory (PCIe zero-copy).
+__global__ void __launch_bounds__(256) kv_move_kernel(const MoveParams p) {
+    pdl_launch_dependents();
+    pdl_wait();  // the lists come from the preceding ledger kernel
+    const int b = blockIdx.y;
+    const int cnt = p.counts[b * 4 + p.which];
+    const int* list = p.lists + (static_cast<size_t>(b) * 4 + p.which) * p.list_ld;
+    const long long vec_per_tok = p.tok_bytes / 16;
+    const long long total = static_cast<long long>(cnt) * vec_per_tok;
+    for (long long v = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; v < total;
+         v += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int t = list[v / vec_per_tok];
+        const size_t off = static_cast<size_t>(b) * p.seq_bytes + static_cast<size_t>(t) * p.tok_bytes +
+                           static_cast<size_t>(v % vec_per_tok) * 16;
+        if (p.which == 0) {
+            uint4* d = reinterpret_cast<uint4*>(p.dev + off);
+            *reinterpret_cast<uint4*>(p.host + off) = *d;
+            if (p.poison) *d = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+        } else {
+            *reinterpret_cast<uint4*>(p.dev + off) = *reinterpret_cast<const uint4*>(p.host + off);
+        }
     }
 }
 
@@ -427,6 +454,24 @@ cudaError_t launch_ledger(const LedgerParams& p, int batch, bool pdl, cudaStream
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
     e = cudaLaunchKernelEx(&cfg, ledger_step_kernel, p);
+    count_launch();
+    return e;
+}
+
+cudaError_t launch_move(const MoveParams& p, int batch, int max_tokens, bool pdl, cudaStream_t st) {
+    const long long vecs = static_cast<long long>(max_tokens) * (p.tok_bytes / 16);
+    const int blocks = static_cast<int>(std::min<long long>((vecs + 255) / 256, 64));
+    if (blocks <= 0) return cudaSuccess;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(blocks, batch);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kv_move_kernel, p);
     count_launch();
     return e;
 }

@@ -38,4 +38,19 @@ struct LedgerParams {
     int store_current; // mark token `existing` stored on device afterwards (store_new)
 };
 
+// apply_actions data movement (engine.hpp:686-716) for one layer: the rows of
+// the tokens in one action list move between the device cache and the pinned,
+// device-mapped host tier (same [B][Ncap][2][H][row] layout in both).
+struct MoveParams {
+    uint8_t* dev;        // layer base of the device cache
+    uint8_t* host;       // layer base of the host tier (mapped pinned memory)
+    const int* lists;    // [B][4][list_ld]
+    const int* counts;   // [B][4]
+    long long list_ld;
+    long long tok_bytes; // 2*H*row bytes
+    long long seq_bytes; // Ncap * tok_bytes
+    int which;           // 0 offload (device -> host), 2 reload (host -> device)
+    int poison;          // offload: overwrite the device row with 0xFF (NaN) afterwards
+};
+
 }  // namespace skvd
