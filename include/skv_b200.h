@@ -217,6 +217,11 @@ skv_status skv_step_actions(skv_cache* cache, int layer, int j, const int32_t* s
 skv_status skv_last_actions(const skv_cache* cache, int layer, int32_t* lists_out, int32_t* counts_out,
                             void* stream);
 
+/* The tcgen05 GEMM recompute_kv uses (C = A . Bt^T; A [M x K], Bt [N x K]
+ * row-major fp16 (bf16 != 0: bf16), C [M x N] fp32; M % 128, N % 256,
+ * K % 64 == 0). Exposed for tests. */
+skv_status skv_gemm_tn(const void* A, const void* Bt, float* C, int M, int N, int K, int bf16, void* stream);
+
 /* ---- device memory helpers for hosts without the CUDA headers (the C++
  * mirror include/skv/b200.hpp uses these). skv_copy is cudaMemcpyDefault
  * (any direction, UVA) on `stream`, then synchronizes that stream. */

@@ -88,6 +88,7 @@ def _declare(lib):
         "skv_ledger_get": (I, [P, I, I, I, I, P, P]),
         "skv_step_actions": (I, [P, I, I, P, I, I, I, P, P, P]),
         "skv_last_actions": (I, [P, I, P, P, P]),
+        "skv_gemm_tn": (I, [P, P, P, I, I, I, I, P]),
         "skv_device_alloc": (I, [I, SZ, P]),
         "skv_device_free": (I, [P]),
         "skv_copy": (I, [P, P, SZ, P]),

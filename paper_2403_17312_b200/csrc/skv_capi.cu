@@ -905,6 +905,14 @@ skv_status skv_last_actions(const skv_cache* c, int layer, int32_t* lists_out, i
     return SKV_OK;
 }
 
+skv_status skv_gemm_tn(const void* A, const void* Bt, float* C, int M, int N, int K, int bf16, void* stream) {
+    SKV_REQUIRE(A && Bt && C, "gemm: null argument");
+    SKV_REQUIRE(M > 0 && M % 128 == 0 && N > 0 && N % 256 == 0 && K > 0 && K % 64 == 0,
+                "gemm: M % 128, N % 256, K % 64 must be 0");
+    SKV_CUDA(launch_gemm_tn(A, Bt, C, nullptr, M, N, K, bf16 != 0, as_stream(stream)));
+    return SKV_OK;
+}
+
 skv_status skv_device_alloc(int device, size_t bytes, void** out) {
     SKV_REQUIRE(out != nullptr, "skv_device_alloc: null output");
     DeviceGuard guard(device);

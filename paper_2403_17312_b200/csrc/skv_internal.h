@@ -31,6 +31,9 @@ cudaError_t launch_cache_write(int kv_dtype, int q_dtype, uint8_t* kv, double* i
 cudaError_t launch_cache_read(int kv_dtype, const uint8_t* kv, float* out, int H, int Ncap, int b0, int nb,
                               int t0, int nt, cudaStream_t st);
 
+cudaError_t launch_gemm_tn(const void* A, const void* Bt, float* C, const int* m_dev, int M_cap, int N, int K,
+                           bool bf16, cudaStream_t st);
+
 // Fused decode kernel: one instantiation per (kv dtype, q dtype, HG).
 struct DecodeLaunch {
     const void* func;
