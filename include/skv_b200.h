@@ -201,6 +201,14 @@ skv_status skv_cache_set_plan(skv_cache* cache, const skv_plan* plan);
  * device row with NaN, so any read of a non-resident row shows up), reloads
  * copy host -> device -- apply_actions (engine.hpp:686-716). */
 skv_status skv_cache_enable_host_tier(skv_cache* cache, int poison);
+/* recompute_kv (engine.hpp:718-737) sources for `layer`: the caller's retained
+ * post-LN1 rows x_ln1 [B][capacity][H*D] (stay owned by the caller, must live
+ * as long as the attachment) and the projections Wk, Wv [H*D][H*D] row-major
+ * (k = x . Wk), copied transposed. With the host tier and a plan, every step
+ * then re-derives the ledger's recompute list with one tcgen05 GEMM and writes
+ * the K/V rows back. fp16/bf16 caches; x_ln1 = NULL detaches. */
+skv_status skv_cache_attach_recompute(skv_cache* cache, int layer, const void* x_ln1, const void* wk,
+                                      const void* wv, void* stream);
 /* KvLedger tiers per token (memsim.hpp:72): 0 Device, 1 Host, 2 Deleted,
  * 255 not stored. src/dst: [nb][len] bytes (host or device). skv_cache_write
  * marks written tokens Device (store_new). */

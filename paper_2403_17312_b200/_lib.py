@@ -79,6 +79,7 @@ def _declare(lib):
         "skv_dequantize": (I, [P, SZ, SZ, P, P, P, P]),
         "skv_cache_set_plan": (I, [P, P]),
         "skv_cache_enable_host_tier": (I, [P, I]),
+        "skv_cache_attach_recompute": (I, [P, I, P, P, P, P]),
         "skv_solve_plan": (I, [P, P, P]),
         "skv_predict_plan": (I, [P, P, P]),
         "skv_cache_set_variant": (I, [P, I, I]),

@@ -326,6 +326,14 @@ class SwaCache:
     def enable_host_tier(self, poison: bool = False):
         check(lib().skv_cache_enable_host_tier(self._h, int(poison)))
 
+    def attach_recompute(self, layer: int, x_ln1: torch.Tensor, wk: torch.Tensor, wv: torch.Tensor):
+        # recompute_kv sources (engine.hpp:718-737); x_ln1 [B, capacity, H*D] is kept by reference
+        self._rec = getattr(self, "_rec", {})
+        self._rec[layer] = x_ln1
+        check(lib().skv_cache_attach_recompute(self._h, layer, _ptr(x_ln1), _ptr(wk.contiguous()),
+                                               _ptr(wv.contiguous()), _stream(x_ln1)))
+        torch.cuda.current_stream(self.dev).synchronize()
+
     def clear_plan(self):
         check(lib().skv_cache_set_plan(self._h, None))
 

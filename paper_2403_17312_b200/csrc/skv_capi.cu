@@ -109,6 +109,13 @@ struct skv_cache {
     int* act_counts = nullptr; // [L][B][4]
     double* sparsity = nullptr;  // [L][B] attention_sparsity of the last step's row
     uint8_t* host_kv = nullptr;  // host tier: mapped pinned mirror of the device layout (or null)
+    // recompute_kv sources (engine.hpp:718-737): per layer the caller's retained
+    // post-LN1 rows [B][Ncap][h] and our transposed [Wk | Wv]^T [2h][h]
+    std::vector<const uint8_t*> rec_x;
+    std::vector<uint8_t*> rec_wt;
+    uint8_t* rec_a = nullptr;  // gathered rows [B*Ncap][h]
+    int2* rec_map = nullptr;   // [B*Ncap] (b, t)
+    int* rec_m = nullptr;      // gathered row count
     bool poison = false;         // offload overwrites device rows (checks residency)
     int variant = SKV_VARIANT_SWA, stride = 0;  // SparsityConfig (attention.hpp:15-21)
     bool has_plan = false;
@@ -223,6 +230,8 @@ skv_status skv_cache_create(const skv_cache_desc* desc, skv_cache** out) {
     c->pend_n.assign(d.layers, -1);
     c->pend_r.assign(d.layers, 0.0);
     c->ledger_j.assign(d.layers, -1);
+    c->rec_x.assign(d.layers, nullptr);
+    c->rec_wt.assign(d.layers, nullptr);
     if (meta_bytes) SKV_CUDA(cudaMemset(c->meta, 0, meta_bytes));
     SKV_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, d.device));
     SKV_CUDA(cudaDeviceGetAttribute(&c->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, d.device));
@@ -243,6 +252,10 @@ skv_status skv_cache_destroy(skv_cache* c) {
     cudaFree(c->act_counts);
     cudaFree(c->sparsity);
     if (c->host_kv) cudaFreeHost(c->host_kv);
+    for (uint8_t* w : c->rec_wt) cudaFree(w);
+    cudaFree(c->rec_a);
+    cudaFree(c->rec_map);
+    cudaFree(c->rec_m);
     cudaFree(c->stage);
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -567,6 +580,24 @@ skv_status launch_movement(skv_cache* c, int layer, bool pdl, cudaStream_t st) {
     SKV_CUDA(launch_move(mp, c->d.batch, c->d.capacity, pdl, st));
     mp.which = 2;
     SKV_CUDA(launch_move(mp, c->d.batch, c->d.capacity, true, st));
+    if (c->rec_x[layer]) {
+        // recompute_kv for this step's list: gather the retained rows, one
+        // tcgen05 GEMM against [Wk | Wv]^T, K/V written straight into the rows
+        const long long h = static_cast<long long>(c->d.heads) * c->d.head_dim;
+        const long long xrow = h * static_cast<long long>(dtype_size(c->d.q_dtype));
+        SKV_CUDA(launch_recompute_gather(c->rec_x[layer], xrow * c->d.capacity, xrow, mp.lists, mp.counts,
+                                         c->d.capacity, c->rec_a, c->rec_map, c->rec_m, c->d.batch, st));
+        skvd::KvScatter sc{};
+        sc.kv = mp.dev;
+        sc.rowmap = c->rec_map;
+        sc.H = c->d.heads;
+        sc.D = c->d.head_dim;
+        sc.Ncap = c->d.capacity;
+        sc.row_bytes = static_cast<int>(c->row_bytes);
+        const int m_cap = static_cast<int>((static_cast<long long>(c->d.batch) * c->d.capacity + 127) / 128 * 128);
+        SKV_CUDA(launch_gemm_tn(c->rec_a, c->rec_wt[layer], nullptr, c->rec_m, m_cap, static_cast<int>(2 * h),
+                                static_cast<int>(h), c->d.q_dtype == SKV_BF16, st, &sc));
+    }
     return SKV_OK;
 }
 
@@ -801,6 +832,40 @@ skv_status skv_cache_enable_host_tier(skv_cache* c, int poison) {
         c->host_kv = static_cast<uint8_t*>(h);
     }
     c->poison = poison != 0;
+    return SKV_OK;
+}
+
+skv_status skv_cache_attach_recompute(skv_cache* c, int layer, const void* x_ln1, const void* wk, const void* wv,
+                                      void* stream) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    SKV_REQUIRE(layer >= 0 && layer < c->d.layers, "KvLedger: layer out of range");
+    if (!(c->d.kv_dtype == c->d.q_dtype && (c->d.q_dtype == SKV_F16 || c->d.q_dtype == SKV_BF16)))
+        return fail(SKV_ERR_UNSUPPORTED, "recompute: fp16/bf16 caches only");
+    const long long h = static_cast<long long>(c->d.heads) * c->d.head_dim;
+    if (h % 256 != 0) return fail(SKV_ERR_UNSUPPORTED, "recompute: hidden %lld not a multiple of 256", h);
+    DeviceGuard guard(c->d.device);
+    if (x_ln1 == nullptr) {
+        c->rec_x[layer] = nullptr;
+        return SKV_OK;
+    }
+    SKV_REQUIRE(wk && wv, "recompute: null weights");
+    const cudaStream_t st = as_stream(stream);
+    auto grab = [&](void** p, size_t bytes) -> bool {
+        if (*p) return true;
+        if (cudaMalloc(p, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return true;
+    };
+    const size_t rows = static_cast<size_t>((static_cast<long long>(c->d.batch) * c->d.capacity + 127) / 128 * 128);
+    if (!grab(reinterpret_cast<void**>(&c->rec_wt[layer]), static_cast<size_t>(2 * h * h) * 2) ||
+        !grab(reinterpret_cast<void**>(&c->rec_a), rows * static_cast<size_t>(h) * 2) ||
+        !grab(reinterpret_cast<void**>(&c->rec_map), rows * sizeof(int2)) ||
+        !grab(reinterpret_cast<void**>(&c->rec_m), sizeof(int)))
+        return fail(SKV_ERR_OOM, "recompute: cannot allocate buffers");
+    SKV_CUDA(launch_transpose_kv_weights(wk, wv, c->rec_wt[layer], static_cast<int>(h), st));
+    c->rec_x[layer] = static_cast<const uint8_t*>(x_ln1);
     return SKV_OK;
 }
 

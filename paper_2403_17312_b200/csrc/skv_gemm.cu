@@ -68,10 +68,11 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                  : "memory");
 }
 
-template <bool BF16>
+template <bool BF16, bool SCATTER>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                   float* __restrict__ C, const int* __restrict__ m_dev, int M_cap, int N, int K) {
+                   float* __restrict__ C, const int* __restrict__ m_dev, int M_cap, int N, int K,
+                   const KvScatter sc) {
     extern __shared__ __align__(1024) uint8_t gsm_raw[];
     uint8_t* gsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(gsm + kGemmStages * kGemmStageBytes);
@@ -150,11 +151,37 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 : "r"(taddr));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             if (row < M) {
-                float4* dst = reinterpret_cast<float4*>(C + static_cast<size_t>(row) * N + n0 + c * 32);
+                if constexpr (!SCATTER) {
+                    float4* dst = reinterpret_cast<float4*>(C + static_cast<size_t>(row) * N + n0 + c * 32);
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
-                                         __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+                    for (int i = 0; i < 8; ++i)
+                        dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                             __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+                } else {
+                    const int2 bt = sc.rowmap[row];
+                    const int hidden = sc.H * sc.D;
+                    const int j = n0 + c * 32;
+                    const int kvsel = j / hidden, hh = (j % hidden) / sc.D, d = j % sc.D;
+                    uint8_t* dst = sc.kv + ((static_cast<size_t>(bt.x) * sc.Ncap + bt.y) * 2 + kvsel) *
+                                               static_cast<size_t>(sc.H) * sc.row_bytes +
+                                   static_cast<size_t>(hh) * sc.row_bytes + static_cast<size_t>(d) * 2;
+                    uint32_t packed[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const float a = __uint_as_float(v[2 * i]), b = __uint_as_float(v[2 * i + 1]);
+                        if constexpr (BF16) {
+                            const __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+                            memcpy(&packed[i], &h2, 4);
+                        } else {
+                            const __half2 h2 = __floats2half2_rn(a, b);
+                            memcpy(&packed[i], &h2, 4);
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        reinterpret_cast<uint4*>(dst)[i] =
+                            make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+                }
             }
         }
     }
@@ -166,9 +193,40 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
 }
 
+// recompute_kv gather: the post-LN1 rows of this step's recompute tokens of
+// every sequence (lists from the ledger) into a dense A [M x h], with the row
+// map (b, t). One CTA per sequence; offsets by a prefix over sequences.
+__global__ void __launch_bounds__(256)
+    recompute_gather_kernel(const uint8_t* __restrict__ x, long long x_seq, long long x_row, const int* lists,
+                            const int* counts, long long list_ld, uint8_t* __restrict__ A, int2* rowmap, int* m_out,
+                            int B) {
+    const int b = blockIdx.x;
+    int off = 0;
+    for (int i = 0; i < b; ++i) off += counts[i * 4 + 3];
+    const int cnt = counts[b * 4 + 3];
+    const int* list = lists + (static_cast<size_t>(b) * 4 + 3) * list_ld;
+    const long long vecs = x_row / 16;
+    for (long long v = threadIdx.x; v < static_cast<long long>(cnt) * vecs; v += blockDim.x) {
+        const int i = static_cast<int>(v / vecs);
+        const int t = list[i];
+        const uint4* src = reinterpret_cast<const uint4*>(x + b * x_seq + static_cast<long long>(t) * x_row);
+        reinterpret_cast<uint4*>(A + static_cast<size_t>(off + i) * x_row)[v % vecs] = src[v % vecs];
+        if (v % vecs == 0) rowmap[off + i] = make_int2(b, t);
+    }
+    if (b == B - 1 && threadIdx.x == 0) *m_out = off + cnt;
+}
+
 }  // namespace skvd
 
 namespace skv_impl {
+
+cudaError_t launch_recompute_gather(const uint8_t* x, long long x_seq, long long x_row, const int* lists,
+                                    const int* counts, long long list_ld, uint8_t* A, int2* rowmap, int* m_out,
+                                    int B, cudaStream_t st) {
+    skvd::recompute_gather_kernel<<<B, 256, 0, st>>>(x, x_seq, x_row, lists, counts, list_ld, A, rowmap, m_out, B);
+    count_launch();
+    return cudaGetLastError();
+}
 using namespace skvd;
 
 namespace {
@@ -210,23 +268,26 @@ bool make_map(CUtensorMap* m, const void* base, bool bf16, uint64_t rows, uint64
 // Rows >= *m_dev (when given) are skipped. N % 256 == 0, K % 64 == 0,
 // M_cap % 128 == 0.
 cudaError_t launch_gemm_tn(const void* A, const void* Bt, float* C, const int* m_dev, int M_cap, int N, int K,
-                           bool bf16, cudaStream_t st) {
+                           bool bf16, cudaStream_t st, const KvScatter* sc) {
     if (N % kGemmBN || K % kGemmBK || M_cap % kGemmBM || M_cap <= 0) return cudaErrorInvalidValue;
     CUtensorMap ma, mb;
     if (!make_map(&ma, A, bf16, static_cast<uint64_t>(M_cap), static_cast<uint64_t>(K), kGemmBM) ||
         !make_map(&mb, Bt, bf16, static_cast<uint64_t>(N), static_cast<uint64_t>(K), kGemmBN))
         return cudaErrorInvalidValue;
-    const void* fn = bf16 ? reinterpret_cast<const void*>(&gemm_tn_kernel<true>)
-                          : reinterpret_cast<const void*>(&gemm_tn_kernel<false>);
+    const void* fns[4] = {reinterpret_cast<const void*>(&gemm_tn_kernel<false, false>),
+                          reinterpret_cast<const void*>(&gemm_tn_kernel<true, false>),
+                          reinterpret_cast<const void*>(&gemm_tn_kernel<false, true>),
+                          reinterpret_cast<const void*>(&gemm_tn_kernel<true, true>)};
+    const void* fn = fns[(bf16 ? 1 : 0) + (sc ? 2 : 0)];
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
     if (e != cudaSuccess) return e;
+    KvScatter none{};
+    const KvScatter& s = sc ? *sc : none;
     dim3 grid(N / kGemmBN, M_cap / kGemmBM);
-    if (bf16)
-        gemm_tn_kernel<true><<<grid, kGemmThreads, kGemmSmem, st>>>(ma, mb, C, m_dev, M_cap, N, K);
-    else
-        gemm_tn_kernel<false><<<grid, kGemmThreads, kGemmSmem, st>>>(ma, mb, C, m_dev, M_cap, N, K);
+    void* args[] = {&ma, &mb, &C, const_cast<int**>(&m_dev), &M_cap, &N, &K, const_cast<KvScatter*>(&s)};
+    e = cudaLaunchKernel(fn, grid, dim3(kGemmThreads), args, kGemmSmem, st);
     count_launch();
-    return cudaGetLastError();
+    return e;
 }
 
 }  // namespace skv_impl

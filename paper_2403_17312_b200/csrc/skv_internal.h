@@ -17,6 +17,7 @@ void count_launch();
 
 cudaError_t launch_select(const skvd::SelectParams& p, int batch, bool pdl, cudaStream_t st);
 cudaError_t launch_ledger(const skvd::LedgerParams& p, int batch, bool pdl, cudaStream_t st);
+cudaError_t launch_transpose_kv_weights(const void* wk, const void* wv, void* bt, int h, cudaStream_t st);
 cudaError_t launch_move(const skvd::MoveParams& p, int batch, int max_tokens, bool pdl, cudaStream_t st);
 cudaError_t launch_top_k(const double* v, int batch, long long ld, int len, int k, int* out,
                          cudaStream_t st);
@@ -31,8 +32,22 @@ cudaError_t launch_cache_write(int kv_dtype, int q_dtype, uint8_t* kv, double* i
 cudaError_t launch_cache_read(int kv_dtype, const uint8_t* kv, float* out, int H, int Ncap, int b0, int nb,
                               int t0, int nt, cudaStream_t st);
 
+}  // namespace skv_impl
+namespace skvd {
+// Epilogue target of the recompute GEMM (skv_gemm.cu): output row r is token
+// rowmap[r] = (b, t); column j < h is K, else V, of head (j mod h) / D.
+struct KvScatter {
+    uint8_t* kv;          // layer base of the cache, rows of `row_bytes`
+    const int2* rowmap;   // [M] (b, t)
+    int H, D, Ncap, row_bytes;
+};
+}
+namespace skv_impl {
 cudaError_t launch_gemm_tn(const void* A, const void* Bt, float* C, const int* m_dev, int M_cap, int N, int K,
-                           bool bf16, cudaStream_t st);
+                           bool bf16, cudaStream_t st, const skvd::KvScatter* sc = nullptr);
+cudaError_t launch_recompute_gather(const uint8_t* x, long long x_seq, long long x_row, const int* lists,
+                                    const int* counts, long long list_ld, uint8_t* A, int2* rowmap, int* m_out,
+                                    int B, cudaStream_t st);
 
 // Fused decode kernel: one instantiation per (kv dtype, q dtype, HG).
 struct DecodeLaunch {

@@ -155,6 +155,20 @@ __global__ void __launch_bounds__(kLedgerThreads) ledger_step_kernel(const Ledge
     }
 }
 
+// Bt [2h x h] = [Wk | Wv]^T for the recompute GEMM (16-bit elements);
+// W* are [h x h] row-major (out = x . W). 32 x 32 tiles through smem.
+__global__ void transpose_kv_weights_kernel(const uint16_t* __restrict__ wk, const uint16_t* __restrict__ wv,
+                                            uint16_t* __restrict__ bt, int h) {
+    __shared__ uint16_t tile[32][33];
+    const int which = blockIdx.z;
+    const uint16_t* w = which ? wv : wk;
+    const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;  // rows i (input), cols j (output) of W
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) tile[r][threadIdx.x] = w[static_cast<size_t>(i0 + r) * h + j0 + threadIdx.x];
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y)
+        bt[static_cast<size_t>(which * h + j0 + r) * h + i0 + threadIdx.x] = tile[threadIdx.x][r];
+}
+
 // Offload / reload the rows of one action list: grid (token chunk, sequence).
 // 16-byte vectors; the host side is mapped pinned memory (PCIe zero-copy).
 __global__ void __launch_bounds__(256) kv_move_kernel(const MoveParams p) {
@@ -474,6 +488,14 @@ cudaError_t launch_move(const MoveParams& p, int batch, int max_tokens, bool pdl
     cudaError_t e = cudaLaunchKernelEx(&cfg, kv_move_kernel, p);
     count_launch();
     return e;
+}
+
+cudaError_t launch_transpose_kv_weights(const void* wk, const void* wv, void* bt, int h, cudaStream_t st) {
+    if (h % 32) return cudaErrorInvalidValue;
+    transpose_kv_weights_kernel<<<dim3(h / 32, h / 32, 2), dim3(32, 8), 0, st>>>(
+        static_cast<const uint16_t*>(wk), static_cast<const uint16_t*>(wv), static_cast<uint16_t*>(bt), h);
+    count_launch();
+    return cudaGetLastError();
 }
 
 cudaError_t launch_top_k(const double* v, int batch, long long ld, int len, int k, int* out,
