@@ -71,7 +71,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -287,6 +287,9 @@ def main():
     cache = api.SwaCache(L, B, H, D, ncap, kv_dtype=cfg["kv"], q_dtype=cfg["q"], device=local)
     cache.set_variant(args.variant)
 
+    sampler = ClockSampler(local) if not args.profile_only else None
+    if sampler:
+        sampler.__enter__()
     # ---- prompt: random K/V for s tokens per layer, accumulator seeded from the
     # dense last row of the prompt (engine.hpp:508-512), all on device.
     g = torch.Generator(device="cuda").manual_seed(2403_17312 + args.config * 1000 + rank)
@@ -305,9 +308,6 @@ def main():
     out = torch.empty((L, B, H, D), device="cuda", dtype=qdt)
     torch.cuda.synchronize()
 
-    sampler = ClockSampler(local) if not args.profile_only else None
-    if sampler:
-        sampler.__enter__()
     n = s
     for i in range(W):
         n += 1
@@ -416,7 +416,7 @@ def main():
                          "step_note": "attend algorithmic bytes of the timed region / timed region "
                                       "(includes select kernels and launch gaps; layers chained with PDL)"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": dict(sampler.summary(), window="warmup + timed region + kernel-event pass") if sampler else None,
+            "clocks": dict(sampler.summary(), window="prompt fill + warmup + timed region + kernel passes (GPU busy throughout)") if sampler else None,
         }
         print(json.dumps(line), flush=True)
     if dist:
