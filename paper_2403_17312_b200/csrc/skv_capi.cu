@@ -328,17 +328,21 @@ skv_status skv_importance_get(const skv_cache* c, int layer, int b0, int nb, int
 
 namespace {
 
-// Pick heads-per-CTA: the smallest head group whose grid still fits in one
-// wave of resident CTAs (all CTAs stream concurrently); otherwise the largest
-// available group. SKV_HG overrides (tuning).
+// Pick heads-per-CTA. Bigger head groups mean bigger bulk copies (the
+// producer's per-copy issue cost is the limiter, profiles/r1_v3_*) and fewer
+// per-CTA select/softmax phases; layer-to-layer PDL overlap covers a grid
+// smaller than one wave. So: the largest group that still gives >= half an
+// SM's worth of CTAs per SM count; for tiny batches the smallest group (most
+// parallelism). SKV_HG overrides (tuning).
 skv_status pick_attend(skv_cache* c, int m, const DecodeLaunch** dl_out, size_t* smem_out) {
     static const int env_hg = [] {
         const char* s = std::getenv("SKV_HG");
         return s ? std::atoi(s) : 0;
     }();
-    const int cands[4] = {1, 2, 4, 8};
-    const DecodeLaunch* best = nullptr;
-    size_t best_smem = 0;
+    const int cands[4] = {8, 4, 2, 1};
+    const DecodeLaunch* chosen = nullptr;
+    const DecodeLaunch* smallest = nullptr;
+    size_t chosen_smem = 0, smallest_smem = 0;
     for (int hg : cands) {
         if (c->d.heads % hg != 0) continue;
         if (env_hg && hg != env_hg) continue;
@@ -346,21 +350,28 @@ skv_status pick_attend(skv_cache* c, int m, const DecodeLaunch** dl_out, size_t*
         if (!dl) continue;
         const size_t smem = dl->smem(m);
         if (smem > static_cast<size_t>(c->max_smem)) continue;
-        best = dl;
-        best_smem = smem;
-        SKV_CUDA(cudaFuncSetAttribute(dl->func, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
-        int occ = 0;
-        SKV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dl->func, skvd::kDecodeThreads, smem));
-        c->last_occ = occ;
+        smallest = dl;
+        smallest_smem = smem;
         const long long ctas = static_cast<long long>(c->d.batch) * (c->d.heads / hg);
-        if (occ > 0 && ctas <= static_cast<long long>(occ) * c->num_sms) break;
+        if (!chosen && 2 * ctas >= c->num_sms) {
+            chosen = dl;
+            chosen_smem = smem;
+        }
     }
-    if (!best)
+    if (!chosen) {
+        chosen = smallest;
+        chosen_smem = smallest_smem;
+    }
+    if (!chosen)
         return fail(SKV_ERR_UNSUPPORTED, "no attend kernel fits (heads %d, m %d, shared memory %d)", c->d.heads, m,
                     c->max_smem);
-    *dl_out = best;
-    *smem_out = best_smem;
+    SKV_CUDA(cudaFuncSetAttribute(chosen->func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(chosen_smem)));
+    int occ = 0;
+    SKV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chosen->func, skvd::kDecodeThreads, chosen_smem));
+    c->last_occ = occ;
+    *dl_out = chosen;
+    *smem_out = chosen_smem;
     return SKV_OK;
 }
 
