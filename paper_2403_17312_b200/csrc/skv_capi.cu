@@ -115,6 +115,7 @@ struct skv_cache {
     std::vector<uint8_t*> rec_wt;
     uint8_t* rec_a = nullptr;  // gathered rows [B*Ncap][h]
     int2* rec_map = nullptr;   // [B*Ncap] (b, t)
+    unsigned* counters = nullptr;  // [L][B] attend-tail arrival counters (zero between launches)
     int* rec_m = nullptr;      // gathered row count
     bool poison = false;         // offload overwrites device rows (checks residency)
     int variant = SKV_VARIANT_SWA, stride = 0;  // SparsityConfig (attention.hpp:15-21)
@@ -199,6 +200,7 @@ skv_status skv_cache_create(const skv_cache_desc* desc, skv_cache** out) {
     const size_t list_bytes = static_cast<size_t>(d.layers) * d.batch * 4 * d.capacity * 4;
     const size_t acnt_bytes = static_cast<size_t>(d.layers) * d.batch * 4 * 4;
     const size_t sp_bytes = static_cast<size_t>(d.layers) * d.batch * 8;
+    const size_t ctr_bytes = static_cast<size_t>(d.layers) * d.batch * 4;
     auto alloc = [&](void** p, size_t bytes) -> bool {
         if (bytes == 0) return true;
         if (cudaMalloc(p, bytes) != cudaSuccess) {
@@ -216,7 +218,8 @@ skv_status skv_cache_create(const skv_cache_desc* desc, skv_cache** out) {
         !alloc(reinterpret_cast<void**>(&c->tiers), tier_bytes) ||
         !alloc(reinterpret_cast<void**>(&c->act_lists), list_bytes) ||
         !alloc(reinterpret_cast<void**>(&c->act_counts), acnt_bytes) ||
-        !alloc(reinterpret_cast<void**>(&c->sparsity), sp_bytes)) {
+        !alloc(reinterpret_cast<void**>(&c->sparsity), sp_bytes) ||
+        !alloc(reinterpret_cast<void**>(&c->counters), ctr_bytes)) {
         const uint64_t want = kv_bytes + meta_bytes + imp_bytes + wpart_bytes + cnt_bytes + tier_bytes + list_bytes +
                               acnt_bytes;
         skv_cache_destroy(c);
@@ -227,6 +230,7 @@ skv_status skv_cache_create(const skv_cache_desc* desc, skv_cache** out) {
     SKV_CUDA(cudaMemset(c->tiers, 0xFF, tier_bytes));
     SKV_CUDA(cudaMemset(c->act_counts, 0, acnt_bytes));
     SKV_CUDA(cudaMemset(c->sparsity, 0, sp_bytes));
+    SKV_CUDA(cudaMemset(c->counters, 0, ctr_bytes));
     c->pend_n.assign(d.layers, -1);
     c->pend_r.assign(d.layers, 0.0);
     c->ledger_j.assign(d.layers, -1);
@@ -251,6 +255,7 @@ skv_status skv_cache_destroy(skv_cache* c) {
     cudaFree(c->act_lists);
     cudaFree(c->act_counts);
     cudaFree(c->sparsity);
+    cudaFree(c->counters);
     if (c->host_kv) cudaFreeHost(c->host_kv);
     for (uint8_t* w : c->rec_wt) cudaFree(w);
     cudaFree(c->rec_a);
@@ -436,9 +441,11 @@ int* layer_idx(const skv_cache* c, int layer) {
 // The per-sequence select kernel for one layer: optionally fold the attend
 // kernel's weight partials into the importance, optionally select for
 // (n_next, r_next) into the layer's index buffer (recorded as pending).
-skv_status launch_select_c(skv_cache* c, int layer, int apply, const int* tok_prev, long long tok_prev_ld,
-                           int m_prev, int G, int cur_tok, int n_next, double r_next, bool pdl, cudaStream_t st,
-                           int sp_n = 0) {
+// SelectParams for one layer: fold the last attend's partials (apply != 0)
+// and/or select for (n_next, r_next) (n_next <= 0: no selection).
+skv_status make_select_params(skv_cache* c, int layer, int apply, const int* tok_prev, long long tok_prev_ld,
+                              int m_prev, int G, int cur_tok, int n_next, double r_next, int sp_n,
+                              skvd::SelectParams* out) {
     skvd::SelectParams p{};
     p.sp_n = apply ? sp_n : 0;
     p.sparsity = c->sparsity + static_cast<size_t>(layer) * c->d.batch;
@@ -454,7 +461,6 @@ skv_status launch_select_c(skv_cache* c, int layer, int apply, const int* tok_pr
     p.idx = layer_idx(c, layer);
     p.idx_ld = c->d.capacity;
     p.pdl_wait = 1;
-    c->pend_n[layer] = -1;
     if (n_next > 0 && n_next <= c->d.capacity) {
         StepShape s;
         if (skv_status e = step_shape(c, n_next, r_next, &s)) return e;
@@ -468,21 +474,64 @@ skv_status launch_select_c(skv_cache* c, int layer, int apply, const int* tok_pr
         p.variant = c->variant == SKV_VARIANT_DENSE ? SKV_VARIANT_SWA : c->variant;
         p.stride = s.stride;
     }
-    if (!p.apply && !p.select) return SKV_OK;
-    SKV_CUDA(launch_select(p, c->d.batch, pdl, st));
-    if (p.select) {
-        c->pend_n[layer] = n_next;
-        c->pend_r[layer] = r_next;
-    }
+    *out = p;
     return SKV_OK;
 }
 
+// Key bytes the selection needs in shared memory (0 for index generators).
+size_t select_key_bytes(const skvd::SelectParams& p) {
+    if (!p.select || p.dense || p.variant == 2 || p.variant == 3) return 0;
+    return static_cast<size_t>(p.n - p.k) * 8;
+}
+
+void note_pending(skv_cache* c, int layer, const skvd::SelectParams& p, double r_next) {
+    if (p.select) {
+        c->pend_n[layer] = p.n;
+        c->pend_r[layer] = r_next;
+    } else {
+        c->pend_n[layer] = -1;
+    }
+}
+
+// The standalone per-sequence select kernel (skv_select.cuh).
+skv_status launch_select_c(skv_cache* c, int layer, int apply, const int* tok_prev, long long tok_prev_ld,
+                           int m_prev, int G, int cur_tok, int n_next, double r_next, bool pdl, cudaStream_t st,
+                           int sp_n = 0) {
+    skvd::SelectParams p;
+    c->pend_n[layer] = -1;
+    if (skv_status e = make_select_params(c, layer, apply, tok_prev, tok_prev_ld, m_prev, G, cur_tok, n_next, r_next,
+                                          sp_n, &p))
+        return e;
+    if (!p.apply && !p.select) return SKV_OK;
+    SKV_CUDA(launch_select(p, c->d.batch, pdl, st));
+    note_pending(c, layer, p, r_next);
+    return SKV_OK;
+}
+
+// What an attend launch folds in its tail (apply 0: nothing).
+struct FoldSpec {
+    int apply = 0;    // 1 add (cur_tok assigned), 2 assign all
+    int cur_tok = -1;
+    int sp_n = 0;     // sparsity row length (0: skip)
+    int n_next = 0;   // select for the next step (0: none)
+    double r_next = 0.0;
+};
+
 skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok, long long tok_ld, bool append,
                            const void* q, const void* k_new, const void* v_new, void* out, int32_t* idx_out,
-                           float* w_out, bool pdl, cudaStream_t st, int* G_out) {
+                           float* w_out, bool pdl, cudaStream_t st, int* G_out, const FoldSpec& fold = FoldSpec{}) {
     const DecodeLaunch* dl = nullptr;
     size_t smem = 0;
     if (skv_status s = pick_attend(c, m, &dl, &smem)) return s;
+    const int G = c->d.heads / dl->hg;
+    skvd::SelectParams sel{};
+    bool fused = fold.apply != 0;
+    if (fused) {
+        if (skv_status e = make_select_params(c, layer, fold.apply, nullptr, 0, m, G, fold.cur_tok, fold.n_next,
+                                              fold.r_next, fold.sp_n, &sel))
+            return e;
+        if (select_key_bytes(sel) > dl->ring_bytes) fused = false;  // too many keys for the tail's buffer
+    }
     const size_t lt = static_cast<size_t>(layer) * c->d.batch * c->d.capacity;
     skvd::AttendParams p{};
     p.kv = c->kv + layer * c->layer_bytes;
@@ -505,7 +554,12 @@ skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok
     p.out_f32 = c->d.out_f32 ? 1 : 0;
     p.pdl_wait = 0;  // inputs are complete before the first (non-PDL) launch of a call
     p.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d.head_dim)));
-    const int grid_g = c->d.heads / dl->hg;
+    if (fused) {
+        p.fold = 1;
+        p.sel = sel;
+        p.counters = c->counters + static_cast<size_t>(layer) * c->d.batch;
+    }
+    const int grid_g = G;
     *G_out = grid_g;
     c->last_hg = dl->hg;
     c->last_grid = grid_g * c->d.batch;
@@ -534,6 +588,16 @@ skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok
         SKV_CUDA(cudaEventRecord(e1, st));
         c->ev.push_back(e0);
         c->ev.push_back(e1);
+    }
+    if (fold.apply) {
+        if (fused) {
+            note_pending(c, layer, sel, fold.r_next);
+        } else {  // fold + select in the separate kernel instead
+            const int* tp = tok;
+            if (skv_status e = launch_select_c(c, layer, fold.apply, tp, tok_ld, m, G, fold.cur_tok, fold.n_next,
+                                               fold.r_next, !c->prof, st, fold.sp_n))
+                return e;
+        }
     }
     return SKV_OK;
 }
@@ -635,11 +699,14 @@ skv_status decode_layer_impl(skv_cache* c, int layer, int n, double r, const voi
         }
     }
     int G = 0;
+    FoldSpec fold;
+    fold.apply = 1;
+    fold.cur_tok = n - 1;
+    fold.sp_n = n;
+    fold.n_next = n + 1;
+    fold.r_next = r;
     if (skv_status e = launch_attend_c(c, layer, n, s.m, layer_idx(c, layer), c->d.capacity, true, q, k_new, v_new,
-                                       out, idx_out, w_out, chained && !fresh, st, &G))
-        return e;
-    if (skv_status e = launch_select_c(c, layer, 1, layer_idx(c, layer), c->d.capacity, s.m, G, n - 1, n + 1, r,
-                                       !c->prof, st, n))
+                                       out, idx_out, w_out, chained && !fresh, st, &G, fold))
         return e;
     if (c->has_plan && c->pend_n[layer] == n + 1) {
         // the next step's KV residency actions (scheduler.hpp:320-381) on the
@@ -669,10 +736,10 @@ skv_status skv_prefill_seed(skv_cache* c, int layer, int n, const void* q_last, 
     DeviceGuard guard(c->d.device);
     const cudaStream_t st = as_stream(stream);
     int G = 0;
-    if (skv_status e = launch_attend_c(c, layer, n, n, nullptr, 0, false, q_last, nullptr, nullptr, out, nullptr,
-                                       nullptr, false, st, &G))
-        return e;
-    return launch_select_c(c, layer, 2, nullptr, 0, n, G, -1, 0, 0.0, true, st);
+    FoldSpec fold;
+    fold.apply = 2;  // engine.hpp:508-512: the seed assigns
+    return launch_attend_c(c, layer, n, n, nullptr, 0, false, q_last, nullptr, nullptr, out, nullptr, nullptr, false,
+                           st, &G, fold);
 }
 
 skv_status skv_swa_decode_layer(skv_cache* c, int layer, int n, double r, const void* q, const void* k_new,
@@ -759,10 +826,11 @@ skv_status skv_attend_over_indices(skv_cache* c, int layer, int n, const int32_t
                         "attend_over_indices: indices must be strictly ascending");
         }
     int G = 0;
-    if (skv_status e = launch_attend_c(c, layer, n, m, idx, m, false, q, nullptr, nullptr, out, nullptr, w_out,
-                                       false, st, &G))
-        return e;
-    return launch_select_c(c, layer, 1, idx, m, m, G, -1, 0, 0.0, true, st, n);
+    FoldSpec fold;
+    fold.apply = 1;  // acc[idx] += w (attention.hpp:219-227)
+    fold.sp_n = n;
+    return launch_attend_c(c, layer, n, m, idx, m, false, q, nullptr, nullptr, out, nullptr, w_out, false, st, &G,
+                           fold);
 }
 
 skv_status skv_swa_select(const double* importance, int batch, int64_t ld, int n, double r, int32_t* idx_out,

@@ -15,7 +15,8 @@ size_t smem_of(int m) {
 template <class KV, class QT, int HG>
 DecodeLaunch make() {
     return DecodeLaunch{reinterpret_cast<const void*>(&swa_attend_kernel<KV, QT, HG>),
-                        &smem_of<KV, QT, HG>, HG};
+                        &smem_of<KV, QT, HG>, HG,
+                        static_cast<size_t>(DecodeCfg<KV, HG>::S) * DecodeCfg<KV, HG>::STAGEB};
 }
 
 struct Entry {

@@ -22,6 +22,7 @@
 #pragma once
 
 #include "skv_device.cuh"
+#include "skv_select.cuh"
 
 #ifndef SKV_STAGE_BYTES
 #define SKV_STAGE_BYTES 16384
@@ -64,6 +65,12 @@ struct AttendParams {
     int B, H, Ncap, n, m;
     int append, out_f32, pdl_wait;
     float scale;
+    // Tail (fold != 0): the last CTA of each sequence folds the head-group
+    // weight partials into the fp64 importance and selects the next step
+    // (fold_and_select, skv_select.cuh) -- no separate select launch.
+    int fold;
+    unsigned* counters;  // [B], zero between launches
+    SelectParams sel;    // imp / wpart / apply / cur_tok / sparsity / next selection; tok_prev = this CTA's list
 };
 
 template <class KV, int HG>
@@ -93,7 +100,7 @@ struct DecodeCfg {
 };
 
 struct DecodeSmem {
-    size_t ring, bars, tok, wts, flag, total;
+    size_t ring, bars, tok, wts, topk, scratch, flag, total;
 };
 
 // Shared-memory carve-up; identical on host (launch size) and device.
@@ -110,6 +117,10 @@ __host__ __device__ inline DecodeSmem decode_smem(int m) {
     o = align_up(o + static_cast<size_t>(m) * 4, 16);
     s.wts = o;  // logits, then weights [HG][m] f32
     o = align_up(o + static_cast<size_t>(HG) * m * 4, 16);
+    s.topk = o;
+    o = align_up(o + sizeof(TopkSmem<kConsumerThreads>), 16);
+    s.scratch = o;
+    o = align_up(o + sizeof(SelectScratch<kConsumerThreads>), 16);
     s.flag = o;
     o += 16;
     s.total = o;
@@ -481,6 +492,30 @@ __global__ void __launch_bounds__(kDecodeThreads)
             static_cast<float*>(p.out)[at] = s;
         else
             static_cast<QT*>(p.out)[at] = from_f<QT>(s);
+    }
+
+    // ---- tail: the last CTA of the sequence folds the G partials (fixed
+    // group order, deterministic) into the importance and selects the next
+    // step's tokens, while the other sequences' CTAs keep streaming.
+    if (p.fold) {
+        int* s_last = reinterpret_cast<int*>(smem + L.flag);
+        named_sync(kBarConsumers, kConsumerThreads);  // ring free: it becomes the key buffer
+        if (ctid == 0) {
+            __threadfence();
+            const unsigned prev = atomicAdd(&p.counters[b], 1u);
+            *s_last = (prev == static_cast<unsigned>(G - 1)) ? 1 : 0;
+        }
+        named_sync(kBarConsumers, kConsumerThreads);
+        if (*s_last) {
+            __threadfence();
+            SelectParams sp = p.sel;
+            sp.tok_prev = tok;  // this CTA's (shared) token list, same for every group
+            sp.tok_prev_ld = 0;
+            fold_and_select<kConsumerThreads, kBarConsumers>(
+                sp, b, ctid, *reinterpret_cast<TopkSmem<kConsumerThreads>*>(smem + L.topk),
+                reinterpret_cast<uint64_t*>(ring), *reinterpret_cast<SelectScratch<kConsumerThreads>*>(smem + L.scratch));
+            if (ctid == 0) p.counters[b] = 0;
+        }
     }
 }
 

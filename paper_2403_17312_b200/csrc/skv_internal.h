@@ -54,6 +54,7 @@ struct DecodeLaunch {
     const void* func;
     size_t (*smem)(int m);
     int hg;
+    size_t ring_bytes;  // shared-memory ring (reused for the tail's selection keys)
 };
 // Returns nullptr when no kernel is compiled for the combination.
 const DecodeLaunch* find_decode(int kv_dtype, int q_dtype, int hg);

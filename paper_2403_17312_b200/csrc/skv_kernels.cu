@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(kLedgerThreads) ledger_step_kernel(const Ledge
     constexpr int NT = kLedgerThreads;
     constexpr uint64_t M21 = (1ull << 21) - 1;
     __shared__ uint64_t wt[NT / 32];
-    extern __shared__ __align__(16) uint8_t smem[];
+    extern __shared__ __align__(128) uint8_t smem[];
     const int b = blockIdx.x, tid = threadIdx.x;
     pdl_launch_dependents();
     pdl_wait();  // the selection comes from the preceding select kernel
@@ -196,85 +196,19 @@ __global__ void __launch_bounds__(256) kv_move_kernel(const MoveParams p) {
 
 // Importance fold + next selection, one CTA per sequence (skv_select.cuh).
 __global__ void __launch_bounds__(kSelectThreads) swa_select_kernel(const SelectParams p) {
-    extern __shared__ __align__(16) uint8_t smem[];
+    extern __shared__ __align__(128) uint8_t smem[];
     TopkSmem<kSelectThreads>& s = *reinterpret_cast<TopkSmem<kSelectThreads>*>(smem);
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem + align_up(sizeof(TopkSmem<kSelectThreads>), 16));
-    const int b = blockIdx.x, tid = threadIdx.x;
+    __shared__ SelectScratch<kSelectThreads> scratch;
     pdl_launch_dependents();
     if (p.pdl_wait) pdl_wait();
-    double* imp = p.imp + static_cast<size_t>(b) * p.imp_ld;
-    __shared__ double red_max[kSelectThreads / 32];
-    __shared__ int red_cnt[kSelectThreads / 32];
-    if (p.apply) {
-        const float* wp = p.wpart + static_cast<size_t>(b) * p.G * p.m_prev;
-        const int* tp = p.tok_prev ? p.tok_prev + static_cast<size_t>(b) * p.tok_prev_ld : nullptr;
-        double vmax = 0.0;
-        for (int pos = tid; pos < p.m_prev; pos += kSelectThreads) {
-            double v = 0.0;
-            for (int g = 0; g < p.G; ++g) v += static_cast<double>(wp[static_cast<size_t>(g) * p.m_prev + pos]);
-            const int t = tp ? tp[pos] : pos;
-            imp[t] = (p.apply == 2 || t == p.cur_tok) ? v : imp[t] + v;
-            vmax = v > vmax ? v : vmax;
-        }
-        if (p.sp_n > 0) {
-            // attention_sparsity (attention.hpp:275-310) of the head-summed step
-            // row new_aw_row (length sp_n, zeros off-selection), threshold 0.01
-            const int lane = tid & 31, warp = tid >> 5;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                const double o = __shfl_xor_sync(0xffffffffu, vmax, off);
-                vmax = o > vmax ? o : vmax;
-            }
-            if (lane == 0) red_max[warp] = vmax;
-            __syncthreads();
-            double mx = 0.0;
-            for (int w = 0; w < kSelectThreads / 32; ++w) mx = red_max[w] > mx ? red_max[w] : mx;
-            const double thr = 0.01 * mx;
-            int below = 0;
-            for (int pos = tid; pos < p.m_prev; pos += kSelectThreads) {
-                double v = 0.0;
-                for (int g = 0; g < p.G; ++g) v += static_cast<double>(wp[static_cast<size_t>(g) * p.m_prev + pos]);
-                below += v < thr;
-            }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) below += __shfl_xor_sync(0xffffffffu, below, off);
-            if (lane == 0) red_cnt[warp] = below;
-            __syncthreads();
-            if (tid == 0) {
-                int cnt = 0;
-                for (int w = 0; w < kSelectThreads / 32; ++w) cnt += red_cnt[w];
-                const int sparse = mx == 0.0 ? p.sp_n : cnt + (p.sp_n - p.m_prev);
-                p.sparsity[b] = static_cast<double>(sparse) / static_cast<double>(p.sp_n);
-            }
-        }
-    }
-    if (!p.select) return;
-    __syncthreads();
-    int* o = p.idx + static_cast<size_t>(b) * p.idx_ld;
-    if (p.variant == 2) {  // local_attention_mask (attention.hpp:247-256): the last m tokens
-        for (int i = tid; i < p.m; i += kSelectThreads) o[i] = p.n - p.m + i;
-        return;
-    }
-    if (p.variant == 3) {  // strided_attention_mask (attention.hpp:258-269), phased onto n-1
-        const int phase = (p.n - 1) % p.stride;
-        for (int i = tid; i < p.m; i += kSelectThreads) o[i] = phase + i * p.stride;
-        return;
-    }
-    if (p.dense) {
-        for (int i = tid; i < p.m; i += kSelectThreads) o[i] = i;
-        return;
-    }
-    const int nc = p.n - p.k;
-    for (int i = tid; i < nc; i += kSelectThreads) keys[i] = order_key(imp[i]);
-    named_sync(1, kSelectThreads);
-    block_topk<kSelectThreads, 1>(keys, nc, p.k, o, s, tid);  // global picks, ascending
-    for (int i = tid; i < p.k; i += kSelectThreads) o[p.k + i] = p.n - p.k + i;  // local window
+    fold_and_select<kSelectThreads, 1>(p, blockIdx.x, threadIdx.x, s, keys, scratch);
 }
 
 // top_k_indices (matrix.hpp:162-176) per row.
 __global__ void __launch_bounds__(kSelThreads)
     top_k_kernel(const double* __restrict__ v, long long ld, int len, int k, int* __restrict__ out) {
-    extern __shared__ __align__(16) uint8_t smem[];
+    extern __shared__ __align__(128) uint8_t smem[];
     TopkSmem<kSelThreads>& s = *reinterpret_cast<TopkSmem<kSelThreads>*>(smem);
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem + align_up(sizeof(TopkSmem<kSelThreads>), 16));
     const int b = blockIdx.x, tid = threadIdx.x;

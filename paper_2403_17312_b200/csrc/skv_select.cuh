@@ -43,6 +43,85 @@ __host__ __device__ inline size_t select_smem(int nc) {
     return align_up(sizeof(TopkSmem<kSelectThreads>), 16) + static_cast<size_t>(nc > 0 ? nc : 0) * 8;
 }
 
-// The kernel itself is defined in skv_kernels.cu.
+template <int NT>
+struct SelectScratch {
+    double red_max[NT / 32];
+    int red_cnt[NT / 32];
+};
+
+// The body shared by swa_select_kernel and the attend kernel's tail: NT
+// threads synchronised on named barrier BAR, sequence b. keys: shared memory
+// for n-k order keys. Weight partials are read through L2 (__ldcg): in the
+// attend tail they come from sibling CTAs of the same grid.
+template <int NT, int BAR>
+__device__ void fold_and_select(const SelectParams& p, int b, int tid, TopkSmem<NT>& s, uint64_t* keys,
+                                SelectScratch<NT>& sc) {
+    double* imp = p.imp + static_cast<size_t>(b) * p.imp_ld;
+    if (p.apply) {
+        const float* wp = p.wpart + static_cast<size_t>(b) * p.G * p.m_prev;
+        const int* tp = p.tok_prev ? p.tok_prev + static_cast<size_t>(b) * p.tok_prev_ld : nullptr;
+        double vmax = 0.0;
+        for (int pos = tid; pos < p.m_prev; pos += NT) {
+            double v = 0.0;
+            for (int g = 0; g < p.G; ++g) v += static_cast<double>(__ldcg(wp + static_cast<size_t>(g) * p.m_prev + pos));
+            const int t = tp ? tp[pos] : pos;
+            imp[t] = (p.apply == 2 || t == p.cur_tok) ? v : imp[t] + v;
+            vmax = v > vmax ? v : vmax;
+        }
+        if (p.sp_n > 0) {
+            // attention_sparsity (attention.hpp:275-310) of the head-summed step
+            // row new_aw_row (length sp_n, zeros off-selection), threshold 0.01
+            const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double o = __shfl_xor_sync(0xffffffffu, vmax, off);
+                vmax = o > vmax ? o : vmax;
+            }
+            if (lane == 0) sc.red_max[warp] = vmax;
+            named_sync(BAR, NT);
+            double mx = 0.0;
+            for (int w = 0; w < NT / 32; ++w) mx = sc.red_max[w] > mx ? sc.red_max[w] : mx;
+            const double thr = 0.01 * mx;
+            int below = 0;
+            for (int pos = tid; pos < p.m_prev; pos += NT) {
+                double v = 0.0;
+                for (int g = 0; g < p.G; ++g)
+                    v += static_cast<double>(__ldcg(wp + static_cast<size_t>(g) * p.m_prev + pos));
+                below += v < thr;
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) below += __shfl_xor_sync(0xffffffffu, below, off);
+            if (lane == 0) sc.red_cnt[warp] = below;
+            named_sync(BAR, NT);
+            if (tid == 0) {
+                int cnt = 0;
+                for (int w = 0; w < NT / 32; ++w) cnt += sc.red_cnt[w];
+                const int sparse = mx == 0.0 ? p.sp_n : cnt + (p.sp_n - p.m_prev);
+                p.sparsity[b] = static_cast<double>(sparse) / static_cast<double>(p.sp_n);
+            }
+        }
+    }
+    if (!p.select) return;
+    named_sync(BAR, NT);  // the folded importance (this thread block's writes) is visible
+    int* o = p.idx + static_cast<size_t>(b) * p.idx_ld;
+    if (p.variant == 2) {  // local_attention_mask (attention.hpp:247-256): the last m tokens
+        for (int i = tid; i < p.m; i += NT) o[i] = p.n - p.m + i;
+        return;
+    }
+    if (p.variant == 3) {  // strided_attention_mask (attention.hpp:258-269), phased onto n-1
+        const int phase = (p.n - 1) % p.stride;
+        for (int i = tid; i < p.m; i += NT) o[i] = phase + i * p.stride;
+        return;
+    }
+    if (p.dense) {
+        for (int i = tid; i < p.m; i += NT) o[i] = i;
+        return;
+    }
+    const int nc = p.n - p.k;
+    for (int i = tid; i < nc; i += NT) keys[i] = order_key(imp[i]);
+    named_sync(BAR, NT);
+    block_topk<NT, BAR>(keys, nc, p.k, o, s, tid);                  // global picks, ascending
+    for (int i = tid; i < p.k; i += NT) o[p.k + i] = p.n - p.k + i;  // local window
+}
 
 }  // namespace skvd
