@@ -1,6 +1,7 @@
 // skv_capi.cu -- the C ABI (include/skv_b200.h): argument checking with the
 // reference's error semantics, the device cache object, kernel selection and
 // launch, host-buffer step, and the measurement hooks used by bench.py.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -530,7 +531,11 @@ skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok
         if (skv_status e = make_select_params(c, layer, fold.apply, nullptr, 0, m, G, fold.cur_tok, fold.n_next,
                                               fold.r_next, fold.sp_n, &sel))
             return e;
-        if (select_key_bytes(sel) > dl->ring_bytes) fused = false;  // too many keys for the tail's buffer
+        // The tail's selection runs on one CTA per sequence while it holds its
+        // attend slot: worth it for short candidate lists (configs 2/3: step
+        // 0.98->1.02, 0.88->1.01), not for n-k in the thousands (config 4:
+        // 0.88->0.79), which keep the separate select kernel.
+        if (select_key_bytes(sel) > std::min<size_t>(dl->ring_bytes, 2048 * 8)) fused = false;
     }
     const size_t lt = static_cast<size_t>(layer) * c->d.batch * c->d.capacity;
     skvd::AttendParams p{};
