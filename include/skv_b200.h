@@ -95,6 +95,21 @@ skv_status skv_importance_get(const skv_cache* cache, int layer, int b0, int nb,
 skv_status skv_prefill_seed(skv_cache* cache, int layer, int n, const void* q_last, void* out,
                             void* stream);
 
+/* Engine::prefill's attention for one layer (engine.hpp:485-529) on tcgen05
+ * tensor cores: causal dense_attention (attention.hpp:91-117) of the s prompt
+ * queries over cached tokens [0, s) (written first with skv_cache_write),
+ * importance[0, s) set to the head-summed last attention row
+ * (engine.hpp:508-512) and the per-sequence prefill sparsity recorded
+ * (engine.hpp:513-518). fp16/bf16 caches only. q: device [B][s][H][D]
+ * q_dtype; out: device [B][s][H][D] (fp32 when out_f32). */
+skv_status skv_prefill_layer(skv_cache* cache, int layer, int s, const void* q, void* out, void* stream);
+/* Mean over heads of attention_sparsity(aw, 0.01, causal) of the last
+ * skv_prefill_layer on `layer`, per sequence: dst [B] (host or device). */
+skv_status skv_prefill_sparsity_get(const skv_cache* cache, int layer, double* dst, void* stream);
+/* Diagnostics: the prefill scratch (S fp32, P, V^T, last rows; see
+ * skv_prefill.cu) of the last skv_prefill_layer. */
+skv_status skv_prefill_scratch(const skv_cache* cache, void** base, size_t* bytes);
+
 /* ---- the hot path ---------------------------------------------------------
  * One SWA decode step of one layer for all B sequences, in the engine's
  * order (engine.hpp:592-629): append the new K/V as token n-1, select from

@@ -249,6 +249,24 @@ class SwaCache:
         check(lib().skv_prefill_seed(self._h, layer, n, _ptr(q_last), _ptr(out), _stream(q_last)))
         return out
 
+    # Engine::prefill's attention (engine.hpp:485-529) on tensor cores: the
+    # prompt's K/V must already be in the cache (append_tokens); returns the
+    # causal attention output [B][s][H][D] and seeds the importance.
+    def prefill_layer(self, layer: int, q: torch.Tensor) -> torch.Tensor:
+        if q.dim() != 4 or q.shape[0] != self.batch or q.shape[2:] != (self.heads, self.head_dim):
+            raise ContractViolation(f"prefill: q must be [B][s][H][D], got {tuple(q.shape)}")
+        s = q.shape[1]
+        self._q(q, (self.batch, s, self.heads, self.head_dim))
+        out = torch.empty(q.shape, dtype=self.out_dtype, device=self.dev)
+        check(lib().skv_prefill_layer(self._h, layer, s, _ptr(q), _ptr(out), _stream(q)))
+        return out
+
+    def prefill_sparsity(self, layer: int) -> torch.Tensor:
+        # engine.hpp:513-518 per sequence: mean over heads of the causal sparsity
+        out = torch.empty(self.batch, dtype=torch.float64, device=self.dev)
+        check(lib().skv_prefill_sparsity_get(self._h, layer, _ptr(out), _stream(out)))
+        return out
+
     # One decode step of one layer (engine.hpp:592-629 order; swa_attention)
     def swa_decode_layer(self, layer: int, n: int, r: float, q, k_new, v_new, out=None,
                          return_indices: bool = False, return_weights: bool = False):

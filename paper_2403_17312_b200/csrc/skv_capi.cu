@@ -128,6 +128,11 @@ struct skv_cache {
     uint64_t device_bytes = 0;
     int num_sms = 0;
     int max_smem = 0;
+    // tensor-core prefill: scratch (grown on demand) and per-(layer, b)
+    // prefill sparsity (engine.hpp:513-518)
+    uint8_t* pf_scratch = nullptr;
+    size_t pf_bytes = 0;
+    double* pf_sparsity = nullptr;
     // host-buffer step staging
     uint8_t* stage = nullptr;
     size_t stage_bytes = 0;
@@ -263,6 +268,8 @@ skv_status skv_cache_destroy(skv_cache* c) {
     cudaFree(c->rec_map);
     cudaFree(c->rec_m);
     cudaFree(c->stage);
+    cudaFree(c->pf_scratch);
+    cudaFree(c->pf_sparsity);
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     delete c;
@@ -745,6 +752,71 @@ skv_status skv_prefill_seed(skv_cache* c, int layer, int n, const void* q_last, 
     fold.apply = 2;  // engine.hpp:508-512: the seed assigns
     return launch_attend_c(c, layer, n, n, nullptr, 0, false, q_last, nullptr, nullptr, out, nullptr, nullptr, false,
                            st, &G, fold);
+}
+
+// Engine::prefill's attention for one layer (engine.hpp:485-529) on tensor
+// cores: dense causal attention of the s prompt queries over the s cached
+// tokens, importance seeded with the head-summed last row, prefill sparsity
+// recorded. See skv_prefill.cu.
+skv_status skv_prefill_layer(skv_cache* c, int layer, int s, const void* q, void* out, void* stream) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    SKV_REQUIRE(layer >= 0 && layer < c->d.layers, "KvLedger: layer out of range");
+    SKV_REQUIRE(s >= 1 && s <= c->d.capacity, "prefill: prompt length out of range");
+    SKV_REQUIRE(q != nullptr && out != nullptr, "prefill: null argument");
+    if (!(c->d.kv_dtype == c->d.q_dtype && (c->d.q_dtype == SKV_F16 || c->d.q_dtype == SKV_BF16)))
+        return fail(SKV_ERR_UNSUPPORTED, "prefill: tensor-core prefill needs an fp16/bf16 cache");
+    DeviceGuard guard(c->d.device);
+    const cudaStream_t st = as_stream(stream);
+    const int B = c->d.batch, H = c->d.heads;
+    const size_t per_seq = prefill_scratch_bytes(c->d.q_dtype == SKV_BF16, 1, H, c->d.head_dim, s);
+    // scratch budget: 8 GiB (SKV_PREFILL_BUDGET bytes overrides), at least one sequence
+    size_t budget = size_t(8) << 30;
+    if (const char* env = std::getenv("SKV_PREFILL_BUDGET")) budget = static_cast<size_t>(std::atoll(env));
+    const size_t want = per_seq * std::min<size_t>(B, std::max<size_t>(1, budget / per_seq));
+    if (c->pf_bytes < want) {
+        SKV_CUDA(cudaStreamSynchronize(st));
+        cudaFree(c->pf_scratch);
+        c->pf_scratch = nullptr;
+        c->pf_bytes = 0;
+        if (cudaMalloc(reinterpret_cast<void**>(&c->pf_scratch), want) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(SKV_ERR_OOM, "prefill: cannot allocate %zu scratch bytes", want);
+        }
+        c->pf_bytes = want;
+    }
+    if (c->pf_sparsity == nullptr) {
+        const size_t bytes = static_cast<size_t>(c->d.layers) * B * 8;
+        if (cudaMalloc(reinterpret_cast<void**>(&c->pf_sparsity), bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(SKV_ERR_OOM, "prefill: cannot allocate sparsity");
+        }
+        SKV_CUDA(cudaMemset(c->pf_sparsity, 0, bytes));
+    }
+    const size_t lay = static_cast<size_t>(layer);
+    SKV_CUDA(launch_prefill(c->d.q_dtype == SKV_BF16, c->d.out_f32 != 0, c->kv + lay * c->layer_bytes, q, out,
+                            c->imp + lay * B * c->d.capacity, c->d.capacity, c->pf_sparsity + lay * B, B, H,
+                            c->d.head_dim, c->d.capacity, s, c->pf_scratch, want, st));
+    c->pend_n[layer] = -1;  // importance changed: any pending selection is stale
+    return SKV_OK;
+}
+
+skv_status skv_prefill_scratch(const skv_cache* c, void** base, size_t* bytes) {
+    SKV_REQUIRE(c != nullptr && base != nullptr && bytes != nullptr, "null argument");
+    *base = c->pf_scratch;
+    *bytes = c->pf_bytes;
+    return SKV_OK;
+}
+
+skv_status skv_prefill_sparsity_get(const skv_cache* c, int layer, double* dst, void* stream) {
+    SKV_REQUIRE(c != nullptr && dst != nullptr, "null argument");
+    SKV_REQUIRE(layer >= 0 && layer < c->d.layers, "KvLedger: layer out of range");
+    SKV_REQUIRE(c->pf_sparsity != nullptr, "prefill sparsity: no tensor-core prefill has run");
+    DeviceGuard guard(c->d.device);
+    const cudaStream_t st = as_stream(stream);
+    SKV_CUDA(cudaMemcpyAsync(dst, c->pf_sparsity + static_cast<size_t>(layer) * c->d.batch,
+                             static_cast<size_t>(c->d.batch) * 8, cudaMemcpyDefault, st));
+    SKV_CUDA(cudaStreamSynchronize(st));
+    return SKV_OK;
 }
 
 skv_status skv_swa_decode_layer(skv_cache* c, int layer, int n, double r, const void* q, const void* k_new,

@@ -1,0 +1,128 @@
+"""GPU parity of the tensor-core prefill against the oracle.
+
+Engine::prefill (engine.hpp:485-529): causal dense_attention per head
+(attention.hpp:91-117), each head's accumulator seeded with its last attention
+row (engine.hpp:508-512), prefill sparsity = mean over heads of
+attention_sparsity(aw, 0.01, causal) (engine.hpp:513-518).
+
+Tolerances: outputs 1e-3 (fp16/bf16 inputs; north_star; bf16 caches with
+fp32 outputs), importance 1e-4
+relative (fp32 weights on device, like the decode path), sparsity within
+2e-3 absolute (cells within fp32 rounding of the 0.01 x max threshold may
+count differently).
+"""
+import numpy as np
+import pytest
+import torch
+
+from skv_testlib import TOL, OracleSeq, assert_close, round_to, selection_flip_is_tie
+
+pytestmark = pytest.mark.gpu
+
+TD = {"f16": torch.float16, "bf16": torch.bfloat16}
+
+
+@pytest.fixture(scope="module")
+def api():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2403_17312_b200 import api as a
+
+    a.lib()
+    return a
+
+
+def cuda(x, dtype):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(device="cuda", dtype=dtype)
+
+
+def _case(api, port, dt, B, H, s, ncap, seed, out_f32=False):
+    D = 128
+    rng = np.random.default_rng(seed)
+    k = round_to(rng.standard_normal((B, s, H, D)), dt)
+    v = round_to(rng.standard_normal((B, s, H, D)), dt)
+    q = round_to(rng.standard_normal((B, s, H, D)) * 0.5, dt)
+    cache = api.SwaCache(2, B, H, D, ncap, kv_dtype=dt, out_f32=out_f32)
+    layer = 1
+    cache.append_tokens(layer, 0, 0, cuda(k, TD[dt]), cuda(v, TD[dt]))
+    out = cache.prefill_layer(layer, cuda(q, TD[dt])).float().cpu().numpy()
+    imp = cache.importance(layer, s).cpu().numpy()
+    sp = cache.prefill_sparsity(layer).cpu().numpy()
+    for b in range(B):
+        seed_row = np.zeros(s)
+        sp_ref = 0.0
+        for h in range(H):
+            attn, aw = port.dense_attention(q[b, :, h], k[b, :, h], v[b, :, h], True)
+            assert_close(out[b, :, h], attn, TOL[dt], f"prefill {dt} b{b} h{h}")
+            seed_row += aw[s - 1]
+            sp_ref += port.attention_sparsity(aw, 0.01, True)
+        np.testing.assert_allclose(imp[b], seed_row, rtol=1e-4, atol=1e-7)
+        assert abs(sp[b] - sp_ref / H) <= 2e-3, (b, sp[b], sp_ref / H)
+    return cache, (q, k, v)
+
+
+@pytest.mark.parametrize("dt", ["f16", "bf16"])
+@pytest.mark.parametrize("s", [1, 77, 128, 200, 300])
+def test_prefill_matches_dense_attention(api, port, dt, s):
+    # a bf16 output alone rounds at 2^-9 relative: bf16 caches report fp32
+    # outputs (out_f32), as in the decode parity tests
+    _case(api, port, dt, B=2, H=4, s=s, ncap=s + 19, seed=s, out_f32=(dt == "bf16"))
+
+
+def test_prefill_fp32_output(api, port):
+    _case(api, port, "f16", B=1, H=2, s=257, ncap=300, seed=3, out_f32=True)
+
+
+def test_prefill_chunked_batch(api, port, monkeypatch):
+    # a scratch budget of one sequence: the batch runs in B chunks
+    monkeypatch.setenv("SKV_PREFILL_BUDGET", "1")
+    _case(api, port, "bf16", B=3, H=2, s=129, ncap=140, seed=4, out_f32=True)
+
+
+def test_prefill_long_prompt(api, port):
+    # several query and key tiles, causal tile skipping, the K-range clip of PV
+    _case(api, port, "f16", B=1, H=2, s=1100, ncap=1100, seed=11)
+
+
+def test_prefill_then_decode(api, port):
+    """Prefill on tensor cores, then SWA decode steps: selections and outputs
+    follow the oracle engine order (engine.hpp:592-629)."""
+    dt, B, H, D, s, steps, r = "f16", 2, 4, 128, 150, 6, 0.25
+    ncap = s + steps
+    rng = np.random.default_rng(21)
+    kv = round_to(rng.standard_normal((B, ncap, 2, H, D)), dt)
+    q0 = round_to(rng.standard_normal((B, s, H, D)) * 0.5, dt)
+    qs = round_to(rng.standard_normal((steps, B, H, D)) * 2.0, dt)
+    cache = api.SwaCache(1, B, H, D, ncap, kv_dtype=dt, out_f32=True)
+    cache.append_tokens(0, 0, 0, cuda(kv[:, :s, 0], TD[dt]), cuda(kv[:, :s, 1], TD[dt]))
+    cache.prefill_layer(0, cuda(q0, TD[dt]))
+    seqs = [OracleSeq(port, H, D, ncap) for _ in range(B)]
+    for b in range(B):
+        for t in range(s):
+            seqs[b].append(t, kv[b, t, 0], kv[b, t, 1])
+        for h in range(H):
+            _, aw = port.dense_attention(q0[b, :, h], seqs[b].keys[h, :s], seqs[b].vals[h, :s], True)
+            seqs[b].acc[h, :s] = aw[s - 1]
+    for j in range(steps):
+        n = s + j + 1
+        imp_pre = [sq.importance(n - 1) for sq in seqs]
+        out, idx, _ = cache.swa_decode_layer(0, n, r, cuda(qs[j], TD[dt]), cuda(kv[:, n - 1, 0], TD[dt]),
+                                             cuda(kv[:, n - 1, 1], TD[dt]), return_indices=True)
+        out, idx = out.cpu().numpy(), idx.cpu().numpy()
+        for b in range(B):
+            seqs[b].append(n - 1, kv[b, n - 1, 0], kv[b, n - 1, 1])
+            attn, aw, oidx = seqs[b].step(n, r, qs[j][b])
+            if not np.array_equal(idx[b], oidx):
+                assert selection_flip_is_tie(idx[b], oidx, imp_pre[b], n, api.swa_window_k(n, r)), (j, b)
+                return
+            assert_close(out[b], attn, TOL[dt], f"decode after prefill step {j}")
+
+
+def test_prefill_rejects_int8_and_bad_shapes(api):
+    c = api.SwaCache(1, 1, 2, 128, 64, kv_dtype="u8", q_dtype="f16")
+    with pytest.raises(api.Unsupported):
+        c.prefill_layer(0, torch.zeros((1, 8, 2, 128), dtype=torch.float16, device="cuda"))
+    c = api.SwaCache(1, 1, 2, 128, 64, kv_dtype="f16")
+    with pytest.raises(api.ContractViolation):
+        c.prefill_layer(0, torch.zeros((1, 65, 2, 128), dtype=torch.float16, device="cuda"))
+    with pytest.raises(api.ContractViolation):
+        c.prefill_sparsity(0)
