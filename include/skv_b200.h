@@ -106,9 +106,6 @@ skv_status skv_prefill_layer(skv_cache* cache, int layer, int s, const void* q, 
 /* Mean over heads of attention_sparsity(aw, 0.01, causal) of the last
  * skv_prefill_layer on `layer`, per sequence: dst [B] (host or device). */
 skv_status skv_prefill_sparsity_get(const skv_cache* cache, int layer, double* dst, void* stream);
-/* Diagnostics: the prefill scratch (S fp32, P, V^T, last rows; see
- * skv_prefill.cu) of the last skv_prefill_layer. */
-skv_status skv_prefill_scratch(const skv_cache* cache, void** base, size_t* bytes);
 
 /* ---- the hot path ---------------------------------------------------------
  * One SWA decode step of one layer for all B sequences, in the engine's

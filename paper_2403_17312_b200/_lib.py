@@ -71,7 +71,6 @@ def _declare(lib):
         "skv_prefill_seed": (I, [P, I, I, P, P, P]),
         "skv_prefill_layer": (I, [P, I, I, P, P, P]),
         "skv_prefill_sparsity_get": (I, [P, I, P, P]),
-        "skv_prefill_scratch": (I, [P, P, P]),
         "skv_swa_decode_layer": (I, [P, I, I, D, P, P, P, P, P, P, P]),
         "skv_swa_decode_step": (I, [P, I, D, P, P, P, P, P]),
         "skv_swa_decode_step_host": (I, [P, I, D, P, P, P, P, P]),

@@ -768,11 +768,7 @@ skv_status skv_prefill_layer(skv_cache* c, int layer, int s, const void* q, void
     DeviceGuard guard(c->d.device);
     const cudaStream_t st = as_stream(stream);
     const int B = c->d.batch, H = c->d.heads;
-    const size_t per_seq = prefill_scratch_bytes(c->d.q_dtype == SKV_BF16, 1, H, c->d.head_dim, s);
-    // scratch budget: 8 GiB (SKV_PREFILL_BUDGET bytes overrides), at least one sequence
-    size_t budget = size_t(8) << 30;
-    if (const char* env = std::getenv("SKV_PREFILL_BUDGET")) budget = static_cast<size_t>(std::atoll(env));
-    const size_t want = per_seq * std::min<size_t>(B, std::max<size_t>(1, budget / per_seq));
+    const size_t want = prefill_scratch_bytes(B, H, s);
     if (c->pf_bytes < want) {
         SKV_CUDA(cudaStreamSynchronize(st));
         cudaFree(c->pf_scratch);
@@ -795,15 +791,8 @@ skv_status skv_prefill_layer(skv_cache* c, int layer, int s, const void* q, void
     const size_t lay = static_cast<size_t>(layer);
     SKV_CUDA(launch_prefill(c->d.q_dtype == SKV_BF16, c->d.out_f32 != 0, c->kv + lay * c->layer_bytes, q, out,
                             c->imp + lay * B * c->d.capacity, c->d.capacity, c->pf_sparsity + lay * B, B, H,
-                            c->d.head_dim, c->d.capacity, s, c->pf_scratch, want, st));
+                            c->d.head_dim, c->d.capacity, s, c->pf_scratch, st));
     c->pend_n[layer] = -1;  // importance changed: any pending selection is stale
-    return SKV_OK;
-}
-
-skv_status skv_prefill_scratch(const skv_cache* c, void** base, size_t* bytes) {
-    SKV_REQUIRE(c != nullptr && base != nullptr && bytes != nullptr, "null argument");
-    *base = c->pf_scratch;
-    *bytes = c->pf_bytes;
     return SKV_OK;
 }
 

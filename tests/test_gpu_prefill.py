@@ -72,9 +72,9 @@ def test_prefill_fp32_output(api, port):
     _case(api, port, "f16", B=1, H=2, s=257, ncap=300, seed=3, out_f32=True)
 
 
-def test_prefill_chunked_batch(api, port, monkeypatch):
-    # a scratch budget of one sequence: the batch runs in B chunks
-    monkeypatch.setenv("SKV_PREFILL_BUDGET", "1")
+def test_prefill_batch_ragged(api, port):
+    # several sequences, one query row past a tile boundary, keys past s in
+    # the cache (capacity > s) that TMA must not read
     _case(api, port, "bf16", B=3, H=2, s=129, ncap=140, seed=4, out_f32=True)
 
 
