@@ -14,9 +14,10 @@
 //                   / l is final, so there is no rescaling: w is counted
 //                   against the 0.01 x row-max threshold (e < 0.01: the row
 //                   max of e is exactly 1), written out for the last query
-//                   row (the seed), stored 16-bit to shared memory and
-//                   multiplied into O += P V on the tensor cores (V read
-//                   MN-major straight from the cache tile).
+//                   row (the seed), stored 16-bit into TMEM over the S
+//                   columns it came from and multiplied into O += P V on the
+//                   tensor cores (A from TMEM, V read MN-major straight from
+//                   the cache tile).
 // Q, K, V come from the caller's q and the cache through 3D tensor maps whose
 // token extent is the prompt length s, so keys / queries >= s are zero-filled
 // by TMA and never carry uninitialised cache bytes into the MMAs.
@@ -24,7 +25,8 @@
 // allocation), warps 2..5 one query row per thread (softmax, P, epilogue).
 // bf16 keeps 8 mantissa bits, too few for the 1e-3 output bound: P is split
 // into hi + lo bf16 halves and both are multiplied against V (fp16 P, 11
-// bits, is stored once).
+// bits, is stored once). (kind::f16 needs A and B of one type, so an fp16 P
+// against bf16 V is not an option: it faults.)
 #include <cuda.h>
 
 #include <algorithm>
@@ -122,37 +124,65 @@ __host__ __device__ constexpr uint32_t flash_idesc() {
 template <bool BF16, bool STATS>
 struct FlashSmem {
     static constexpr int kQ = 0;
-    static constexpr int kK = kQ + kFTileBytes;      // 2 stages
-    static constexpr int kV = kK + 2 * kFTileBytes;  // 2 stages (pass 2)
-    static constexpr int kP = kV + (STATS ? 0 : 2 * kFTileBytes);
-    static constexpr int kBar = kP + (STATS ? 0 : (BF16 ? 2 : 1) * kFTileBytes);
+    static constexpr int kK = kQ + kFTileBytes;                    // pass 1: 2 stages, pass 2: 1
+    static constexpr int kV = kK + (STATS ? 2 : 1) * kFTileBytes;  // pass 2: 1 stage
+    static constexpr int kBar = kV + (STATS ? 0 : kFTileBytes);
     static constexpr int kBytes = kBar + 256 + 1024;  // barriers + alignment slack
 };
 
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// A operand from TMEM (P), B from shared memory (V)
+__device__ __forceinline__ void umma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(addr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+
+// Two CTAs per SM (96 KB shared memory, 256 TMEM columns, <= 168 registers
+// each) so one CTA's softmax overlaps the other's MMAs. TMEM per CTA:
+//   pass 1: S double buffer, columns [0, 256);
+//   pass 2: S / P in [0, 128) -- P is written over the S columns it came
+//           from, 32 keys per 32-column chunk: hi in the chunk's first 16
+//           columns, bf16 lo in the next 16 -- and O in [128, 256).
 template <bool BF16, bool STATS>
-__global__ void __launch_bounds__(kFThreads, 1)
+__global__ void __launch_bounds__(kFThreads, 2)
     flash_prefill_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
                          const FlashParams p) {
     using L = FlashSmem<BF16, STATS>;
-    constexpr uint32_t kCols = STATS ? 256 : 512;  // S double buffer (+ O)
+    constexpr uint32_t kCols = 256;
+    constexpr int KS = STATS ? 2 : 1;  // K stages
     extern __shared__ __align__(1024) uint8_t raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = sm + L::kQ;
     uint8_t* sK = sm + L::kK;
     uint8_t* sV = sm + L::kV;
-    uint8_t* sP = sm + L::kP;
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::kBar);
     uint64_t* q_full = bar;
-    uint64_t* k_full = bar + 1;    // [2]
-    uint64_t* k_empty = bar + 3;   // [2]
-    uint64_t* v_full = bar + 5;    // [2]
-    uint64_t* v_empty = bar + 7;   // [2]
-    uint64_t* s_full = bar + 9;    // [2]
-    uint64_t* s_empty = bar + 11;  // [2]
-    uint64_t* p_full = bar + 13;
-    uint64_t* p_empty = bar + 14;
-    uint64_t* o_full = bar + 15;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 16);
+    uint64_t* k_full = bar + 1;    // [KS]
+    uint64_t* k_empty = bar + 3;   // [KS]
+    uint64_t* v_full = bar + 5;
+    uint64_t* v_empty = bar + 6;
+    uint64_t* s_full = bar + 7;    // [2]
+    uint64_t* s_empty = bar + 9;   // [2] (pass 1)
+    uint64_t* p_full = bar + 11;
+    uint64_t* p_empty = bar + 12;
+    uint64_t* o_full = bar + 13;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 14);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int z = blockIdx.x, qt = gridDim.y - 1 - blockIdx.y;  // heaviest query tiles first
@@ -165,11 +195,11 @@ __global__ void __launch_bounds__(kFThreads, 1)
         for (int i = 0; i < 2; ++i) {
             mbar_init(&k_full[i], 1);
             mbar_init(&k_empty[i], 1);
-            mbar_init(&v_full[i], 1);
-            mbar_init(&v_empty[i], 1);
             mbar_init(&s_full[i], 1);
             mbar_init(&s_empty[i], 128);
         }
+        mbar_init(v_full, 1);
+        mbar_init(v_empty, 1);
         mbar_init(p_full, 128);
         mbar_init(p_empty, 1);
         mbar_init(o_full, 1);
@@ -193,18 +223,17 @@ __global__ void __launch_bounds__(kFThreads, 1)
             tma3d(sQ, &map_q, xq, m0, b, q_full);
             tma3d(sQ + kFHalf, &map_q, xq + 64, m0, b, q_full);
             for (int j = 0; j < T; ++j) {
-                const int st = j & 1;
-                if (j >= 2) mbar_wait(&k_empty[st], ((j >> 1) - 1) & 1);
+                const int st = j % KS;
+                if (j >= KS) mbar_wait(&k_empty[st], ((j / KS) - 1) & 1);
                 uint8_t* dk = sK + st * kFTileBytes;
                 mbar_arrive_expect_tx(&k_full[st], kFTileBytes);
                 tma3d(dk, &map_kv, xq, j * kFTile, b, &k_full[st]);
                 tma3d(dk + kFHalf, &map_kv, xq + 64, j * kFTile, b, &k_full[st]);
                 if constexpr (!STATS) {
-                    if (j >= 2) mbar_wait(&v_empty[st], ((j >> 1) - 1) & 1);
-                    uint8_t* dv = sV + st * kFTileBytes;
-                    mbar_arrive_expect_tx(&v_full[st], kFTileBytes);
-                    tma3d(dv, &map_kv, p.HD + xq, j * kFTile, b, &v_full[st]);
-                    tma3d(dv + kFHalf, &map_kv, p.HD + xq + 64, j * kFTile, b, &v_full[st]);
+                    if (j >= 1) mbar_wait(v_empty, (j - 1) & 1);
+                    mbar_arrive_expect_tx(v_full, kFTileBytes);
+                    tma3d(sV, &map_kv, p.HD + xq, j * kFTile, b, v_full);
+                    tma3d(sV + kFHalf, &map_kv, p.HD + xq + 64, j * kFTile, b, v_full);
                 }
             }
         }
@@ -214,41 +243,51 @@ __global__ void __launch_bounds__(kFThreads, 1)
             constexpr uint32_t id_s = flash_idesc<BF16, false>();
             constexpr uint32_t id_o = flash_idesc<BF16, true>();
             mbar_wait(q_full, 0);
-            auto issue_s = [&](int j) {
-                const int st = j & 1;
-                mbar_wait(&k_full[st], (j >> 1) & 1);
-                if (j >= 2) mbar_wait(&s_empty[st], ((j >> 1) - 1) & 1);
+            auto issue_s = [&](int j, uint32_t dst) {
+                const int st = j % KS;
+                mbar_wait(&k_full[st], (j / KS) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint8_t* k = sK + st * kFTileBytes;
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
                     const int off = (kk >> 2) * kFHalf + (kk & 3) * 32;
-                    umma(tmem + st * 128, desc_k(sQ + off), desc_k(k + off), id_s, kk > 0);
+                    umma(dst, desc_k(sQ + off), desc_k(k + off), id_s, kk > 0);
                 }
-                umma_commit(&s_full[st]);
                 umma_commit(&k_empty[st]);
             };
-            issue_s(0);
-            for (int j = 0; j < T; ++j) {
-                if (j + 1 < T) issue_s(j + 1);
-                if constexpr (!STATS) {
-                    const int st = j & 1;
-                    mbar_wait(&v_full[st], (j >> 1) & 1);
+            if constexpr (STATS) {
+                for (int j = 0; j < T; ++j) {
+                    const int sb = j & 1;
+                    if (j >= 2) {
+                        mbar_wait(&s_empty[sb], ((j >> 1) - 1) & 1);
+                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    }
+                    issue_s(j, tmem + sb * 128);
+                    umma_commit(&s_full[sb]);
+                }
+            } else {
+                for (int j = 0; j < T; ++j) {
+                    // S_j overwrites P_{j-1}: PV_{j-1} must have consumed it
+                    if (j >= 1) {
+                        mbar_wait(p_empty, (j - 1) & 1);
+                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    }
+                    issue_s(j, tmem);
+                    umma_commit(&s_full[0]);
+                    mbar_wait(v_full, j & 1);
                     mbar_wait(p_full, j & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint8_t* v = sV + st * kFTileBytes;
 #pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) {
-                        const int aoff = (kk >> 2) * kFHalf + (kk & 3) * 32;
-                        umma(tmem + 256, desc_k(sP + aoff), desc_mn(v + kk * 2048), id_o, (j | kk) != 0);
-                        if constexpr (BF16)
-                            umma(tmem + 256, desc_k(sP + kFTileBytes + aoff), desc_mn(v + kk * 2048), id_o, 1);
+                    for (int kk = 0; kk < 8; ++kk) {  // 16 keys: chunk kk/2, half kk%2
+                        const uint32_t pa = tmem + (kk >> 1) * 32 + (kk & 1) * 8;
+                        umma_ts(tmem + 128, pa, desc_mn(sV + kk * 2048), id_o, (j | kk) != 0);
+                        if constexpr (BF16) umma_ts(tmem + 128, pa + 16, desc_mn(sV + kk * 2048), id_o, 1);
                     }
                     umma_commit(p_empty);
-                    umma_commit(&v_empty[st]);
+                    umma_commit(v_empty);
                 }
+                umma_commit(o_full);
             }
-            if constexpr (!STATS) umma_commit(o_full);
         }
     } else {
         // ------------------------------------------------ rows: softmax / P / O
@@ -269,72 +308,63 @@ __global__ void __launch_bounds__(kFThreads, 1)
         unsigned cnt = 0;
         const bool last_row = r == p.s - 1;
         for (int j = 0; j < T; ++j) {
-            const int st = j & 1;
-            mbar_wait(&s_full[st], (j >> 1) & 1);
+            const int sb = STATS ? (j & 1) : 0;
+            mbar_wait(&s_full[sb], STATS ? ((j >> 1) & 1) : (j & 1));
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            float sv[128];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_ld32(tl + st * 128 + c * 32, sv + c * 32);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            mbar_arrive(&s_empty[st]);
             const int lim = valid ? min(r - j * kFTile, kFTile - 1) : -1;  // keys 0..lim of this tile count
-            if constexpr (STATS) {
-                if (lim >= 0) {
-                    float mx = m;
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                float sv[32];
+                const uint32_t ca = tl + sb * 128 + c * 32;
+                tmem_ld32(ca, sv);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                const int cl = lim - c * 32;  // keys 0..cl of this chunk count
+                if constexpr (STATS) {
+                    if (cl >= 0) {
+                        float mx = m;
 #pragma unroll
-                    for (int k = 0; k < 128; ++k)
-                        if (k <= lim) mx = fmaxf(mx, sv[k] * p.c1);
-                    float acc = 0.f;
+                        for (int k = 0; k < 32; ++k)
+                            if (k <= cl) mx = fmaxf(mx, sv[k] * p.c1);
+                        float acc = 0.f;
 #pragma unroll
-                    for (int k = 0; k < 128; ++k)
-                        if (k <= lim) acc += exp2f(sv[k] * p.c1 - mx);
-                    l = l * exp2f(m - mx) + acc;
-                    m = mx;
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < 128; ++k) {
-                    float e = 0.f;
-                    if (k <= lim) {
-                        e = exp2f(sv[k] * p.c1 - m);
-                        cnt += e < 0.01f;
+                        for (int k = 0; k < 32; ++k)
+                            if (k <= cl) acc += ex2(sv[k] * p.c1 - mx);
+                        l = l * ex2(m - mx) + acc;
+                        m = mx;
                     }
-                    sv[k] = e * inv_l;
-                }
-                if (last_row) {
-                    float* wl = p.wlast + zrow + j * kFTile;
+                } else {
 #pragma unroll
-                    for (int k = 0; k < 128; ++k)
-                        if (k <= lim) wl[k] = sv[k];
-                }
-                if (j > 0) mbar_wait(p_empty, (j - 1) & 1);
-                // row rl of the K-major SW128 P tile: 16-byte chunk c of a
-                // 64-key half lands at chunk c ^ (rl & 7)
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const float* w = sv + hh * 64 + c * 8;
-                        const uint32_t off = hh * kFHalf + rl * 128 + ((c ^ (rl & 7)) << 4);
-                        uint4 hi;
-                        hi.x = pack2<BF16>(w[0], w[1]);
-                        hi.y = pack2<BF16>(w[2], w[3]);
-                        hi.z = pack2<BF16>(w[4], w[5]);
-                        hi.w = pack2<BF16>(w[6], w[7]);
-                        *reinterpret_cast<uint4*>(sP + off) = hi;
-                        if constexpr (BF16) {
-                            uint4 lo;
-                            lo.x = pack2<true>(bf16_rest(w[0]), bf16_rest(w[1]));
-                            lo.y = pack2<true>(bf16_rest(w[2]), bf16_rest(w[3]));
-                            lo.z = pack2<true>(bf16_rest(w[4]), bf16_rest(w[5]));
-                            lo.w = pack2<true>(bf16_rest(w[6]), bf16_rest(w[7]));
-                            *reinterpret_cast<uint4*>(sP + kFTileBytes + off) = lo;
+                    for (int k = 0; k < 32; ++k) {
+                        float e = 0.f;
+                        if (k <= cl) {
+                            e = ex2(sv[k] * p.c1 - m);
+                            cnt += e < 0.01f;
                         }
+                        sv[k] = e * inv_l;
+                    }
+                    if (last_row) {
+                        float* wl = p.wlast + zrow + j * kFTile + c * 32;
+#pragma unroll
+                        for (int k = 0; k < 32; ++k)
+                            if (k <= cl) wl[k] = sv[k];
+                    }
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) pk[i] = pack2<BF16>(sv[2 * i], sv[2 * i + 1]);
+                    tmem_st16(ca, pk);
+                    if constexpr (BF16) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) pk[i] = pack2<true>(bf16_rest(sv[2 * i]), bf16_rest(sv[2 * i + 1]));
+                        tmem_st16(ca + 16, pk);
                     }
                 }
-                // generic-proxy stores -> visible to the tensor core's async proxy
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            }
+            if constexpr (STATS) {
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                mbar_arrive(&s_empty[sb]);
+            } else {
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 mbar_arrive(p_full);
             }
         }
@@ -344,10 +374,10 @@ __global__ void __launch_bounds__(kFThreads, 1)
             mbar_wait(o_full, 0);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const size_t row0 = (static_cast<size_t>(b) * p.s + r) * p.HD + static_cast<size_t>(h) * 128;
-#pragma unroll
+#pragma unroll 1
             for (int c = 0; c < 4; ++c) {
                 float o[32];
-                tmem_ld32(tl + 256 + c * 32, o);
+                tmem_ld32(tl + 128 + c * 32, o);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 if (!valid) continue;
                 if (p.out_f32) {
@@ -367,8 +397,6 @@ __global__ void __launch_bounds__(kFThreads, 1)
                     }
                 }
             }
-        }
-        if constexpr (!STATS) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
             if (lane == 0 && cnt) atomicAdd(&p.below[z], cnt);
