@@ -27,6 +27,7 @@ SHAPES = [  # (name, B, H, s, dtype)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--no-flash", action="store_true", help="skip the flash_attn comparison")
     args = ap.parse_args()
     td = {"f16": torch.float16, "bf16": torch.bfloat16}
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -58,6 +59,8 @@ def main():
                 "tflops": round(flops / ms / 1e9, 1), "tokens_per_s": round(B * s / ms * 1e3),
                 "peak_tflops": peaks.get("bf16_tflops")}
         try:
+            if args.no_flash:
+                raise RuntimeError("skipped (--no-flash)")
             from flash_attn import flash_attn_func
 
             for _ in range(2):
