@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <mutex>
 
 #include "skv_internal.h"
@@ -36,19 +37,21 @@
 namespace skvd {
 
 constexpr int kFTile = 128;    // query rows per tile
-constexpr int kFKeys = 64;     // keys per tile
+constexpr int kFKeys = 128;    // keys per tile (N = 128 S MMAs: an M = 128 MMA costs about the same for N <= 256)
 constexpr int kFHalf = 16384;  // one 64-column SW128 box of the 128-row Q tile
 constexpr int kFTileBytes = 2 * kFHalf;
 constexpr int kFKHalf = kFKeys * 128;  // one 64-column SW128 box of a 64-key K / V tile
 constexpr int kFKBytes = 2 * kFKHalf;
-constexpr int kFSlots = 2;  // query tiles in flight per CTA
-constexpr int kFThreads = 128 + kFSlots * 128;
+constexpr int kFBufs = 2;    // S / P buffers in TMEM, K / V stages in shared memory
+constexpr int kFHK = kFKeys / 2;  // keys per row thread per tile
+constexpr int kFThreads = 128 + 256;  // 4 control warps + 8 row warps
 
 struct FlashParams {
     int s, H, HD;
     int Z, nqt;       // work items: Z x nqt query tiles
+    int s_pad;        // nqt * 128: row stride of mrow
     float c1;         // log2(e) / sqrt(D): exp(x / sqrt(D)) = exp2(x * c1)
-    float* mrow;      // [Z][s] row max of S = Q K^T over the causal keys (pass 1)
+    float* mrow;      // [Z][s_pad] row max of S = Q K^T over the causal keys (pass 1)
     void* out;        // [B][s][H][D], 16-bit or fp32 (out_f32)
     int out_f32;
     float* wlast;     // [Z][s] the last query row's e = exp(S/sqrt(D) - max)
@@ -106,17 +109,27 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, float* v) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// a -> low half, b -> high half; one F2FP.PACK_AB (separate F2F conversions
+// would run on the XU pipe next to the exp2s)
 template <bool BF16>
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
-    if constexpr (BF16)
-        return static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(a))) |
-               (static_cast<uint32_t>(__bfloat16_as_ushort(__float2bfloat16_rn(b))) << 16);
-    else
-        return static_cast<uint32_t>(__half_as_ushort(__float2half_rn(a))) |
-               (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(b))) << 16);
+    uint32_t r;
+    if constexpr (BF16) {
+        const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+        r = *reinterpret_cast<const uint32_t*>(&h);
+    } else {
+        const __half2 h = __floats2half2_rn(a, b);
+        r = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    return r;
 }
 
-__device__ __forceinline__ float bf16_rest(float a) { return a - __bfloat162float(__float2bfloat16_rn(a)); }
+__device__ __forceinline__ float bf16_rest(float a) {
+    // a - bf16(a): bf16 rounding is exact on the fp32 bit pattern (RNE on the low 16 bits)
+    const uint32_t u = __float_as_uint(a);
+    const uint32_t hi = (u + 0x7FFFu + ((u >> 16) & 1u)) & 0xFFFF0000u;
+    return a - __uint_as_float(hi);
+}
 
 // instruction descriptor, kind::f16, fp32 accumulate, M = 128, A K-major
 template <bool BF16, bool B_MN, int N>
@@ -127,11 +140,14 @@ __host__ __device__ constexpr uint32_t flash_idesc() {
 
 template <bool BF16, bool STATS>
 struct FlashSmem {
-    // per slot: Q, K x 2 stages, V x 2 stages (pass 2)
-    static constexpr int kSlot = kFTileBytes + (STATS ? 2 : 4) * kFKBytes;
-    static constexpr int kBar = kFSlots * kSlot;
-    static constexpr int kNBar = 20;  // per slot
-    static constexpr int kBytes = kBar + kFSlots * kNBar * 8 + 16 + 1024;  // barriers, TMEM slot, alignment
+    static constexpr int kQ = 0;                                // [2] query tiles (double buffered across items)
+    static constexpr int kK = kQ + 2 * kFTileBytes;             // [kFBufs] key tiles
+    static constexpr int kV = kK + kFBufs * kFKBytes;           // [kFBufs] value tiles (pass 2)
+    static constexpr int kM = kV + (STATS ? 0 : kFBufs * kFKBytes);  // [2][128] row max (pass 2)
+    static constexpr int kR = kM + 2 * 128 * 4;                 // [2][2][128] per-half row partials
+    static constexpr int kBar = kR + 2 * 2 * 128 * 4;
+    static constexpr int kNBar = 40;
+    static constexpr int kBytes = kBar + kNBar * 8 + 16 + 1024;  // barriers, TMEM slot, alignment
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -157,18 +173,36 @@ __device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t* v) {
         : "memory");
 }
 
-// Persistent, one CTA per SM with two independent query-tile slots, so one
-// slot's softmax overlaps the other's MMAs and each slot's producer loads the
-// next work item's Q / K / V while the current item drains. Keys go in tiles
-// of 64: K and V are double buffered in shared memory and S in TMEM, so the
-// MMA for key tile g + 1 runs while the row threads work on tile g. Per slot:
-// a TMA thread, an MMA thread, a warpgroup of row threads (one query row
-// each), 96 KB of shared memory and 256 TMEM columns:
-//   S / P buffers b = 0, 1 at columns [64 b, 64 b + 64) -- P is written over
-//   the S columns it came from, 32 keys per 32-column chunk: hi in the
-//   chunk's first 16 columns, bf16 lo in the next 16 -- and O in [128, 256).
-// Warps: 0 / 2 TMA for slot 0 / 1, 1 / 3 MMA, 4..7 rows of slot 0, 8..11 rows
-// of slot 1 (warp w may touch TMEM lanes 32 (w % 4) ..).
+// Persistent, one CTA per SM over a contiguous run of work items (query
+// tiles). Keys go in tiles of 128 through a double-buffered pipeline: K / V
+// stages in shared memory, S / P buffers in TMEM, so the MMA for key tile
+// g + 1 runs while the row threads work on tile g. Q (and the pass-1 row
+// max) is double buffered across items so the next item's loads overlap the
+// current item's tail. (An M = 128 tcgen05.mma costs about the same for any
+// N <= 256 -- measured ~130 cycles per K = 16 step at N = 64 -- so the S
+// MMAs use N = 128 key tiles rather than 64.)
+// TMEM: S / P buffer b at columns [128 b, 128 b + 128) -- P is written over
+// the S columns it came from, 32 keys per 32-column chunk: hi in the first
+// 16 columns, bf16 lo in the next 16 -- and O in [256, 384).
+// Warps: 0 TMA, 1 MMA (+ TMEM allocation), 4..7 and 8..11 the row threads:
+// warp w owns rows 32 (w % 4) .. (its TMEM lane quarter) and key columns
+// 64 hf .. 64 hf + 63 of every tile (hf = 0 for warps 4..7, 1 for 8..11),
+// and O columns 64 hf .. 64 hf + 63.
+#ifdef PF_TRACE
+__device__ long long g_pft[2][8][32];
+__device__ __forceinline__ int pft_tag(const char* t) {
+    return t[0] == 't' ? 0 : t[4] == 's' && t[0] == 'm' ? 1 : t[4] == 's' ? 2 : t[4] == 'l' ? 3 : t[4] == 'm' ? 4 : t[4] == 'p' && t[0] == 'r' ? 5 : 6;
+}
+#define PFT(tag, gg)                                                                  \
+    do {                                                                              \
+        if (blockIdx.x == 0 && (gg) < 32) g_pft[STATS ? 0 : 1][pft_tag(tag)][gg] = clock64(); \
+    } while (0)
+#else
+#define PFT(tag, gg) \
+    do {             \
+    } while (0)
+#endif
+
 template <bool BF16, bool STATS>
 __global__ void __launch_bounds__(kFThreads, 1)
     flash_prefill_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
@@ -177,34 +211,38 @@ __global__ void __launch_bounds__(kFThreads, 1)
     extern __shared__ __align__(1024) uint8_t raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int slot = warp < 4 ? (warp >> 1) : (warp - 4) / 4;
-    uint8_t* sQ = sm + slot * L::kSlot;
-    uint8_t* sK = sQ + kFTileBytes;       // [2] stages
-    uint8_t* sV = sK + 2 * kFKBytes;      // [2] stages (pass 2)
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::kBar) + slot * L::kNBar;
-    uint64_t* q_full = bar;
-    uint64_t* q_empty = bar + 1;
-    uint64_t* k_full = bar + 2;    // [2]
-    uint64_t* k_empty = bar + 4;   // [2]
-    uint64_t* v_full = bar + 6;    // [2]
-    uint64_t* v_empty = bar + 8;   // [2]
-    uint64_t* s_full = bar + 10;   // [2] MMA -> rows
-    uint64_t* s_free = bar + 12;   // [2] pass 1: rows read S;      pass 2: PV consumed P
-    uint64_t* p_full = bar + 14;   // [2] pass 2: rows wrote P
-    uint64_t* o_full = bar + 16;
-    uint64_t* o_empty = bar + 17;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(reinterpret_cast<uint64_t*>(sm + L::kBar) + kFSlots * L::kNBar);
+    uint8_t* sQ = sm + L::kQ;
+    uint8_t* sK = sm + L::kK;
+    uint8_t* sV = sm + L::kV;
+    float* sM = reinterpret_cast<float*>(sm + L::kM);  // [2][128]
+    float* sR = reinterpret_cast<float*>(sm + L::kR);  // [2][2][128]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::kBar);
+    uint64_t* q_full = bar;        // [2]
+    uint64_t* q_empty = bar + 2;   // [2]
+    uint64_t* k_full = bar + 4;    // [4]
+    uint64_t* k_empty = bar + 8;   // [4]
+    uint64_t* v_full = bar + 12;   // [4]
+    uint64_t* v_empty = bar + 16;  // [4]
+    uint64_t* s_full = bar + 20;   // [4] MMA -> rows
+    uint64_t* s_free = bar + 24;   // [4] pass 1: rows read S; pass 2: PV consumed P
+    uint64_t* p_full = bar + 28;   // [4] pass 2: rows wrote P
+    uint64_t* o_full = bar + 32;
+    uint64_t* o_empty = bar + 33;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + L::kNBar);
 
-    if (threadIdx.x < kFSlots) {
-        uint64_t* bb = reinterpret_cast<uint64_t*>(sm + L::kBar) + threadIdx.x * L::kNBar;
-        for (int i = 0; i < 18; ++i) mbar_init(&bb[i], 1);
-        if (STATS) {
-            mbar_init(&bb[12], 128);
-            mbar_init(&bb[13], 128);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 34; ++i) mbar_init(&bar[i], 1);
+        if (!STATS) {
+            // Q + row-max buffer: MMA commit after the item's last S + every row
+            // thread after reading its row max
+            mbar_init(&q_empty[0], 257);
+            mbar_init(&q_empty[1], 257);
         }
-        mbar_init(&bb[14], 128);
-        mbar_init(&bb[15], 128);
-        mbar_init(&bb[17], 128);
+        for (int i = 0; i < 4; ++i) {
+            if (STATS) mbar_init(&s_free[i], 256);
+            mbar_init(&p_full[i], 256);
+        }
+        mbar_init(o_empty, 256);
         fence_barrier_init();
     }
     if (warp == 1) {
@@ -215,31 +253,36 @@ __global__ void __launch_bounds__(kFThreads, 1)
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = *tslot + slot * 256;
+    const uint32_t tmem = *tslot;
+    // Contiguous runs of items, (sequence, head)-major with the heaviest query
+    // tile first: consecutive items re-read the same K / V from L2 and the
+    // concurrent working set (one (sequence, head) per SM) stays in L2.
     const int items = p.Z * p.nqt;
-    // Each slot takes a contiguous run of items; items are (sequence, head)-
-    // major with the heaviest query tile first, so a slot's consecutive items
-    // re-read the same K / V from L2 and the concurrent working set (one
-    // (sequence, head) per slot) stays far below the 126 MB L2.
-    const int nslot = gridDim.x * kFSlots, sl = blockIdx.x * kFSlots + slot;
-    const int first = static_cast<int>(static_cast<long long>(items) * sl / nslot);
-    const int last = static_cast<int>(static_cast<long long>(items) * (sl + 1) / nslot);
+    const int first = static_cast<int>(static_cast<long long>(items) * blockIdx.x / gridDim.x);
+    const int last = static_cast<int>(static_cast<long long>(items) * (blockIdx.x + 1) / gridDim.x);
 
-    if (warp < 4 && (warp & 1) == 0) {
+    if (warp == 0) {
         // ---------------------------------------------------------------- TMA
         if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
             int g = 0, n = 0;
             for (int it = first; it < last; ++it, ++n) {
                 const int qt = p.nqt - 1 - it % p.nqt, z = it / p.nqt;
                 const int b = z / p.H, xq = (z % p.H) * 128;
-                const int T = 2 * (qt + 1);
-                if (n >= 1) mbar_wait(q_empty, (n - 1) & 1);
-                mbar_arrive_expect_tx(q_full, kFTileBytes);
-                tma3d(sQ, &map_q, xq, qt * kFTile, b, q_full);
-                tma3d(sQ + kFHalf, &map_q, xq + 64, qt * kFTile, b, q_full);
+                const int T = qt + 1;
+                const int qb = n & 1;
+                if (n >= 2) mbar_wait(&q_empty[qb], ((n >> 1) - 1) & 1);
+                mbar_arrive_expect_tx(&q_full[qb], kFTileBytes + (STATS ? 0 : 512));
+                uint8_t* dq = sQ + qb * kFTileBytes;
+                tma3d(dq, &map_q, xq, qt * kFTile, b, &q_full[qb]);
+                tma3d(dq + kFHalf, &map_q, xq + 64, qt * kFTile, b, &q_full[qb]);
+                if constexpr (!STATS)
+                    bulk_g2s(sM + qb * 128, p.mrow + static_cast<size_t>(z) * p.s_pad + qt * kFTile, 512,
+                             &q_full[qb], pol);
                 for (int j = 0; j < T; ++j, ++g) {
                     const int st = g & 1;
                     if (g >= 2) mbar_wait(&k_empty[st], ((g >> 1) - 1) & 1);
+                    PFT("tma_k", g);
                     uint8_t* dk = sK + st * kFKBytes;
                     mbar_arrive_expect_tx(&k_full[st], kFKBytes);
                     tma3d(dk, &map_kv, xq, j * kFKeys, b, &k_full[st]);
@@ -254,45 +297,52 @@ __global__ void __launch_bounds__(kFThreads, 1)
                 }
             }
         }
-    } else if (warp < 4) {
+    } else if (warp == 1) {
         // ---------------------------------------------------------------- MMA
         if (lane == 0) {
             constexpr uint32_t id_s = flash_idesc<BF16, false, kFKeys>();
             constexpr uint32_t id_o = flash_idesc<BF16, true, 128>();
             int g = 0, n = 0;
-            auto issue_s = [&](int gg) {
+            auto issue_s = [&](int gg, const uint8_t* q) {
                 const int sb = gg & 1;
-                if (gg >= 2) mbar_wait(&s_free[sb], ((gg >> 1) - 1) & 1);  // S_gg overwrites S / P_{gg-2}
+                if (gg >= 2) mbar_wait(&s_free[sb], ((gg >> 1) - 1) & 1);  // buffer's S / P consumed
                 mbar_wait(&k_full[sb], (gg >> 1) & 1);
+                PFT("mma_s", gg);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint8_t* k = sK + sb * kFKBytes;
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                    umma(tmem + sb * 64, desc_k(sQ + (kk >> 2) * kFHalf + (kk & 3) * 32),
+                    umma(tmem + sb * kFKeys, desc_k(q + (kk >> 2) * kFHalf + (kk & 3) * 32),
                          desc_k(k + (kk >> 2) * kFKHalf + (kk & 3) * 32), id_s, kk > 0);
                 umma_commit(&k_empty[sb]);
                 umma_commit(&s_full[sb]);
             };
             for (int it = first; it < last; ++it, ++n) {
                 const int qt = p.nqt - 1 - it % p.nqt;
-                const int T = 2 * (qt + 1);
-                mbar_wait(q_full, n & 1);
-                issue_s(g);
+                const int T = qt + 1;
+                const int qb = n & 1;
+                const uint8_t* q = sQ + qb * kFTileBytes;
+                mbar_wait(&q_full[qb], (n >> 1) & 1);
+                issue_s(g, q);
+                if (T == 1) umma_commit(&q_empty[qb]);
                 for (int j = 0; j < T; ++j, ++g) {
-                    if (j + 1 < T) issue_s(g + 1);
-                    if (j + 1 == T) umma_commit(q_empty);  // the item's last S issued: Q is free
+                    if (j + 1 < T) {
+                        issue_s(g + 1, q);
+                        if (j + 2 == T) umma_commit(&q_empty[qb]);  // the item's last S: Q is free
+                    }
                     if constexpr (!STATS) {
                         const int sb = g & 1;
                         mbar_wait(&v_full[sb], (g >> 1) & 1);
                         mbar_wait(&p_full[sb], (g >> 1) & 1);
                         if (j == 0 && n >= 1) mbar_wait(o_empty, (n - 1) & 1);  // O of the previous item read
+                        PFT("mma_pv", g);
                         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                         const uint8_t* v = sV + sb * kFKBytes;
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {  // 16 keys: chunk kk/2, half kk%2
-                            const uint32_t pa = tmem + sb * 64 + (kk >> 1) * 32 + (kk & 1) * 8;
-                            umma_ts(tmem + 128, pa, desc_mn(v + kk * 2048), id_o, (j | kk) != 0);
-                            if constexpr (BF16) umma_ts(tmem + 128, pa + 16, desc_mn(v + kk * 2048), id_o, 1);
+                        for (int kk = 0; kk < kFKeys / 16; ++kk) {  // 16 keys: 32-key chunk kk/2, 8-column group kk%2
+                            const uint32_t pa = tmem + sb * kFKeys + (kk >> 1) * 32 + (kk & 1) * 8;
+                            umma_ts(tmem + 256, pa, desc_mn(v + kk * 2048), id_o, (j | kk) != 0);
+                            if constexpr (BF16) umma_ts(tmem + 256, pa + 16, desc_mn(v + kk * 2048), id_o, 1);
                         }
                         umma_commit(&v_empty[sb]);
                         umma_commit(&s_free[sb]);
@@ -301,23 +351,27 @@ __global__ void __launch_bounds__(kFThreads, 1)
                 }
             }
         }
-    } else {
+    } else if (warp >= 4) {
         // ------------------------------------------------ rows: softmax / P / O
-        const int q4 = warp & 3;  // TMEM lane quarter this warp may access
+        const int q4 = warp & 3;      // TMEM lane quarter this warp may access
+        const int hf = (warp - 4) >> 2;  // key half of each tile / O half
         const int rl = q4 * 32 + lane;
         const uint32_t tl = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
         int g = 0, n = 0;
         for (int it = first; it < last; ++it, ++n) {
             const int qt = p.nqt - 1 - it % p.nqt, z = it / p.nqt;
-            const int T = 2 * (qt + 1);
+            const int T = qt + 1;
             const int r = qt * kFTile + rl;
+            const int qb = n & 1;
             const bool valid = r < p.s;
             const size_t zrow = static_cast<size_t>(z) * p.s;
-            float mx = -INFINITY;  // pass 1: raw row max
+            float mx = -INFINITY;  // pass 1: raw row max (this half's keys)
             float mc = 0.f;        // pass 2: row max x c1
-            float l = 0.f;         // pass 2: sum of e
+            float l = 0.f;         // pass 2: sum of e (this half's keys)
             if constexpr (!STATS) {
-                if (valid) mc = p.mrow[zrow + r] * p.c1;
+                mbar_wait(&q_full[qb], (n >> 1) & 1);
+                mc = valid ? sM[qb * 128 + rl] * p.c1 : 0.f;
+                mbar_arrive(&q_empty[qb]);
             }
             unsigned cnt = 0;
             const bool last_row = r == p.s - 1;
@@ -325,94 +379,111 @@ __global__ void __launch_bounds__(kFThreads, 1)
                 const int sb = g & 1;
                 // key tiles past the query tile's first row need the causal mask
                 const bool diag = (j + 1) * kFKeys - 1 > qt * kFTile;
+                const uint32_t ca = tl + sb * kFKeys + hf * kFHK;
                 mbar_wait(&s_full[sb], (g >> 1) & 1);
+                if (warp == 4 && lane == 0) PFT("row_s", g);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                float sv[64];
-                tmem_ld32(tl + sb * 64, sv);
-                tmem_ld32(tl + sb * 64 + 32, sv + 32);
+                float sv[kFHK];
+#pragma unroll
+                for (int c = 0; c < kFHK / 32; ++c) tmem_ld32(ca + c * 32, sv + c * 32);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                const int lim = valid ? min(r - j * kFKeys, kFKeys - 1) : -1;  // keys 0..lim of this tile count
+                if (warp == 4 && lane == 0) PFT("row_ld", g);
+                const int lim = valid ? min(r - j * kFKeys - hf * kFHK, kFHK - 1) : -1;  // keys 0..lim of this half count
                 if constexpr (STATS) {
                     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                     mbar_arrive(&s_free[sb]);
+                    float m4[4] = {mx, mx, mx, mx};
                     if (diag) {
 #pragma unroll
-                        for (int k = 0; k < 64; ++k)
-                            if (k <= lim) mx = fmaxf(mx, sv[k]);
+                        for (int k = 0; k < kFHK; ++k)
+                            if (k <= lim) m4[k & 3] = fmaxf(m4[k & 3], sv[k]);
                     } else {
 #pragma unroll
-                        for (int k = 0; k < 64; ++k) mx = fmaxf(mx, sv[k]);
+                        for (int k = 0; k < kFHK; ++k) m4[k & 3] = fmaxf(m4[k & 3], sv[k]);
                     }
+                    mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
                 } else {
+                    float l4[4] = {0.f, 0.f, 0.f, 0.f};
+                    unsigned c4[4] = {0u, 0u, 0u, 0u};
                     if (diag) {
 #pragma unroll
-                        for (int k = 0; k < 64; ++k) {
+                        for (int k = 0; k < kFHK; ++k) {
                             const float e = k <= lim ? ex2(fmaf(sv[k], p.c1, -mc)) : 0.f;
-                            cnt += (k <= lim) & (e < 0.01f);
-                            l += e;
+                            c4[k & 3] += (k <= lim) & (e < 0.01f);
+                            l4[k & 3] += e;
                             sv[k] = e;
                         }
                     } else {
-                        unsigned c2 = 0;
 #pragma unroll
-                        for (int k = 0; k < 64; ++k) {
+                        for (int k = 0; k < kFHK; ++k) {
                             const float e = ex2(fmaf(sv[k], p.c1, -mc));
-                            c2 += e < 0.01f;
-                            l += e;
+                            c4[k & 3] += e < 0.01f;
+                            l4[k & 3] += e;
                             sv[k] = e;
                         }
-                        cnt += valid ? c2 : 0u;
                     }
+                    l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
+                    const unsigned ct = (c4[0] + c4[1]) + (c4[2] + c4[3]);
+                    cnt += valid ? ct : 0u;
                     if (last_row) {
-                        float* wl = p.wlast + zrow + j * kFKeys;
+                        float* wl = p.wlast + zrow + j * kFKeys + hf * kFHK;
 #pragma unroll
-                        for (int k = 0; k < 64; ++k)
+                        for (int k = 0; k < kFHK; ++k)
                             if (k <= lim) wl[k] = sv[k];
                     }
 #pragma unroll
-                    for (int c = 0; c < 2; ++c) {
+                    for (int c = 0; c < kFHK / 32; ++c) {  // 32-key chunks: hi in 16 columns, bf16 lo in the next 16
                         uint32_t pk[16];
 #pragma unroll
                         for (int i = 0; i < 16; ++i) pk[i] = pack2<BF16>(sv[c * 32 + 2 * i], sv[c * 32 + 2 * i + 1]);
-                        tmem_st16(tl + sb * 64 + c * 32, pk);
+                        tmem_st16(ca + c * 32, pk);
                         if constexpr (BF16) {
 #pragma unroll
                             for (int i = 0; i < 16; ++i)
                                 pk[i] = pack2<true>(bf16_rest(sv[c * 32 + 2 * i]), bf16_rest(sv[c * 32 + 2 * i + 1]));
-                            tmem_st16(tl + sb * 64 + c * 32 + 16, pk);
+                            tmem_st16(ca + c * 32 + 16, pk);
                         }
                     }
+                    if (warp == 4 && lane == 0) PFT("row_math", g);
                     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                     mbar_arrive(&p_full[sb]);
+                    if (warp == 4 && lane == 0) PFT("row_p", g);
                 }
             }
+            // combine the two key halves of each row
+            float* red = sR + (n & 1) * 256;
+            red[hf * 128 + rl] = STATS ? mx : l;
+            named_sync(1, 256);
+            const float other = red[(hf ^ 1) * 128 + rl];
             if constexpr (STATS) {
-                if (valid) p.mrow[zrow + r] = mx;
+                if (hf == 0 && valid) p.mrow[static_cast<size_t>(z) * p.s_pad + r] = fmaxf(mx, other);
             } else {
-                if (last_row) p.llast[z] = l;
+                l += other;
+                if (last_row && hf == 0) p.llast[z] = l;
                 const float inv_l = 1.0f / l;
                 mbar_wait(o_full, n & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const size_t row0 =
-                    (static_cast<size_t>(z / p.H) * p.s + r) * p.HD + static_cast<size_t>(z % p.H) * 128;
-#pragma unroll 1
-                for (int c = 0; c < 4; ++c) {
-                    float o[32];
-                    tmem_ld32(tl + 128 + c * 32, o);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    if (!valid) continue;
+                float o[64];
+                tmem_ld32(tl + 256 + hf * 64, o);
+                tmem_ld32(tl + 256 + hf * 64 + 32, o + 32);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                mbar_arrive(o_empty);
+                if (valid) {
+                    const size_t row0 = (static_cast<size_t>(z / p.H) * p.s + r) * p.HD +
+                                        static_cast<size_t>(z % p.H) * 128 + hf * 64;
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) o[i] *= inv_l;
+                    for (int i = 0; i < 64; ++i) o[i] *= inv_l;
                     if (p.out_f32) {
-                        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + row0 + c * 32);
+                        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + row0);
 #pragma unroll
-                        for (int i = 0; i < 8; ++i)
+                        for (int i = 0; i < 16; ++i)
                             dst[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
                     } else {
-                        uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + row0 + c * 32);
+                        uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + row0);
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) {
+                        for (int i = 0; i < 8; ++i) {
                             uint4 v;
                             v.x = pack2<BF16>(o[8 * i + 0], o[8 * i + 1]);
                             v.y = pack2<BF16>(o[8 * i + 2], o[8 * i + 3]);
@@ -422,8 +493,6 @@ __global__ void __launch_bounds__(kFThreads, 1)
                         }
                     }
                 }
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                mbar_arrive(o_empty);
 #pragma unroll
                 for (int o2 = 16; o2 > 0; o2 >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o2);
                 if (lane == 0 && cnt) atomicAdd(&p.below[z], cnt);
@@ -432,9 +501,20 @@ __global__ void __launch_bounds__(kFThreads, 1)
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+#ifdef PF_TRACE
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const char* names[7] = {"tma_k", "mma_s", "row_s", "row_ld", "row_math", "row_p", "mma_pv"};
+        const long long t0 = g_pft[STATS ? 0 : 1][0][0];
+        for (int gg = 0; gg < 32; ++gg) {
+            printf("P%d g=%2d", STATS ? 1 : 2, gg);
+            for (int t = 0; t < 7; ++t) printf(" %s=%8lld", names[t], g_pft[STATS ? 0 : 1][t][gg] - t0);
+            printf("\n");
+        }
+    }
+#endif
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tslot), "n"(512));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
     }
 }
 
@@ -510,8 +590,7 @@ cudaError_t run_flash(const CUtensorMap& mq, const CUtensorMap& mkv, const Flash
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int items = p.Z * p.nqt;
-    const int grid = std::max(1, std::min(sms, (items + kFSlots - 1) / kFSlots));
+    const int grid = std::max(1, std::min(sms, p.Z * p.nqt));
     e = cudaLaunchKernel(fn, dim3(grid), dim3(kFThreads), args, smem, st);
     count_launch();
     return e;
@@ -521,10 +600,10 @@ size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 }  // namespace
 
-// mrow fp32 [Z][s], wlast fp32 [Z][s], llast fp32 [Z], below u32 [Z]
+// mrow fp32 [Z][s_pad], wlast fp32 [Z][s], llast fp32 [Z], below u32 [Z]
 size_t prefill_scratch_bytes(int B, int H, int s) {
-    const size_t Z = static_cast<size_t>(B) * H;
-    return align256(Z * s * 4) + align256(Z * s * 4) + align256(Z * 4) + align256(Z * 4);
+    const size_t Z = static_cast<size_t>(B) * H, s_pad = (static_cast<size_t>(s) + kFTile - 1) / kFTile * kFTile;
+    return align256(Z * s_pad * 4) + align256(Z * s * 4) + align256(Z * 4) + align256(Z * 4);
 }
 
 // Causal prefill of one cache layer (see the file comment). kv: layer base
@@ -536,8 +615,9 @@ cudaError_t launch_prefill(bool bf16, bool out_f32, const void* kv, const void* 
     if (D != 128) return cudaErrorInvalidValue;
     const int Z = B * H, nqt = (s + kFTile - 1) / kFTile;
     const uint64_t HD = static_cast<uint64_t>(H) * D;
+    const int s_pad = nqt * kFTile;
     float* mrow = reinterpret_cast<float*>(scratch);
-    float* wlast = reinterpret_cast<float*>(scratch + align256(static_cast<size_t>(Z) * s * 4));
+    float* wlast = reinterpret_cast<float*>(scratch + align256(static_cast<size_t>(Z) * s_pad * 4));
     float* llast = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(wlast) + align256(static_cast<size_t>(Z) * s * 4));
     unsigned* below = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(llast) + align256(static_cast<size_t>(Z) * 4));
     cudaError_t e = cudaMemsetAsync(below, 0, static_cast<size_t>(Z) * 4, st);
@@ -552,6 +632,7 @@ cudaError_t launch_prefill(bool bf16, bool out_f32, const void* kv, const void* 
     p.HD = static_cast<int>(HD);
     p.Z = Z;
     p.nqt = nqt;
+    p.s_pad = s_pad;
     p.c1 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D)));
     p.mrow = mrow;
     p.llast = llast;
