@@ -44,7 +44,7 @@ constexpr int kFKHalf = kFKeys * 128;  // one 64-column SW128 box of a 64-key K 
 constexpr int kFKBytes = 2 * kFKHalf;
 constexpr int kFBufs = 2;    // S / P buffers in TMEM, K / V stages in shared memory
 constexpr int kFHK = kFKeys / 2;  // keys per row thread per tile
-constexpr int kFThreads = 128 + 256;  // 4 control warps + 8 row warps
+constexpr int kFThreads = 448;  // warps 0..3 control / epilogue, 4..11 rows, 12..13 epilogue
 
 struct FlashParams {
     int s, H, HD;
@@ -145,7 +145,8 @@ struct FlashSmem {
     static constexpr int kV = kK + kFBufs * kFKBytes;           // [kFBufs] value tiles (pass 2)
     static constexpr int kM = kV + (STATS ? 0 : kFBufs * kFKBytes);  // [2][128] row max (pass 2)
     static constexpr int kR = kM + 2 * 128 * 4;                 // [2][2][128] per-half row partials
-    static constexpr int kBar = kR + 2 * 2 * 128 * 4;
+    static constexpr int kL = kR + 2 * 2 * 128 * 4;             // [2][128] 1 / l per O buffer (pass 2)
+    static constexpr int kBar = kL + 2 * 128 * 4;
     static constexpr int kNBar = 40;
     static constexpr int kBytes = kBar + kNBar * 8 + 16 + 1024;  // barriers, TMEM slot, alignment
 };
@@ -183,11 +184,12 @@ __device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t* v) {
 // MMAs use N = 128 key tiles rather than 64.)
 // TMEM: S / P buffer b at columns [128 b, 128 b + 128) -- P is written over
 // the S columns it came from, 32 keys per 32-column chunk: hi in the first
-// 16 columns, bf16 lo in the next 16 -- and O in [256, 384).
+// 16 columns, bf16 lo in the next 16 -- and O buffers in [256, 512).
 // Warps: 0 TMA, 1 MMA (+ TMEM allocation), 4..7 and 8..11 the row threads:
 // warp w owns rows 32 (w % 4) .. (its TMEM lane quarter) and key columns
-// 64 hf .. 64 hf + 63 of every tile (hf = 0 for warps 4..7, 1 for 8..11),
-// and O columns 64 hf .. 64 hf + 63.
+// 64 hf .. 64 hf + 63 of every tile (hf = 0 for warps 4..7, 1 for 8..11);
+// 2, 3, 12, 13 (lane quarters 2, 3, 0, 1) drain O (double buffered: columns
+// [256, 384) and [384, 512)) while the row threads move on to the next item.
 #ifdef PF_TRACE
 __device__ long long g_pft[2][8][32];
 __device__ __forceinline__ int pft_tag(const char* t) {
@@ -216,6 +218,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
     uint8_t* sV = sm + L::kV;
     float* sM = reinterpret_cast<float*>(sm + L::kM);  // [2][128]
     float* sR = reinterpret_cast<float*>(sm + L::kR);  // [2][2][128]
+    float* sL = reinterpret_cast<float*>(sm + L::kL);  // [2][128]
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::kBar);
     uint64_t* q_full = bar;        // [2]
     uint64_t* q_empty = bar + 2;   // [2]
@@ -226,12 +229,13 @@ __global__ void __launch_bounds__(kFThreads, 1)
     uint64_t* s_full = bar + 20;   // [4] MMA -> rows
     uint64_t* s_free = bar + 24;   // [4] pass 1: rows read S; pass 2: PV consumed P
     uint64_t* p_full = bar + 28;   // [4] pass 2: rows wrote P
-    uint64_t* o_full = bar + 32;
-    uint64_t* o_empty = bar + 33;
+    uint64_t* o_full = bar + 32;   // [2] MMA -> epilogue
+    uint64_t* o_empty = bar + 34;  // [2] epilogue read O
+    uint64_t* l_full = bar + 36;   // [2] rows wrote 1 / l
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + L::kNBar);
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 34; ++i) mbar_init(&bar[i], 1);
+        for (int i = 0; i < 38; ++i) mbar_init(&bar[i], 1);
         if (!STATS) {
             // Q + row-max buffer: MMA commit after the item's last S + every row
             // thread after reading its row max
@@ -242,7 +246,10 @@ __global__ void __launch_bounds__(kFThreads, 1)
             if (STATS) mbar_init(&s_free[i], 256);
             mbar_init(&p_full[i], 256);
         }
-        mbar_init(o_empty, 256);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&o_empty[i], 128);
+            mbar_init(&l_full[i], 128);
+        }
         fence_barrier_init();
     }
     if (warp == 1) {
@@ -317,41 +324,53 @@ __global__ void __launch_bounds__(kFThreads, 1)
                 umma_commit(&k_empty[sb]);
                 umma_commit(&s_full[sb]);
             };
+            // The S stream runs one tile ahead of the PV stream, across item
+            // boundaries: the next item's first S is on the tensor pipe while
+            // the row threads finish the current item (O is double buffered and
+            // drained by the epilogue warps).
+            int itS = first, jS = 0, nS = 0, gS = 0;
+            auto issue_next_s = [&]() {
+                if (itS >= last) return;
+                const int TS = p.nqt - itS % p.nqt;
+                const int qb = nS & 1;
+                if (jS == 0) mbar_wait(&q_full[qb], (nS >> 1) & 1);
+                issue_s(gS++, sQ + qb * kFTileBytes);
+                if (++jS == TS) {
+                    umma_commit(&q_empty[qb]);  // the item's last S: Q is free
+                    jS = 0;
+                    ++itS;
+                    ++nS;
+                }
+            };
+            issue_next_s();
             for (int it = first; it < last; ++it, ++n) {
-                const int qt = p.nqt - 1 - it % p.nqt;
-                const int T = qt + 1;
-                const int qb = n & 1;
-                const uint8_t* q = sQ + qb * kFTileBytes;
-                mbar_wait(&q_full[qb], (n >> 1) & 1);
-                issue_s(g, q);
-                if (T == 1) umma_commit(&q_empty[qb]);
+                const int T = p.nqt - it % p.nqt;
+                const int ob = n & 1;
                 for (int j = 0; j < T; ++j, ++g) {
-                    if (j + 1 < T) {
-                        issue_s(g + 1, q);
-                        if (j + 2 == T) umma_commit(&q_empty[qb]);  // the item's last S: Q is free
-                    }
+                    issue_next_s();  // S_{g+1}
                     if constexpr (!STATS) {
                         const int sb = g & 1;
                         mbar_wait(&v_full[sb], (g >> 1) & 1);
                         mbar_wait(&p_full[sb], (g >> 1) & 1);
-                        if (j == 0 && n >= 1) mbar_wait(o_empty, (n - 1) & 1);  // O of the previous item read
+                        if (j == 0 && n >= 2) mbar_wait(&o_empty[ob], ((n >> 1) - 1) & 1);  // O buffer drained
                         PFT("mma_pv", g);
                         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                         const uint8_t* v = sV + sb * kFKBytes;
+                        const uint32_t od = tmem + 256 + ob * 128;
 #pragma unroll
                         for (int kk = 0; kk < kFKeys / 16; ++kk) {  // 16 keys: 32-key chunk kk/2, 8-column group kk%2
                             const uint32_t pa = tmem + sb * kFKeys + (kk >> 1) * 32 + (kk & 1) * 8;
-                            umma_ts(tmem + 256, pa, desc_mn(v + kk * 2048), id_o, (j | kk) != 0);
-                            if constexpr (BF16) umma_ts(tmem + 256, pa + 16, desc_mn(v + kk * 2048), id_o, 1);
+                            umma_ts(od, pa, desc_mn(v + kk * 2048), id_o, (j | kk) != 0);
+                            if constexpr (BF16) umma_ts(od, pa + 16, desc_mn(v + kk * 2048), id_o, 1);
                         }
                         umma_commit(&v_empty[sb]);
                         umma_commit(&s_free[sb]);
-                        if (j + 1 == T) umma_commit(o_full);
+                        if (j + 1 == T) umma_commit(&o_full[ob]);
                     }
                 }
             }
         }
-    } else if (warp >= 4) {
+    } else if (warp >= 4 && warp < 12) {
         // ------------------------------------------------ rows: softmax / P / O
         const int q4 = warp & 3;      // TMEM lane quarter this warp may access
         const int hf = (warp - 4) >> 2;  // key half of each tile / O half
@@ -460,43 +479,62 @@ __global__ void __launch_bounds__(kFThreads, 1)
                 if (hf == 0 && valid) p.mrow[static_cast<size_t>(z) * p.s_pad + r] = fmaxf(mx, other);
             } else {
                 l += other;
-                if (last_row && hf == 0) p.llast[z] = l;
-                const float inv_l = 1.0f / l;
-                mbar_wait(o_full, n & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                float o[64];
-                tmem_ld32(tl + 256 + hf * 64, o);
-                tmem_ld32(tl + 256 + hf * 64 + 32, o + 32);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                mbar_arrive(o_empty);
-                if (valid) {
-                    const size_t row0 = (static_cast<size_t>(z / p.H) * p.s + r) * p.HD +
-                                        static_cast<size_t>(z % p.H) * 128 + hf * 64;
-#pragma unroll
-                    for (int i = 0; i < 64; ++i) o[i] *= inv_l;
-                    if (p.out_f32) {
-                        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + row0);
-#pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            dst[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
-                    } else {
-                        uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + row0);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            uint4 v;
-                            v.x = pack2<BF16>(o[8 * i + 0], o[8 * i + 1]);
-                            v.y = pack2<BF16>(o[8 * i + 2], o[8 * i + 3]);
-                            v.z = pack2<BF16>(o[8 * i + 4], o[8 * i + 5]);
-                            v.w = pack2<BF16>(o[8 * i + 6], o[8 * i + 7]);
-                            dst[i] = v;
-                        }
-                    }
+                if (hf == 0) {
+                    if (last_row) p.llast[z] = l;
+                    const int ob = n & 1;
+                    if (n >= 2) mbar_wait(&o_empty[ob], ((n >> 1) - 1) & 1);  // sL[ob] of item n - 2 read
+                    sL[ob * 128 + rl] = 1.0f / l;
+                    mbar_arrive(&l_full[ob]);
                 }
 #pragma unroll
                 for (int o2 = 16; o2 > 0; o2 >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o2);
                 if (lane == 0 && cnt) atomicAdd(&p.below[z], cnt);
             }
+        }
+    } else if (!STATS && (warp >= 12 || warp == 2 || warp == 3)) {
+        // ------------------------------------------- O epilogue (lane quarters 2, 3, 0, 1)
+        const int q4 = warp & 3;
+        const int rl = q4 * 32 + lane;
+        const uint32_t tl = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
+        int n = 0;
+        for (int it = first; it < last; ++it, ++n) {
+            const int qt = p.nqt - 1 - it % p.nqt, z = it / p.nqt;
+            const int r = qt * kFTile + rl;
+            const bool valid = r < p.s;
+            const int ob = n & 1;
+            mbar_wait(&l_full[ob], (n >> 1) & 1);
+            const float inv_l = sL[ob * 128 + rl];
+            mbar_wait(&o_full[ob], (n >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const size_t row0 =
+                (static_cast<size_t>(z / p.H) * p.s + r) * p.HD + static_cast<size_t>(z % p.H) * 128;
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                float o[32];
+                tmem_ld32(tl + 256 + ob * 128 + c * 32, o);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (!valid) continue;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) o[i] *= inv_l;
+                if (p.out_f32) {
+                    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + row0 + c * 32);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) dst[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+                } else {
+                    uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + row0 + c * 32);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        uint4 v;
+                        v.x = pack2<BF16>(o[8 * i + 0], o[8 * i + 1]);
+                        v.y = pack2<BF16>(o[8 * i + 2], o[8 * i + 3]);
+                        v.z = pack2<BF16>(o[8 * i + 4], o[8 * i + 5]);
+                        v.w = pack2<BF16>(o[8 * i + 6], o[8 * i + 7]);
+                        dst[i] = v;
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            mbar_arrive(&o_empty[ob]);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
