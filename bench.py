@@ -191,7 +191,8 @@ def run_config5(args, cfg, rank: int, world: int):
             kp, vp = kv_of(l, 0, s)
             cache.append_tokens(l, 0, 0, kp, vp)
             del kp, vp
-            cache.prefill_seed(l, s, qin[0][l].contiguous())
+            # Engine::prefill's attention on the tensor cores seeds the importance
+            cache.prefill_layer(l, torch.randn((B, s, H, D), generator=g, device="cuda", dtype=qdt) * 0.5)
         if phase > 1:
             cache.enable_host_tier(poison=False)
             for l in range(L):
@@ -290,9 +291,13 @@ def main():
     sampler = ClockSampler(local) if not args.profile_only else None
     if sampler:
         sampler.__enter__()
-    # ---- prompt: random K/V for s tokens per layer, accumulator seeded from the
-    # dense last row of the prompt (engine.hpp:508-512), all on device.
+    # ---- prompt: random K/V for s tokens per layer, then Engine::prefill's
+    # attention (engine.hpp:485-529) on the tensor cores: causal attention of
+    # all s prompt queries, the accumulator seeded with the last row
+    # (engine.hpp:508-512). INT8 caches take the last-row seed only.
     g = torch.Generator(device="cuda").manual_seed(2403_17312 + args.config * 1000 + rank)
+    tc_prefill = cfg["kv"] in ("f16", "bf16")
+    pf_ms, pf_events = 0.0, []
     for l in range(L):
         chunk = max(1, min(B, (1 << 30) // (s * H * D * 2)))
         for c0 in range(0, B, chunk):
@@ -301,7 +306,37 @@ def main():
             vp = torch.randn((nb, s, H, D), generator=g, device="cuda", dtype=qdt)
             cache.append_tokens(l, c0, 0, kp, vp)
             del kp, vp
-        cache.prefill_seed(l, s, torch.randn((B, H, D), generator=g, device="cuda", dtype=qdt))
+        if tc_prefill:
+            qp = torch.randn((B, s, H, D), generator=g, device="cuda", dtype=qdt) * 0.5
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            cache.prefill_layer(l, qp)
+            e1.record()
+            pf_events.append((e0, e1))
+            del qp
+        else:
+            cache.prefill_seed(l, s, torch.randn((B, H, D), generator=g, device="cuda", dtype=qdt))
+    torch.cuda.synchronize()
+    prefill = None
+    if pf_events:
+        # the first layer includes one-time scratch allocation and module load
+        times = [a.elapsed_time(b) for a, b in pf_events]
+        steady = times[1:] if len(times) > 1 else times
+        pf_ms = sum(steady) / len(steady)
+        flops = 4.0 * B * H * (s * (s + 1) / 2) * D  # QK^T and PV over the causal triangle
+        tf = flops / (pf_ms / 1000.0) / 1e12
+        bf16_peak = None
+        try:
+            bf16_peak = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                    "MEASURED_PEAKS.json"))).get("bf16_tflops")
+        except (OSError, ValueError):
+            pass
+        prefill = {"ms_per_layer": pf_ms, "layers": L, "prompt_tokens_per_s": world * B * s / (pf_ms / 1000.0),
+                   "tflops": tf, "peak_tflops": bf16_peak, "frac": (tf / bf16_peak) if bf16_peak else None,
+                   "kernel": "skvd::flash_prefill_kernel (max pass + P.V pass) + prefill_seed_kernel",
+                   "note": "causal dense attention of the prompt per layer (skv_prefill_layer), mean over "
+                           "layers 2..L; flops = 4 B H s(s+1)/2 D (the two causal GEMMs; the kernel "
+                           "recomputes QK^T once more for the exact row max)"}
     pool = min(W + K, 8)
     inputs = [tuple(torch.randn((L, B, H, D), generator=g, device="cuda", dtype=qdt) for _ in range(3))
               for _ in range(pool)]
@@ -415,7 +450,7 @@ def main():
                          "step_achieved": step_achieved, "step_frac": step_achieved / peak,
                          "step_note": "attend algorithmic bytes of the timed region / timed region "
                                       "(includes select kernels and launch gaps; layers chained with PDL)"},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "prefill": prefill,
             "clocks": dict(sampler.summary(), window="prompt fill + warmup + timed region + kernel passes (GPU busy throughout)") if sampler else None,
         }
         print(json.dumps(line), flush=True)
