@@ -59,32 +59,75 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the run
+    (B200_PROFILING.md clocks line): NVML polled every 2 ms from a thread
+    (nvidia-smi's 50 ms loop as the fallback), with the timed region's host
+    window marked so its own samples are reported."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.stop, self.window = index, [], threading.Event(), None
+        self.kind = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                        rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.rows.append((time.perf_counter(), float(sm),
+                                          [n for n, bit in zip(self.NAMES, bits) if rs & bit]))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+
+            self.kind = "nvml 2 ms"
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            pass
+        try:
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
                                           "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            self.max_mhz = None
+
+            def read():
+                for line in self.proc.stdout:
+                    r = [x.strip() for x in line.split(",")]
+                    try:
+                        self.max_mhz = float(r[1])
+                        self.rows.append((time.perf_counter(), float(r[0]),
+                                          [n for n, v in zip(self.NAMES, r[2:]) if v == "Active"]))
+                    except Exception:
+                        pass
+
+            self.kind = "nvidia-smi 50 ms"
+            self.t = threading.Thread(target=read, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.kind = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+    def mark(self, t0: float, t1: float):
+        self.window = (t0, t1)
 
     def __exit__(self, *a):
-        if self.proc:
+        self.stop.set()
+        if getattr(self, "proc", None):
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -92,14 +135,15 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        rows = list(self.rows)
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        timed = [r for r in rows if self.window and self.window[0] <= r[0] <= self.window[1]]
+        use = timed or rows
+        return {"sm_mhz": statistics.median(r[1] for r in use), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted({n for r in rows for n in r[2]}), "samples": len(rows),
+                "samples_timed_region": len(timed), "sampler": self.kind,
+                "sm_mhz_min_timed": min(r[1] for r in timed) if timed else None}
 
 
 def cpu_baseline(cfg, n_mid: int, budget_s: float = 15.0):
@@ -282,8 +326,8 @@ def main():
 
     L, B, H, s = cfg["L"], cfg["B"], cfg["H"], cfg["s"]
     W, K = args.warmup, args.steps
-    e2e_steps = 0 if (args.no_e2e or args.profile_only) else max(3, min(K, 20))
-    ncap = s + W + K + min(K, 10) + e2e_steps + 1
+    e2e_steps = 0 if (args.no_e2e or args.profile_only) else max(3, min(K, 50))
+    ncap = s + W + K + min(K, 10) + e2e_steps + (2 if e2e_steps else 0) + 1
     qdt = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[cfg["q"]]
     cache = api.SwaCache(L, B, H, D, ncap, kv_dtype=cfg["kv"], q_dtype=cfg["q"], device=local)
     cache.set_variant(args.variant)
@@ -359,6 +403,7 @@ def main():
     n_first = n + 1
     cache.profile(False)  # reset the launch / algorithmic-byte counters; no per-kernel events
     launches0 = api.launch_count()
+    t_host0 = time.perf_counter()
     ev0.record(stream)
     for i in range(K):
         n += 1
@@ -366,6 +411,8 @@ def main():
         cache.swa_decode_step(n, RATIO, q, k, v, out)
     ev1.record(stream)
     torch.cuda.synchronize()
+    if sampler:
+        sampler.mark(t_host0, time.perf_counter())
     launches = api.launch_count() - launches0
     elapsed_ms = ev0.elapsed_time(ev1)
     _, step_launches, step_algo = cache.profile_read()
@@ -407,6 +454,9 @@ def main():
         oh = torch.empty((L, B, H, D), dtype=qdt).pin_memory()
         for t_, src in zip((qh, kh, vh), inputs[0]):
             t_.copy_(src.cpu())
+        for i in range(2):  # untimed: staging allocation, copy streams
+            n += 1
+            cache.swa_decode_step_host(n, RATIO, qh, kh, vh, oh)
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
@@ -421,7 +471,7 @@ def main():
         per = L * B * H * D * qh.element_size()
         e2e = {"value": world * B * e2e_steps / (e2e_ms / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": 3 * per, "d2h_bytes_per_step": per,
-               "path": "skv_swa_decode_step_host (pinned host q/k/v in, out back)"}
+               "path": "skv_swa_decode_step_host (pinned host q/k/v in, out back; 4 layer chunks pipelined over h2d/d2h copy streams)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_only:
@@ -451,7 +501,7 @@ def main():
                          "step_note": "attend algorithmic bytes of the timed region / timed region "
                                       "(includes select kernels and launch gaps; layers chained with PDL)"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "prefill": prefill,
-            "clocks": dict(sampler.summary(), window="prompt fill + warmup + timed region + kernel passes (GPU busy throughout)") if sampler else None,
+            "clocks": dict(sampler.summary(), window="sm_mhz: median over the timed region's samples (else the whole run); reasons: whole run") if sampler else None,
         }
         print(json.dumps(line), flush=True)
     if dist:

@@ -124,9 +124,11 @@ skv_status skv_swa_decode_layer(skv_cache* cache, int layer, int n, double r, co
 /* All L layers of one decode step (q/k/v/out device [L][B][H][D]); L launches. */
 skv_status skv_swa_decode_step(skv_cache* cache, int n, double r, const void* q,
                                const void* k_new, const void* v_new, void* out, void* stream);
-/* Same with HOST buffers (pageable or pinned): copies q/k/v in, runs the
- * step, copies out back, all on `stream`; returns after enqueueing
- * (synchronize the stream before reading out_host). */
+/* Same with HOST buffers (pinned for overlap; pageable works but serialises):
+ * the layers are cut into chunks whose q/k/v uploads, attention and output
+ * downloads overlap on two internal copy streams ordered against `stream`.
+ * Returns after enqueueing: the host buffers must stay untouched until
+ * `stream` is synchronised, which also covers every copy of the call. */
 skv_status skv_swa_decode_step_host(skv_cache* cache, int n, double r, const void* q_host,
                                     const void* k_host, const void* v_host, void* out_host,
                                     void* stream);

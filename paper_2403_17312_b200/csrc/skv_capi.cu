@@ -133,9 +133,11 @@ struct skv_cache {
     uint8_t* pf_scratch = nullptr;
     size_t pf_bytes = 0;
     double* pf_sparsity = nullptr;
-    // host-buffer step staging
+    // host-buffer step staging: layer chunks pipelined over two copy streams
     uint8_t* stage = nullptr;
     size_t stage_bytes = 0;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    std::vector<cudaEvent_t> ev_in, ev_comp, ev_out;  // per chunk
     // measurement
     bool prof = false;
     std::vector<cudaEvent_t> ev;  // start/stop pairs
@@ -145,6 +147,8 @@ struct skv_cache {
     int last_hg = 0, last_grid = 0, last_occ = 0;
     size_t last_smem = 0;
 };
+
+constexpr int kHostChunks = 4;  // layer chunks of the host-buffer step pipeline (2-4 best on the box: fewer, larger copies)
 
 static size_t out_size(const skv_cache* c) { return c->d.out_f32 ? 4 : dtype_size(c->d.q_dtype); }
 
@@ -268,6 +272,10 @@ skv_status skv_cache_destroy(skv_cache* c) {
     cudaFree(c->rec_map);
     cudaFree(c->rec_m);
     cudaFree(c->stage);
+    for (auto* v : {&c->ev_in, &c->ev_comp, &c->ev_out})
+        for (cudaEvent_t e : *v) cudaEventDestroy(e);
+    if (c->h2d) cudaStreamDestroy(c->h2d);
+    if (c->d2h) cudaStreamDestroy(c->d2h);
     cudaFree(c->pf_scratch);
     cudaFree(c->pf_sparsity);
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
@@ -817,6 +825,25 @@ skv_status skv_swa_decode_layer(skv_cache* c, int layer, int n, double r, const 
     return decode_layer_impl(c, layer, n, r, q, k_new, v_new, out, idx_out, w_out, false, as_stream(stream));
 }
 
+// Layers [l0, l1) of one decode step; layer l > l0 launches with programmatic
+// dependent launch: its inputs were complete before the range's first launch,
+// so it can stream while the previous layer's kernels drain.
+static skv_status decode_layers(skv_cache* c, int l0, int l1, int n, double r, const void* q, const void* k_new,
+                                const void* v_new, void* out, cudaStream_t st) {
+    const size_t per_layer = static_cast<size_t>(c->d.batch) * c->d.heads * c->d.head_dim * dtype_size(c->d.q_dtype);
+    const size_t per_layer_out = static_cast<size_t>(c->d.batch) * c->d.heads * c->d.head_dim * out_size(c);
+    for (int l = l0; l < l1; ++l) {
+        const size_t o = per_layer * l;
+        if (skv_status s = decode_layer_impl(c, l, n, r, static_cast<const uint8_t*>(q) + o,
+                                             static_cast<const uint8_t*>(k_new) + o,
+                                             static_cast<const uint8_t*>(v_new) + o,
+                                             static_cast<uint8_t*>(out) + per_layer_out * l, nullptr, nullptr,
+                                             l > l0, st))
+            return s;
+    }
+    return SKV_OK;
+}
+
 skv_status skv_swa_decode_step(skv_cache* c, int n, double r, const void* q, const void* k_new,
                                const void* v_new, void* out, void* stream) {
     SKV_REQUIRE(c != nullptr, "null cache");
@@ -824,20 +851,27 @@ skv_status skv_swa_decode_step(skv_cache* c, int n, double r, const void* q, con
     StepShape s;
     if (skv_status st = step_shape(c, n, r, &s)) return st;
     DeviceGuard guard(c->d.device);
-    const size_t per_layer = static_cast<size_t>(c->d.batch) * c->d.heads * c->d.head_dim * dtype_size(c->d.q_dtype);
-    const size_t per_layer_out = static_cast<size_t>(c->d.batch) * c->d.heads * c->d.head_dim * out_size(c);
-    for (int l = 0; l < c->d.layers; ++l) {
-        const size_t o = per_layer * l;
-        // Layer l > 0 launches with programmatic dependent launch: its inputs
-        // were complete before this call's first launch, so it can stream
-        // while the previous layer's kernels drain.
-        if (skv_status st = decode_layer_impl(c, l, n, r, static_cast<const uint8_t*>(q) + o,
-                                              static_cast<const uint8_t*>(k_new) + o,
-                                              static_cast<const uint8_t*>(v_new) + o,
-                                              static_cast<uint8_t*>(out) + per_layer_out * l, nullptr, nullptr,
-                                              l > 0, as_stream(stream)))
-            return st;
-    }
+    return decode_layers(c, 0, c->d.layers, n, r, q, k_new, v_new, out, as_stream(stream));
+}
+
+// Host buffers: the step's layers are cut into chunks; chunk i's q/k/v go up
+// on the h2d copy stream, its layers run on `stream` once they have landed,
+// and its outputs go down on the d2h copy stream, so PCIe traffic in both
+// directions overlaps the attention of the other chunks (and, across calls,
+// of the previous step). Staging hazards are per chunk: the upload of chunk i
+// waits for the previous step's compute of chunk i (the last reader of its
+// staging), the compute waits for the previous download of chunk i (the last
+// reader of its output staging). `stream` finally waits for the last download,
+// so synchronising it covers every copy of the call.
+static skv_status host_pipe_init(skv_cache* c, int chunks) {
+    if (!c->h2d) SKV_CUDA(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+    if (!c->d2h) SKV_CUDA(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+    for (auto* v : {&c->ev_in, &c->ev_comp, &c->ev_out})
+        while (static_cast<int>(v->size()) < chunks) {
+            cudaEvent_t e;
+            SKV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            v->push_back(e);
+        }
     return SKV_OK;
 }
 
@@ -845,10 +879,13 @@ skv_status skv_swa_decode_step_host(skv_cache* c, int n, double r, const void* q
                                     const void* v_host, void* out_host, void* stream) {
     SKV_REQUIRE(c != nullptr, "null cache");
     SKV_REQUIRE(q_host && k_host && v_host && out_host, "decode_step: null argument");
+    StepShape shape;
+    if (skv_status st = step_shape(c, n, r, &shape)) return st;
     DeviceGuard guard(c->d.device);
-    const size_t bytes = static_cast<size_t>(c->d.layers) * c->d.batch * c->d.heads * c->d.head_dim *
-                         dtype_size(c->d.q_dtype);
-    const size_t obytes = static_cast<size_t>(c->d.layers) * c->d.batch * c->d.heads * c->d.head_dim * out_size(c);
+    const int L = c->d.layers;
+    const size_t per_layer = static_cast<size_t>(c->d.batch) * c->d.heads * c->d.head_dim * dtype_size(c->d.q_dtype);
+    const size_t per_layer_out = static_cast<size_t>(c->d.batch) * c->d.heads * c->d.head_dim * out_size(c);
+    const size_t bytes = per_layer * L, obytes = per_layer_out * L;
     if (c->stage_bytes < 3 * bytes + obytes) {
         cudaFree(c->stage);
         c->stage = nullptr;
@@ -859,13 +896,34 @@ skv_status skv_swa_decode_step_host(skv_cache* c, int n, double r, const void* q
         }
         c->stage_bytes = 3 * bytes + obytes;
     }
+    static const int env_chunks = [] {
+        const char* e = std::getenv("SKV_HOST_CHUNKS");  // tuning override
+        return e ? std::max(1, std::atoi(e)) : kHostChunks;
+    }();
+    const int chunks = std::min(L, env_chunks);
+    if (skv_status s = host_pipe_init(c, chunks)) return s;
     const cudaStream_t st = as_stream(stream);
     uint8_t *dq = c->stage, *dk = dq + bytes, *dv = dk + bytes, *dout = dv + bytes;
-    SKV_CUDA(cudaMemcpyAsync(dq, q_host, bytes, cudaMemcpyHostToDevice, st));
-    SKV_CUDA(cudaMemcpyAsync(dk, k_host, bytes, cudaMemcpyHostToDevice, st));
-    SKV_CUDA(cudaMemcpyAsync(dv, v_host, bytes, cudaMemcpyHostToDevice, st));
-    if (skv_status s = skv_swa_decode_step(c, n, r, dq, dk, dv, dout, stream)) return s;
-    SKV_CUDA(cudaMemcpyAsync(out_host, dout, obytes, cudaMemcpyDeviceToHost, st));
+    const uint8_t* src[3] = {static_cast<const uint8_t*>(q_host), static_cast<const uint8_t*>(k_host),
+                             static_cast<const uint8_t*>(v_host)};
+    uint8_t* dst[3] = {dq, dk, dv};
+    for (int i = 0; i < chunks; ++i) {
+        const int l0 = L * i / chunks, l1 = L * (i + 1) / chunks;
+        const size_t o = per_layer * l0, len = per_layer * (l1 - l0);
+        SKV_CUDA(cudaStreamWaitEvent(c->h2d, c->ev_comp[i], 0));
+        for (int t = 0; t < 3; ++t)
+            SKV_CUDA(cudaMemcpyAsync(dst[t] + o, src[t] + o, len, cudaMemcpyHostToDevice, c->h2d));
+        SKV_CUDA(cudaEventRecord(c->ev_in[i], c->h2d));
+        SKV_CUDA(cudaStreamWaitEvent(st, c->ev_in[i], 0));
+        SKV_CUDA(cudaStreamWaitEvent(st, c->ev_out[i], 0));
+        if (skv_status s = decode_layers(c, l0, l1, n, r, dq, dk, dv, dout, st)) return s;
+        SKV_CUDA(cudaEventRecord(c->ev_comp[i], st));
+        SKV_CUDA(cudaStreamWaitEvent(c->d2h, c->ev_comp[i], 0));
+        SKV_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(out_host) + per_layer_out * l0, dout + per_layer_out * l0,
+                                 per_layer_out * (l1 - l0), cudaMemcpyDeviceToHost, c->d2h));
+        SKV_CUDA(cudaEventRecord(c->ev_out[i], c->d2h));
+    }
+    SKV_CUDA(cudaStreamWaitEvent(st, c->ev_out[chunks - 1], 0));
     return SKV_OK;
 }
 

@@ -319,6 +319,34 @@ def test_decode_multilayer_step(api):
         assert torch.equal(caches[0].importance(l, n), caches[1].importance(l, n))
 
 
+def test_decode_step_host_pipelined(api):
+    """The host-buffer step (layer chunks pipelined over two copy streams)
+    over several back-to-back calls with no synchronisation in between ==
+    the device step, bit for bit; L=11 gives uneven chunks."""
+    rng = np.random.default_rng(9)
+    L, B, H, D, s, steps = 11, 3, 4, 128, 60, 4
+    kv = torch.from_numpy(rng.standard_normal((L, B, s, 2, H, D))).half().cuda()
+    qs = [[torch.from_numpy(rng.standard_normal((L, B, H, D))).half() for _ in range(3)] for _ in range(steps)]
+    caches = [api.SwaCache(L, B, H, D, s + steps, kv_dtype="f16") for _ in range(2)]
+    for c in caches:
+        for l in range(L):
+            c.append_tokens(l, 0, 0, kv[l, :, :, 0].contiguous(), kv[l, :, :, 1].contiguous())
+            c.prefill_seed(l, s, qs[0][0][l].cuda())
+    want, got = [], []
+    for j in range(steps):
+        want.append(caches[0].swa_decode_step(s + j + 1, 0.2, *(t.cuda() for t in qs[j])).cpu())
+    torch.cuda.synchronize()
+    pinned = [[t.pin_memory() for t in qs[j]] for j in range(steps)]
+    for j in range(steps):
+        got.append(torch.empty((L, B, H, D), dtype=torch.float16).pin_memory())
+        caches[1].swa_decode_step_host(s + j + 1, 0.2, *pinned[j], got[j])
+    torch.cuda.synchronize()
+    for j in range(steps):
+        assert torch.equal(want[j], got[j]), j
+    for l in range(L):
+        assert torch.equal(caches[0].importance(l, s + steps), caches[1].importance(l, s + steps))
+
+
 def test_decode_errors(api):
     cache = api.SwaCache(2, 1, 4, 128, 8, kv_dtype="f16")
     x = torch.zeros((1, 4, 128), device="cuda", dtype=torch.float16)
