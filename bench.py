@@ -146,6 +146,20 @@ class ClockSampler:
                 "sm_mhz_min_timed": min(r[1] for r in timed) if timed else None}
 
 
+def attend_algo_bytes(cfg, n: int) -> int:
+    """Algorithmic HBM bytes of one attend launch at n tokens (mirrors
+    attend_algo_bytes in skv_capi.cu): q in, out out, the new K/V rows in and
+    stored, every other selected row of K and V gathered once."""
+    from paper_2403_17312_b200.api import swa_keep_count
+
+    e = {"f32": 4, "f16": 2, "bf16": 2, "u8": 1}
+    H, B = cfg["H"], cfg["B"]
+    row = D * e[cfg["kv"]] + (8 if cfg["kv"] == "u8" else 0)
+    eq = e[cfg["q"]]
+    m = swa_keep_count(n, RATIO)
+    return B * (H * D * 2 * eq + 2 * H * D * eq + 2 * H * row + 2 * (m - 1) * H * row)
+
+
 def cpu_baseline(cfg, n_mid: int, budget_s: float = 15.0):
     """The reference's own swa_attention (oracle/_ref, compiled from the
     reference headers) -- else the oracle port -- on all host cores, one
@@ -403,6 +417,8 @@ def main():
     n_first = n + 1
     cache.profile(False)  # reset the launch / algorithmic-byte counters; no per-kernel events
     launches0 = api.launch_count()
+    if args.profile_only:  # ncu --profile-from-start off: capture starts at the timed region
+        torch.cuda.cudart().cudaProfilerStart()
     t_host0 = time.perf_counter()
     ev0.record(stream)
     for i in range(K):
@@ -411,6 +427,8 @@ def main():
         cache.swa_decode_step(n, RATIO, q, k, v, out)
     ev1.record(stream)
     torch.cuda.synchronize()
+    if args.profile_only:
+        torch.cuda.cudart().cudaProfilerStop()
     if sampler:
         sampler.mark(t_host0, time.perf_counter())
     launches = api.launch_count() - launches0
@@ -477,6 +495,12 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_only:
         cpu = cpu_baseline(cfg, n_first + K // 2)
 
+    traffic = {}
+    try:  # DRAM bytes of one attend launch from the committed ncu --set full capture (scripts/profile_round.sh)
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(str(args.config), {}) if args.variant == "swa" else {}
+    except (OSError, ValueError):
+        traffic = {}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
@@ -487,7 +511,9 @@ def main():
                        "parallelism": f"batch-sharded x{world} (no collective)", "rank0_batch_offset": b0,
                        "l2": "inputs larger than L2 (per-step KV gather >> 126 MB)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic.get("dram_bytes"),
+                         "traffic_capture": traffic or None,
+                         "frac_nominal_8tbs": achieved / 8000.0 if achieved else None,
                          "peak_kind": peak_kind, "kernel": "skvd::swa_attend_kernel", "launch": launch_cfg,
                          "algo_bytes_per_launch": chain_algo / chain_n if chain_n else None,
                          "kernel_ms_avg": chain_ms / chain_n if chain_n else None,
@@ -501,6 +527,10 @@ def main():
                          "step_note": "attend algorithmic bytes of the timed region / timed region "
                                       "(includes select kernels and launch gaps; layers chained with PDL)"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "prefill": prefill,
+            "profile_capture": {"n_first": n_first, "attend_algo_bytes_first_step": attend_algo_bytes(cfg, n_first),
+                                "note": "--profile-only: ncu --profile-from-start off sees the timed region only; "
+                                        "attend launch i of it is layer i % L of step n_first + i // L"}
+            if args.profile_only else None,
             "clocks": dict(sampler.summary(), window="sm_mhz: median over the timed region's samples (else the whole run); reasons: whole run") if sampler else None,
         }
         print(json.dumps(line), flush=True)
