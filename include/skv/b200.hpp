@@ -105,6 +105,20 @@ class DeviceCache {
     void importance(int layer, int b0, int nb, int len, double* dst, void* st = nullptr) const {
         check(skv_importance_get(c_, layer, b0, nb, len, dst, st));
     }
+    // Engine::prefill's attention on the tensor cores (engine.hpp:485-529)
+    void prefill_layer(int layer, int s, const void* q, void* out, void* st = nullptr) {
+        check(skv_prefill_layer(c_, layer, s, q, out, st));
+    }
+    void decode_step_host(int n, double r, const void* q, const void* k, const void* v, void* out,
+                          void* st = nullptr) {
+        check(skv_swa_decode_step_host(c_, n, r, q, k, v, out, st));
+    }
+    // Head sharding (B < #GPU): this cache holds heads [head_offset, +H) of
+    // total_heads; `reduce` sums the fp64 step row across the shards on the
+    // given stream, e.g. with ncclAllReduce.
+    void set_head_shard(int head_offset, int total_heads, skv_reduce_fn reduce, void* user) {
+        check(skv_cache_set_head_shard(c_, head_offset, total_heads, reduce, user));
+    }
 
   private:
     skv_cache* c_ = nullptr;

@@ -173,6 +173,24 @@ skv_status skv_selection_size(const skv_cache* cache, int n, double r, int32_t* 
  * sequence's last decode step of `layer`; dst [nb] fp64 (host or device). */
 skv_status skv_sparsity_get(const skv_cache* cache, int layer, int b0, int nb, double* dst, void* stream);
 
+/* ---- head sharding (SURVEY §8 e: when B < #GPU, e.g. config 1) -----------
+ * The selection ranks tokens by the attention weight summed over ALL heads
+ * (head_summed_accum, attention.hpp:77-85), so a cache that holds only heads
+ * [head_offset, head_offset + H) of total_heads needs, once per layer-step,
+ * the head-summed row of the step summed across the shards. The library
+ * calls `reduce(buf, count, stream, user)` at that point with `count` fp64
+ * values in device memory: it must sum `buf` element-wise across the shards
+ * in place, ordered on `stream` (ncclAllReduce(buf, buf, count, ncclDouble,
+ * ncclSum, comm, stream) is the intended body). Every shard
+ * then folds the same row and makes the same selection. q / k / v / out
+ * carry the shard's H heads. The tensor-core prefill's seed row and its
+ * sparsity are exchanged the same way. reduce = NULL restores the unsharded
+ * cache (head_offset 0, total_heads H or 0). Returning nonzero from reduce
+ * fails the calling entry point with that status. */
+typedef skv_status (*skv_reduce_fn)(double* buf, size_t count, void* stream, void* user);
+skv_status skv_cache_set_head_shard(skv_cache* cache, int head_offset, int total_heads, skv_reduce_fn reduce,
+                                    void* user);
+
 /* ---- KV residency bookkeeping for the three-phase schedule ----------------
  * SchedulePlan (scheduler.hpp:28-39) + the workload lengths step_actions reads
  * from CostParams (input_len s, output_len n). */

@@ -53,6 +53,11 @@ def build(force: bool = False) -> str:
     return SO_PATH
 
 
+# skv_reduce_fn (include/skv_b200.h): sum `count` device fp64 values in place
+# across the head shards, ordered on `stream`.
+REDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+
+
 def _declare(lib):
     P, I, I64, U64, SZ, D = C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.c_size_t, C.c_double
     sig = {
@@ -85,6 +90,7 @@ def _declare(lib):
         "skv_solve_plan": (I, [P, P, P]),
         "skv_predict_plan": (I, [P, P, P]),
         "skv_cache_set_variant": (I, [P, I, I]),
+        "skv_cache_set_head_shard": (I, [P, I, I, REDUCE_FN, P]),
         "skv_selection_size": (I, [P, I, D, P, P]),
         "skv_sparsity_get": (I, [P, I, I, I, P, P]),
         "skv_ledger_set": (I, [P, I, I, I, I, P, P]),

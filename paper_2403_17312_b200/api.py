@@ -12,7 +12,8 @@ from dataclasses import dataclass
 
 import torch
 
-from ._lib import ContractViolation, CudaError, InfeasiblePlan, OutOfDeviceMemory, Unsupported, check, lib  # noqa: F401
+from ._lib import (REDUCE_FN, ContractViolation, CudaError, InfeasiblePlan, OutOfDeviceMemory,  # noqa: F401
+                   Unsupported, check, lib)
 
 SKV_F32, SKV_F16, SKV_BF16, SKV_U8 = 0, 1, 2, 3
 _DT = {torch.float32: SKV_F32, torch.float16: SKV_F16, torch.bfloat16: SKV_BF16, torch.uint8: SKV_U8}
@@ -40,6 +41,15 @@ def _ptr(t: torch.Tensor | None):
     if not t.is_contiguous():
         raise ContractViolation("contiguous tensor required")
     return C.c_void_p(t.data_ptr())
+
+
+class _DeviceView:
+    """A device fp64 buffer owned by the library, seen by torch through
+    __cuda_array_interface__ (no copy)."""
+
+    def __init__(self, ptr: int, count: int, device: int):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8", "data": (int(ptr), False),
+                                         "version": 3, "strides": None, "stream": None}
 
 
 # ---- attention.hpp:122-138 -------------------------------------------------
@@ -196,6 +206,31 @@ class SwaCache:
         h = C.c_void_p()
         check(lib().skv_cache_create(C.byref(d), C.byref(h)))
         self._h = h
+
+    def set_head_shard(self, head_offset: int, total_heads: int, reduce=None):
+        """Hold heads [head_offset, head_offset + heads) of a model with
+        total_heads (SURVEY §8 e). `reduce(buf, stream)` gets a device fp64
+        tensor viewing the library's exchange row and must sum it in place
+        across the shards, ordered on `stream` (a torch.cuda.ExternalStream),
+        e.g. shard.dist_reducer(). reduce=None: unsharded again."""
+        if reduce is None:
+            self._reduce_cb = None
+            check(lib().skv_cache_set_head_shard(self._h, 0, 0, REDUCE_FN(), None))
+            return
+        dev = self.dev
+
+        def _cb(ptr, count, stream, _user):
+            try:
+                buf = torch.as_tensor(_DeviceView(ptr, count, dev.index), device=dev)
+                reduce(buf, torch.cuda.ExternalStream(stream or 0, device=dev))
+                return 0
+            except Exception as e:  # surfaces as the entry point's error
+                import sys
+                print(f"skv head-shard reduce failed: {e!r}", file=sys.stderr)
+                return 4  # SKV_ERR_CUDA
+
+        self._reduce_cb = REDUCE_FN(_cb)
+        check(lib().skv_cache_set_head_shard(self._h, head_offset, total_heads, self._reduce_cb, None))
 
     def close(self):
         if getattr(self, "_h", None):

@@ -138,6 +138,12 @@ struct skv_cache {
     size_t stage_bytes = 0;
     cudaStream_t h2d = nullptr, d2h = nullptr;
     std::vector<cudaEvent_t> ev_in, ev_comp, ev_out;  // per chunk
+    // head sharding: this cache holds heads [head_offset, head_offset + H) of
+    // total_heads; the head-summed rows are summed across shards by `reduce`
+    skv_reduce_fn reduce = nullptr;
+    void* reduce_user = nullptr;
+    int head_offset = 0, total_heads = 0;
+    double* xbuf = nullptr;  // [B][Ncap] step rows / prefill seed rows, then [B] prefill sparsity
     // measurement
     bool prof = false;
     std::vector<cudaEvent_t> ev;  // start/stop pairs
@@ -272,6 +278,7 @@ skv_status skv_cache_destroy(skv_cache* c) {
     cudaFree(c->rec_map);
     cudaFree(c->rec_m);
     cudaFree(c->stage);
+    cudaFree(c->xbuf);
     for (auto* v : {&c->ev_in, &c->ev_comp, &c->ev_out})
         for (cudaEvent_t e : *v) cudaEventDestroy(e);
     if (c->h2d) cudaStreamDestroy(c->h2d);
@@ -512,12 +519,14 @@ void note_pending(skv_cache* c, int layer, const skvd::SelectParams& p, double r
 // The standalone per-sequence select kernel (skv_select.cuh).
 skv_status launch_select_c(skv_cache* c, int layer, int apply, const int* tok_prev, long long tok_prev_ld,
                            int m_prev, int G, int cur_tok, int n_next, double r_next, bool pdl, cudaStream_t st,
-                           int sp_n = 0) {
+                           int sp_n = 0, double* wsum_out = nullptr, const double* wsum = nullptr) {
     skvd::SelectParams p;
     c->pend_n[layer] = -1;
     if (skv_status e = make_select_params(c, layer, apply, tok_prev, tok_prev_ld, m_prev, G, cur_tok, n_next, r_next,
                                           sp_n, &p))
         return e;
+    p.wsum_out = wsum_out;
+    p.wsum = wsum;
     if (!p.apply && !p.select) return SKV_OK;
     SKV_CUDA(launch_select(p, c->d.batch, pdl, st));
     note_pending(c, layer, p, r_next);
@@ -551,6 +560,7 @@ skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok
         // 0.98->1.02, 0.88->1.01), not for n-k in the thousands (config 4:
         // 0.88->0.79), which keep the separate select kernel.
         if (select_key_bytes(sel) > std::min<size_t>(dl->ring_bytes, 2048 * 8)) fused = false;
+        if (c->reduce) fused = false;  // the step row is summed across head shards first
     }
     const size_t lt = static_cast<size_t>(layer) * c->d.batch * c->d.capacity;
     skvd::AttendParams p{};
@@ -612,6 +622,19 @@ skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok
     if (fold.apply) {
         if (fused) {
             note_pending(c, layer, sel, fold.r_next);
+        } else if (c->reduce) {
+            // head shards: this shard's head-summed row -> all-reduce across
+            // the shards (the caller's collective, ordered on st) -> fold it
+            // and select; every shard then holds the same importance and
+            // makes the same selection.
+            if (skv_status e = launch_select_c(c, layer, fold.apply, tok, tok_ld, m, G, fold.cur_tok, 0, 0.0,
+                                               !c->prof, st, 0, c->xbuf, nullptr))
+                return e;
+            if (skv_status e = c->reduce(c->xbuf, static_cast<size_t>(c->d.batch) * m, st, c->reduce_user))
+                return fail(e, "head-shard reduce failed (%d)", static_cast<int>(e));
+            if (skv_status e = launch_select_c(c, layer, fold.apply, tok, tok_ld, m, G, fold.cur_tok, fold.n_next,
+                                               fold.r_next, false, st, fold.sp_n, nullptr, c->xbuf))
+                return e;
         } else {  // fold + select in the separate kernel instead
             const int* tp = tok;
             if (skv_status e = launch_select_c(c, layer, fold.apply, tp, tok_ld, m, G, fold.cur_tok, fold.n_next,
@@ -797,9 +820,24 @@ skv_status skv_prefill_layer(skv_cache* c, int layer, int s, const void* q, void
         SKV_CUDA(cudaMemset(c->pf_sparsity, 0, bytes));
     }
     const size_t lay = static_cast<size_t>(layer);
-    SKV_CUDA(launch_prefill(c->d.q_dtype == SKV_BF16, c->d.out_f32 != 0, c->kv + lay * c->layer_bytes, q, out,
-                            c->imp + lay * B * c->d.capacity, c->d.capacity, c->pf_sparsity + lay * B, B, H,
-                            c->d.head_dim, c->d.capacity, s, c->pf_scratch, st));
+    double* imp = c->imp + lay * B * c->d.capacity;
+    double* psp = c->pf_sparsity + lay * B;
+    if (c->reduce) {
+        // head shards: seed rows and the sparsity share (local sum / all heads)
+        // into xbuf, summed across the shards, then into the importance
+        double* xs = c->xbuf + static_cast<size_t>(B) * c->d.capacity;
+        SKV_CUDA(launch_prefill(c->d.q_dtype == SKV_BF16, c->d.out_f32 != 0, c->kv + lay * c->layer_bytes, q, out,
+                                c->xbuf, c->d.capacity, xs, B, H, c->d.head_dim, c->d.capacity, s, c->pf_scratch, st,
+                                c->total_heads));
+        if (skv_status e = c->reduce(c->xbuf, static_cast<size_t>(B) * (c->d.capacity + 1), st, c->reduce_user))
+            return fail(e, "head-shard reduce failed (%d)", static_cast<int>(e));
+        SKV_CUDA(cudaMemcpy2DAsync(imp, c->d.capacity * 8, c->xbuf, c->d.capacity * 8, static_cast<size_t>(s) * 8,
+                                   B, cudaMemcpyDeviceToDevice, st));
+        SKV_CUDA(cudaMemcpyAsync(psp, xs, static_cast<size_t>(B) * 8, cudaMemcpyDeviceToDevice, st));
+    } else {
+        SKV_CUDA(launch_prefill(c->d.q_dtype == SKV_BF16, c->d.out_f32 != 0, c->kv + lay * c->layer_bytes, q, out,
+                                imp, c->d.capacity, psp, B, H, c->d.head_dim, c->d.capacity, s, c->pf_scratch, st));
+    }
     c->pend_n[layer] = -1;  // importance changed: any pending selection is stale
     return SKV_OK;
 }
@@ -1069,6 +1107,37 @@ skv_status skv_cache_attach_recompute(skv_cache* c, int layer, const void* x_ln1
         return fail(SKV_ERR_OOM, "recompute: cannot allocate buffers");
     SKV_CUDA(launch_transpose_kv_weights(wk, wv, c->rec_wt[layer], static_cast<int>(h), st));
     c->rec_x[layer] = static_cast<const uint8_t*>(x_ln1);
+    return SKV_OK;
+}
+
+skv_status skv_cache_set_head_shard(skv_cache* c, int head_offset, int total_heads, skv_reduce_fn reduce,
+                                    void* user) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    if (reduce == nullptr) {
+        SKV_REQUIRE(head_offset == 0 && (total_heads == 0 || total_heads == c->d.heads),
+                    "head shard: a cache without a reduce holds every head");
+        c->reduce = nullptr;
+        c->reduce_user = nullptr;
+        c->head_offset = 0;
+        c->total_heads = c->d.heads;
+        return SKV_OK;
+    }
+    SKV_REQUIRE(total_heads >= c->d.heads && head_offset >= 0 && head_offset + c->d.heads <= total_heads,
+                "head shard: heads [offset, offset + H) must lie inside total_heads");
+    DeviceGuard guard(c->d.device);
+    if (c->xbuf == nullptr) {
+        const size_t bytes = static_cast<size_t>(c->d.batch) * (c->d.capacity + 1) * 8;
+        if (cudaMalloc(reinterpret_cast<void**>(&c->xbuf), bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(SKV_ERR_OOM, "head shard: cannot allocate the exchange row");
+        }
+        SKV_CUDA(cudaMemset(c->xbuf, 0, bytes));
+        c->device_bytes += bytes;
+    }
+    c->reduce = reduce;
+    c->reduce_user = user;
+    c->head_offset = head_offset;
+    c->total_heads = total_heads;
     return SKV_OK;
 }
 

@@ -47,7 +47,7 @@ cudaError_t launch_gemm_tn(const void* A, const void* Bt, float* C, const int* m
                            bool bf16, cudaStream_t st, const skvd::KvScatter* sc = nullptr);
 cudaError_t launch_prefill(bool bf16, bool out_f32, const void* kv, const void* q, void* out, double* imp,
                            long long imp_ld, double* psp, int B, int H, int D, int Ncap, int s, uint8_t* scratch,
-                           cudaStream_t st);
+                           cudaStream_t st, int h_div = 0);
 size_t prefill_scratch_bytes(int B, int H, int s);
 cudaError_t launch_recompute_gather(const uint8_t* x, long long x_seq, long long x_row, const int* lists,
                                     const int* counts, long long list_ld, uint8_t* A, int2* rowmap, int* m_out,

@@ -562,14 +562,14 @@ __global__ void __launch_bounds__(kFThreads, 1)
 // sparsity counts (engine.hpp:513-518).
 __global__ void prefill_seed_kernel(const float* __restrict__ wlast, const float* __restrict__ llast,
                                     const unsigned* __restrict__ below, double* __restrict__ imp,
-                                    double* __restrict__ psp, int H, int s, long long imp_ld) {
+                                    double* __restrict__ psp, int H, int s, long long imp_ld, int h_div) {
     const int b = blockIdx.y;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (psp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
         const double cells = 0.5 * static_cast<double>(s) * static_cast<double>(s + 1);
         double sp = 0.0;
         for (int h = 0; h < H; ++h) sp += static_cast<double>(below[b * H + h]) / cells;
-        psp[b] = sp / static_cast<double>(H);
+        psp[b] = sp / static_cast<double>(h_div);  // h_div = all heads of the model (H unless head-sharded)
     }
     if (j >= s) return;
     double acc = 0.0;
@@ -649,7 +649,7 @@ size_t prefill_scratch_bytes(int B, int H, int s) {
 // out_f32); imp: layer importance [B][imp_ld]; psp (nullable): [B].
 cudaError_t launch_prefill(bool bf16, bool out_f32, const void* kv, const void* q, void* out, double* imp,
                            long long imp_ld, double* psp, int B, int H, int D, int Ncap, int s, uint8_t* scratch,
-                           cudaStream_t st) {
+                           cudaStream_t st, int h_div) {
     if (D != 128) return cudaErrorInvalidValue;
     const int Z = B * H, nqt = (s + kFTile - 1) / kFTile;
     const uint64_t HD = static_cast<uint64_t>(H) * D;
@@ -682,7 +682,8 @@ cudaError_t launch_prefill(bool bf16, bool out_f32, const void* kv, const void* 
     if (e != cudaSuccess) return e;
     e = bf16 ? run_flash<true, false>(mq, mkv, p, st) : run_flash<false, false>(mq, mkv, p, st);
     if (e != cudaSuccess) return e;
-    prefill_seed_kernel<<<dim3((s + 255) / 256, B), 256, 0, st>>>(wlast, llast, below, imp, psp, H, s, imp_ld);
+    prefill_seed_kernel<<<dim3((s + 255) / 256, B), 256, 0, st>>>(wlast, llast, below, imp, psp, H, s, imp_ld,
+                                                                  h_div > 0 ? h_div : H);
     count_launch();
     return cudaGetLastError();
 }

@@ -37,6 +37,12 @@ struct SelectParams {
     int* idx;  // [B][idx_ld]
     long long idx_ld;
     int pdl_wait;
+    // head sharding (the cache holds some of the model's heads): the step row
+    // v[pos] = sum over ALL heads of w is summed across the shards between a
+    // partial pass (wsum_out: this shard's head sum, nothing else) and the
+    // fold (wsum: the all-reduced row, used instead of the local partials).
+    double* wsum_out;    // [B][m_prev]
+    const double* wsum;  // [B][m_prev]
 };
 
 __host__ __device__ inline size_t select_smem(int nc) {
@@ -60,10 +66,22 @@ __device__ void fold_and_select(const SelectParams& p, int b, int tid, TopkSmem<
     if (p.apply) {
         const float* wp = p.wpart + static_cast<size_t>(b) * p.G * p.m_prev;
         const int* tp = p.tok_prev ? p.tok_prev + static_cast<size_t>(b) * p.tok_prev_ld : nullptr;
-        double vmax = 0.0;
-        for (int pos = tid; pos < p.m_prev; pos += NT) {
+        const double* ws = p.wsum ? p.wsum + static_cast<size_t>(b) * p.m_prev : nullptr;
+        // the head-summed weight of selected position pos, in fixed group order
+        auto row = [&](int pos) {
+            if (ws) return ws[pos];
             double v = 0.0;
             for (int g = 0; g < p.G; ++g) v += static_cast<double>(__ldcg(wp + static_cast<size_t>(g) * p.m_prev + pos));
+            return v;
+        };
+        if (p.wsum_out) {  // head-shard partial pass: this shard's sum only
+            double* wo = p.wsum_out + static_cast<size_t>(b) * p.m_prev;
+            for (int pos = tid; pos < p.m_prev; pos += NT) wo[pos] = row(pos);
+            return;
+        }
+        double vmax = 0.0;
+        for (int pos = tid; pos < p.m_prev; pos += NT) {
+            const double v = row(pos);
             const int t = tp ? tp[pos] : pos;
             imp[t] = (p.apply == 2 || t == p.cur_tok) ? v : imp[t] + v;
             vmax = v > vmax ? v : vmax;
@@ -83,12 +101,7 @@ __device__ void fold_and_select(const SelectParams& p, int b, int tid, TopkSmem<
             for (int w = 0; w < NT / 32; ++w) mx = sc.red_max[w] > mx ? sc.red_max[w] : mx;
             const double thr = 0.01 * mx;
             int below = 0;
-            for (int pos = tid; pos < p.m_prev; pos += NT) {
-                double v = 0.0;
-                for (int g = 0; g < p.G; ++g)
-                    v += static_cast<double>(__ldcg(wp + static_cast<size_t>(g) * p.m_prev + pos));
-                below += v < thr;
-            }
+            for (int pos = tid; pos < p.m_prev; pos += NT) below += row(pos) < thr;
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) below += __shfl_xor_sync(0xffffffffu, below, off);
             if (lane == 0) sc.red_cnt[warp] = below;

@@ -1,4 +1,5 @@
-"""Multi-GPU plumbing for the SWA decode path: batch sharding.
+"""Multi-GPU plumbing for the SWA decode path: batch sharding (the default)
+and head sharding (when there are fewer sequences than GPUs).
 
 Selection is per (sequence, layer) (attention.hpp:235-244), so sequences are
 independent: each rank owns a contiguous slice of the batch and runs the
@@ -46,3 +47,34 @@ def gather_batch(local: torch.Tensor, global_batch: int) -> torch.Tensor:
     dist.all_gather(parts, pad)
     out = [parts[r][: shard_range(global_batch, world, r)[1]] for r in range(world)]
     return torch.cat(out, 0)
+
+
+def head_shard_range(heads: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous heads [h0, h0 + nh) of `heads` for `rank` (same split rule
+    as shard_range). Head sharding is for B < #GPU (SURVEY §8 e): attention
+    per head is independent, only the head-summed step row that ranks the
+    tokens (head_summed_accum, attention.hpp:77-85) crosses ranks."""
+    if heads < world:
+        raise ValueError(f"{heads} heads cannot be split over {world} ranks")
+    return shard_range(heads, world, rank)
+
+
+def dist_reducer(group=None):
+    """The head-shard exchange (SwaCache.set_head_shard): one SUM all-reduce
+    of the fp64 step row across the process group. NCCL (over NVLink on a
+    GPU box) is enqueued on the library's stream, so the exchange stays
+    asynchronous; host-transport backends (gloo: the -m gpu tests, where two
+    ranks share one GPU) synchronise the stream and reduce a host copy."""
+
+    def reduce(buf: torch.Tensor, stream) -> None:
+        if dist.get_backend(group) == "nccl":
+            with torch.cuda.stream(stream):
+                dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+            return
+        stream.synchronize()
+        host = buf.cpu()
+        dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)
+        buf.copy_(host)  # on the current stream: synchronise it before the library reads buf
+        torch.cuda.current_stream(buf.device).synchronize()
+
+    return reduce

@@ -21,7 +21,7 @@ def lib():
 
 
 def declared():
-    src = open(HEADER).read()
+    src = "\n".join(ln for ln in open(HEADER).read().splitlines() if not ln.lstrip().startswith("typedef"))
     return sorted(set(re.findall(r"\b(skv_[a-z0-9_]+)\s*\(", src)))
 
 
