@@ -694,10 +694,8 @@ skv_status launch_movement(skv_cache* c, int layer, bool pdl, cudaStream_t st) {
     mp.tok_bytes = static_cast<long long>(c->tok_bytes);
     mp.seq_bytes = static_cast<long long>(c->tok_bytes) * c->d.capacity;
     mp.poison = c->poison ? 1 : 0;
-    mp.which = 0;
+    mp.which = -1;  // offload and reload in one launch: both PCIe directions at once
     SKV_CUDA(launch_move(mp, c->d.batch, c->d.capacity, pdl, st));
-    mp.which = 2;
-    SKV_CUDA(launch_move(mp, c->d.batch, c->d.capacity, true, st));
     if (c->rec_x[layer]) {
         // recompute_kv for this step's list: gather the retained rows, one
         // tcgen05 GEMM against [Wk | Wv]^T, K/V written straight into the rows

@@ -169,26 +169,47 @@ __global__ void transpose_kv_weights_kernel(const uint16_t* __restrict__ wk, con
         bt[static_cast<size_t>(which * h + j0 + r) * h + i0 + threadIdx.x] = tile[threadIdx.x][r];
 }
 
-// Offload / reload the rows of one action list: grid (token chunk, sequence).
-// 16-byte vectors; the host side is mapped pinned memory (PCIe zero-copy).
+// Ascending list membership (the ledger's lists are in token order).
+__device__ __forceinline__ bool in_sorted(const int* list, int cnt, int t) {
+    int lo = 0, hi = cnt;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(list + mid) < t) lo = mid + 1; else hi = mid;
+    }
+    return lo < cnt && __ldg(list + lo) == t;
+}
+
+// Offload / reload the rows of one action list: grid (token chunk, sequence[,
+// direction]). 16-byte vectors; the host side is mapped pinned memory (PCIe
+// zero-copy). With which = -1 one launch runs both lists at once, offload on
+// blockIdx.z 0 and reload on 1, so device->host writes and host->device reads
+// share the PCIe link in both directions. A token on both lists (offloaded
+// and selected in the same step, scheduler.hpp:360-375) keeps its device row:
+// the offload copies it out without poisoning it and the reload skips it --
+// the state the sequential offload-then-reload leaves behind.
 __global__ void __launch_bounds__(256) kv_move_kernel(const MoveParams p) {
     pdl_launch_dependents();
     pdl_wait();  // the lists come from the preceding ledger kernel
     const int b = blockIdx.y;
-    const int cnt = p.counts[b * 4 + p.which];
-    const int* list = p.lists + (static_cast<size_t>(b) * 4 + p.which) * p.list_ld;
+    const bool both = p.which < 0;
+    const int which = both ? (blockIdx.z == 0 ? 0 : 2) : p.which;
+    const int cnt = p.counts[b * 4 + which];
+    const int* list = p.lists + (static_cast<size_t>(b) * 4 + which) * p.list_ld;
+    const int ocnt = both ? p.counts[b * 4 + (2 - which)] : 0;
+    const int* other = p.lists + (static_cast<size_t>(b) * 4 + (2 - which)) * p.list_ld;
     const long long vec_per_tok = p.tok_bytes / 16;
     const long long total = static_cast<long long>(cnt) * vec_per_tok;
     for (long long v = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; v < total;
          v += static_cast<long long>(gridDim.x) * blockDim.x) {
         const int t = list[v / vec_per_tok];
+        const bool shared = both && in_sorted(other, ocnt, t);
         const size_t off = static_cast<size_t>(b) * p.seq_bytes + static_cast<size_t>(t) * p.tok_bytes +
                            static_cast<size_t>(v % vec_per_tok) * 16;
-        if (p.which == 0) {
+        if (which == 0) {
             uint4* d = reinterpret_cast<uint4*>(p.dev + off);
             *reinterpret_cast<uint4*>(p.host + off) = *d;
-            if (p.poison) *d = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-        } else {
+            if (p.poison && !shared) *d = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+        } else if (!shared) {
             *reinterpret_cast<uint4*>(p.dev + off) = *reinterpret_cast<const uint4*>(p.host + off);
         }
     }
@@ -411,7 +432,7 @@ cudaError_t launch_move(const MoveParams& p, int batch, int max_tokens, bool pdl
     const int blocks = static_cast<int>(std::min<long long>((vecs + 255) / 256, 64));
     if (blocks <= 0) return cudaSuccess;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(blocks, batch);
+    cfg.gridDim = dim3(blocks, batch, p.which < 0 ? 2 : 1);
     cfg.blockDim = dim3(256);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];

@@ -49,7 +49,8 @@ struct MoveParams {
     long long list_ld;
     long long tok_bytes; // 2*H*row bytes
     long long seq_bytes; // Ncap * tok_bytes
-    int which;           // 0 offload (device -> host), 2 reload (host -> device)
+    int which;           // 0 offload (device -> host), 2 reload (host -> device),
+                         // -1 both at once (blockIdx.z 0 / 1): the two PCIe directions overlap
     int poison;          // offload: overwrite the device row with 0xFF (NaN) afterwards
 };
 
