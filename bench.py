@@ -36,9 +36,9 @@ CONFIGS = {
     1: dict(name="config1: single SWA layer fp32 b=1 H=32 D=128 n=512 r=0.2", L=1, B=1, H=32, s=511,
             kv="f32", q="f32"),
     2: dict(name="config2: OPT-6.7B attention shape fp16 L=32 H=32 D=128 b=64 s=512 decode r=0.2",
-            L=32, B=64, H=32, s=512, kv="f16", q="f16"),
+            L=32, B=64, H=32, s=512, kv="f16", q="f16", decode=512),
     3: dict(name="config3: OPT-13B attention shape bf16 L=40 H=40 D=128 s=1024 decode r=0.2, 16 seq/GPU",
-            L=40, B=16, H=40, s=1024, kv="bf16", q="bf16"),
+            L=40, B=16, H=40, s=1024, kv="bf16", q="bf16", decode=1024),
     4: dict(name="config4: OPT-30B attention shape L=48 H=56 D=128 n=4096 INT8 KV (fp16 q) b=32 r=0.2",
             L=48, B=32, H=56, s=4095, kv="u8", q="f16"),
     5: dict(name="config5: three-phase schedule sweep, OPT-6.7B attention shape fp16 L=32 H=32 D=128, "
@@ -47,6 +47,20 @@ CONFIGS = {
 }
 RATIO = 0.2
 D = 128
+
+
+def timed_window(cfg, W: int, K: int):
+    """-> (warm-up steps, first timed n). Configs with a decode length
+    (2: n = 513..1024, 3: n = 1025..2048) centre the K timed steps on the
+    middle of that decode: a step's bytes grow linearly with n, so the mean
+    over the window equals the mean over the whole decode, and tokens/s is the
+    full decode's. The steps before the window are untimed warm-up."""
+    s, dec = cfg["s"], cfg.get("decode")
+    n_first = s + W + 1
+    if dec and K < dec:
+        centre = s + (dec + 1) / 2.0  # mean n of n = s+1 .. s+dec
+        n_first = max(n_first, int(round(centre - (K - 1) / 2.0)))
+    return n_first - s - 1, n_first
 
 
 def peaks():
@@ -186,7 +200,7 @@ def run_reference(args, cfg, rank: int, world: int):
     """--impl reference: the reference CPU implementation on this box's cores."""
     if rank != 0:
         return
-    n_mid = cfg["s"] + 1 + args.warmup + args.steps // 2
+    n_mid = timed_window(cfg, args.warmup, args.steps)[1] + args.steps // 2
     budget = max(0.5, min(15.0, 120.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
         cpu_baseline(cfg, n_mid, budget_s=budget / 4)
@@ -304,6 +318,8 @@ def main():
                     help="attention variant (engine.hpp:531-569); dense = the full-KV decode baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-centre", action="store_true",
+                    help="time the first K decode steps instead of centring them on the config's decode")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no clocks/baseline/e2e)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
@@ -347,6 +363,8 @@ def main():
         b0, _ = shard_range(world * cfg["B"], world, rank)
     seqs = B if head_shard else world * B  # sequences decoded by the whole job per step
     W, K = args.warmup, args.steps
+    if not args.no_centre:
+        W, _ = timed_window(cfg, W, K)
     e2e_steps = 0 if (args.no_e2e or args.profile_only) else max(3, min(K, 50))
     ncap = s + W + K + min(K, 10) + e2e_steps + (2 if e2e_steps else 0) + 1
     qdt = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[cfg["q"]]
@@ -513,11 +531,16 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+            "warmup_requested": args.warmup,
             "ms_per_step": elapsed_ms / K, "higher_is_better": True,
             "scaling": "strong" if head_shard else "weak",
             "vs_baseline": None, "dtype": cfg["kv"], "data": "synthetic (torch.randn K/V/q, seeded)",
             "config": {"workload": cfg["name"], "variant": args.variant, "per_gpu_batch": B, "global_batch": seqs, "layers": L,
                        "heads": H, "head_dim": D, "ratio": RATIO, "n_range": [n_first, n_first + K - 1],
+                       "decode_window": (f"timed steps centred on the {cfg['decode']}-step decode "
+                                         f"(n = {s + 1}..{s + cfg['decode']}): step cost is linear in n, so the "
+                                         "window's mean is the whole decode's; earlier steps are untimed warm-up")
+                       if cfg.get("decode") and not args.no_centre else "steady state at the config's KV length",
                        "parallelism": (f"head-sharded x{world} ({H} of {cfg['H']} heads per GPU; one fp64 "
                                        "all-reduce of the step row per layer-step over NCCL)") if head_shard
                        else f"batch-sharded x{world} (no collective)", "rank0_batch_offset": b0,
