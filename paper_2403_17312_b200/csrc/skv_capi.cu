@@ -144,6 +144,12 @@ struct skv_cache {
     void* reduce_user = nullptr;
     int head_offset = 0, total_heads = 0;
     double* xbuf = nullptr;  // [B][Ncap] step rows / prefill seed rows, then [B] prefill sparsity
+    // whole-step decode with separate select kernels: the layers' fold+select
+    // launches are collected and issued as one batched launch after the
+    // step's attends (they only feed the next step), instead of one select
+    // CTA set interleaved with every attend
+    bool defer_select = false;
+    std::vector<std::pair<int, skvd::SelectParams>> deferred;  // (layer, params)
     // measurement
     bool prof = false;
     std::vector<cudaEvent_t> ev;  // start/stop pairs
@@ -635,6 +641,14 @@ skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok
             if (skv_status e = launch_select_c(c, layer, fold.apply, tok, tok_ld, m, G, fold.cur_tok, fold.n_next,
                                                fold.r_next, false, st, fold.sp_n, nullptr, c->xbuf))
                 return e;
+        } else if (c->defer_select) {
+            skvd::SelectParams sp;
+            if (skv_status e = make_select_params(c, layer, fold.apply, tok, tok_ld, m, G, fold.cur_tok, fold.n_next,
+                                                  fold.r_next, fold.sp_n, &sp))
+                return e;
+            c->pend_n[layer] = -1;
+            c->deferred.emplace_back(layer, sp);
+            note_pending(c, layer, sp, fold.r_next);
         } else {  // fold + select in the separate kernel instead
             const int* tp = tok;
             if (skv_status e = launch_select_c(c, layer, fold.apply, tp, tok_ld, m, G, fold.cur_tok, fold.n_next,
@@ -868,15 +882,39 @@ static skv_status decode_layers(skv_cache* c, int l0, int l1, int n, double r, c
                                 const void* v_new, void* out, cudaStream_t st) {
     const size_t per_layer = static_cast<size_t>(c->d.batch) * c->d.heads * c->d.head_dim * dtype_size(c->d.q_dtype);
     const size_t per_layer_out = static_cast<size_t>(c->d.batch) * c->d.heads * c->d.head_dim * out_size(c);
-    for (int l = l0; l < l1; ++l) {
+    // Selects that cannot ride in the attend tail are batched after the
+    // layers (plans and head shards need them per layer: ledger / exchange).
+    c->defer_select = !c->has_plan && !c->reduce && !c->prof;
+    c->deferred.clear();
+    skv_status status = SKV_OK;
+    for (int l = l0; l < l1 && status == SKV_OK; ++l) {
         const size_t o = per_layer * l;
-        if (skv_status s = decode_layer_impl(c, l, n, r, static_cast<const uint8_t*>(q) + o,
-                                             static_cast<const uint8_t*>(k_new) + o,
-                                             static_cast<const uint8_t*>(v_new) + o,
-                                             static_cast<uint8_t*>(out) + per_layer_out * l, nullptr, nullptr,
-                                             l > l0, st))
-            return s;
+        status = decode_layer_impl(c, l, n, r, static_cast<const uint8_t*>(q) + o,
+                                   static_cast<const uint8_t*>(k_new) + o, static_cast<const uint8_t*>(v_new) + o,
+                                   static_cast<uint8_t*>(out) + per_layer_out * l, nullptr, nullptr, l > l0, st);
     }
+    c->defer_select = false;
+    if (status != SKV_OK || c->deferred.empty()) {
+        c->deferred.clear();
+        return status;
+    }
+    // One launch over the deferred layers (consecutive, same shape), in
+    // plain stream order: it needs every attend of the range complete, and
+    // the PDL-chained attends only order against their direct predecessor.
+    skvd::SelectParams p = c->deferred.front().second;
+    const int first = c->deferred.front().first;
+    const int cnt = static_cast<int>(c->deferred.size());
+    for (int i = 0; i < cnt; ++i)
+        SKV_REQUIRE(c->deferred[i].first == first + i && c->deferred[i].second.m_prev == p.m_prev &&
+                        c->deferred[i].second.G == p.G,
+                    "decode_step: deferred selects must be consecutive layers of one shape");
+    p.ls_imp = static_cast<long long>(c->d.batch) * c->d.capacity;
+    p.ls_wpart = static_cast<long long>(c->d.batch) * c->d.heads * c->d.capacity;
+    p.ls_idx = static_cast<long long>(c->d.batch) * c->d.capacity;
+    p.ls_sp = c->d.batch;
+    p.pdl_wait = 0;
+    c->deferred.clear();
+    SKV_CUDA(launch_select(p, c->d.batch, false, st, cnt));
     return SKV_OK;
 }
 

@@ -223,7 +223,18 @@ __global__ void __launch_bounds__(kSelectThreads) swa_select_kernel(const Select
     __shared__ SelectScratch<kSelectThreads> scratch;
     pdl_launch_dependents();
     if (p.pdl_wait) pdl_wait();
-    fold_and_select<kSelectThreads, 1>(p, blockIdx.x, threadIdx.x, s, keys, scratch);
+    if (blockIdx.y == 0) {
+        fold_and_select<kSelectThreads, 1>(p, blockIdx.x, threadIdx.x, s, keys, scratch);
+        return;
+    }
+    SelectParams q = p;  // layer blockIdx.y of a batched launch
+    const long long y = blockIdx.y;
+    q.imp += y * p.ls_imp;
+    q.wpart += y * p.ls_wpart;
+    q.idx += y * p.ls_idx;
+    if (q.tok_prev) q.tok_prev += y * p.ls_idx;
+    q.sparsity += y * p.ls_sp;
+    fold_and_select<kSelectThreads, 1>(q, blockIdx.x, threadIdx.x, s, keys, scratch);
 }
 
 // top_k_indices (matrix.hpp:162-176) per row.
@@ -386,14 +397,14 @@ __global__ void cache_read_kernel(const uint8_t* __restrict__ kv, float* __restr
 namespace skv_impl {
 using namespace skvd;
 
-cudaError_t launch_select(const SelectParams& p, int batch, bool pdl, cudaStream_t st) {
+cudaError_t launch_select(const SelectParams& p, int batch, bool pdl, cudaStream_t st, int layers) {
     const int nc = (p.select && !p.dense) ? p.n - p.k : 0;
     const size_t smem = select_smem(nc);
     cudaError_t e = cudaFuncSetAttribute(swa_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(batch);
+    cfg.gridDim = dim3(batch, layers);
     cfg.blockDim = dim3(kSelectThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;

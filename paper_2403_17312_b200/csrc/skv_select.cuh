@@ -17,7 +17,11 @@
 
 namespace skvd {
 
-constexpr int kSelectThreads = 256;
+#ifndef SKV_SELECT_THREADS
+#define SKV_SELECT_THREADS 256
+#endif
+// standalone select width (256 measured best: it must fit beside attend CTAs)
+constexpr int kSelectThreads = SKV_SELECT_THREADS;
 
 struct SelectParams {
     double* imp;  // [B][imp_ld]
@@ -43,6 +47,9 @@ struct SelectParams {
     // fold (wsum: the all-reduced row, used instead of the local partials).
     double* wsum_out;    // [B][m_prev]
     const double* wsum;  // [B][m_prev]
+    // several layers in one launch (blockIdx.y = layer offset): element
+    // strides of imp, wpart, idx/tok_prev and sparsity per layer (0: one layer)
+    long long ls_imp, ls_wpart, ls_idx, ls_sp;
 };
 
 __host__ __device__ inline size_t select_smem(int nc) {

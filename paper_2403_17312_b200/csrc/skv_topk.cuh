@@ -16,6 +16,7 @@ template <int NT>
 struct TopkSmem {
     uint32_t hist[256];
     uint64_t warp_tot[NT / 32];
+    uint64_t warp_and[NT / 32], warp_or[NT / 32];
     uint64_t prefix;
     uint64_t mask;
     int remaining;
@@ -39,14 +40,51 @@ template <int NT, int BAR>
 __device__ void block_topk(const uint64_t* keys, int nc, int k, int* out, TopkSmem<NT>& s,
                            int tid) {
     const int lane = tid & 31, warp = tid >> 5;
+    // Bytes every candidate shares need no histogram pass: start the radix at
+    // the first byte where the keys differ (importance values of one order of
+    // magnitude share their sign/exponent byte).
+    uint64_t kand = ~0ull, kor = 0;
+    for (int i = tid; i < nc; i += NT) {
+        kand &= keys[i];
+        kor |= keys[i];
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        kand &= __shfl_xor_sync(0xffffffffu, kand, off);
+        kor |= __shfl_xor_sync(0xffffffffu, kor, off);
+    }
+    if (lane == 0) {
+        s.warp_and[warp] = kand;
+        s.warp_or[warp] = kor;
+    }
+    named_sync(BAR, NT);
+    kand = ~0ull;
+    kor = 0;
+    for (int w = 0; w < NT / 32; ++w) {
+        kand &= s.warp_and[w];
+        kor |= s.warp_or[w];
+    }
+    const uint64_t diff = kand ^ kor;  // bits that vary among the candidates
+    int top = 56;
     uint64_t prefix = 0, mask = 0;
+    while (top > 0 && ((diff >> top) & 0xFFull) == 0) {
+        mask |= 0xFFull << top;
+        top -= 8;
+    }
+    prefix = kand & mask;
     int remaining = k;
-    for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int shift = top; shift >= 0; shift -= 8) {
         for (int i = tid; i < 256; i += NT) s.hist[i] = 0;
         named_sync(BAR, NT);
-        for (int i = tid; i < nc; i += NT) {
-            const uint64_t key = keys[i];
-            if ((key & mask) == prefix) atomicAdd(&s.hist[(key >> shift) & 255u], 1u);
+        // warp-aggregated histogram: lanes with the same digit add once, so
+        // a crowded bin costs one shared atomic per warp, not one per lane
+        for (int i0 = tid - lane; i0 < nc; i0 += NT) {
+            const int i = i0 + lane;
+            const uint64_t key = i < nc ? keys[i] : 0;
+            const bool take = i < nc && (key & mask) == prefix;
+            const unsigned bin = take ? static_cast<unsigned>((key >> shift) & 255u) : 256u + lane;
+            const unsigned peers = __match_any_sync(0xffffffffu, bin);
+            if (take && lane == __ffs(peers) - 1) atomicAdd(&s.hist[bin], static_cast<unsigned>(__popc(peers)));
         }
         named_sync(BAR, NT);
         if (warp == 0) {

@@ -294,29 +294,34 @@ def test_decode_variants_and_sparsity(api, port, variant, stride):
             assert abs(sp[b] - want_sp) <= 1.0 / n + 1e-12, (variant, j, sp[b], want_sp)
 
 
-def test_decode_multilayer_step(api):
+@pytest.mark.parametrize("s", [100, 2700])
+def test_decode_multilayer_step(api, s):
     """skv_swa_decode_step over L layers == per-layer calls; host-buffer
-    variant == device variant."""
+    variant == device variant. s=2700 has n-k > 2048 candidates: the select
+    leaves the attend tail and the step batches the layers' selects in one
+    launch after the attends."""
     rng = np.random.default_rng(8)
-    L, B, H, D, s = 3, 4, 8, 128, 100
+    L, B, H, D = 3, 4, 8, 128
     kv = torch.from_numpy(rng.standard_normal((L, B, s, 2, H, D))).half().cuda()
     q, kn, vn = (torch.from_numpy(rng.standard_normal((L, B, H, D))).half().cuda() for _ in range(3))
-    caches = [api.SwaCache(L, B, H, D, s + 2, kv_dtype="f16") for _ in range(3)]
+    caches = [api.SwaCache(L, B, H, D, s + 3, kv_dtype="f16") for _ in range(3)]
     for c in caches:
         for l in range(L):
             c.append_tokens(l, 0, 0, kv[l, :, :, 0].contiguous(), kv[l, :, :, 1].contiguous())
             c.prefill_seed(l, s, q[l])
-    n = s + 1
-    a = caches[0].swa_decode_step(n, 0.2, q, kn, vn)
-    b = torch.stack([caches[1].swa_decode_layer(l, n, 0.2, q[l].contiguous(), kn[l].contiguous(),
-                                                vn[l].contiguous())[0] for l in range(L)])
     outh = torch.empty_like(q, device="cpu").pin_memory()
-    caches[2].swa_decode_step_host(n, 0.2, q.cpu().pin_memory(), kn.cpu().pin_memory(), vn.cpu().pin_memory(), outh)
-    torch.cuda.synchronize()
-    assert torch.equal(a, b)
-    assert torch.equal(a.cpu(), outh)
-    for l in range(L):
-        assert torch.equal(caches[0].importance(l, n), caches[1].importance(l, n))
+    for n in (s + 1, s + 2):  # the second step uses the selection the first one made
+        a = caches[0].swa_decode_step(n, 0.2, q, kn, vn)
+        b = torch.stack([caches[1].swa_decode_layer(l, n, 0.2, q[l].contiguous(), kn[l].contiguous(),
+                                                    vn[l].contiguous())[0] for l in range(L)])
+        caches[2].swa_decode_step_host(n, 0.2, q.cpu().pin_memory(), kn.cpu().pin_memory(), vn.cpu().pin_memory(),
+                                       outh)
+        torch.cuda.synchronize()
+        assert torch.equal(a, b)
+        assert torch.equal(a.cpu(), outh)
+        for l in range(L):
+            assert torch.equal(caches[0].importance(l, n), caches[1].importance(l, n))
+            assert torch.equal(caches[0].importance(l, n), caches[2].importance(l, n))
 
 
 def test_decode_step_host_pipelined(api):
