@@ -21,6 +21,8 @@
 // the ring keeps HBM busy across the softmax in between.
 #pragma once
 
+#include <type_traits>
+
 #include "skv_device.cuh"
 #include "skv_select.cuh"
 
@@ -312,10 +314,19 @@ __global__ void __launch_bounds__(kDecodeThreads)
     const int h = slot % HG;
     const int c = lane % LR;
     float2 q2[V2];
+    // INT8 codes against an fp16 query: the logit dot runs on FHFMA over the
+    // packed query halves (dot_u8_f16)
+    constexpr bool kFh = QUANT && std::is_same<QT, __half>::value;
+    uint32_t qh[kFh ? 8 : 1];
     {
         const QT* qrow = static_cast<const QT*>(p.q) + (static_cast<size_t>(b) * H + g * HG + h) * D + c * VE;
 #pragma unroll
         for (int i = 0; i < V2; ++i) q2[i] = make_float2(to_f(qrow[2 * i]), to_f(qrow[2 * i + 1]));
+        if constexpr (kFh) {
+            const uint4 a = reinterpret_cast<const uint4*>(qrow)[0], bq = reinterpret_cast<const uint4*>(qrow)[1];
+            qh[0] = a.x, qh[1] = a.y, qh[2] = a.z, qh[3] = a.w;
+            qh[4] = bq.x, qh[5] = bq.y, qh[6] = bq.z, qh[7] = bq.w;
+        }
     }
     float qsum = 0.f;
     if constexpr (QUANT) {
@@ -350,12 +361,16 @@ __global__ void __launch_bounds__(kDecodeThreads)
         float part[RS];
 #pragma unroll
         for (int i = 0; i < RS; ++i) {
-            float2 kf[V2];
-            cvt16x2(raw[i], kf, KV{});
-            float2 a = __fmul2_rn(q2[0], kf[0]);
+            if constexpr (kFh) {
+                part[i] = dot_u8_f16(raw[i], qh);  // biased codes, like cvt16x2 (KvU8)
+            } else {
+                float2 kf[V2];
+                cvt16x2(raw[i], kf, KV{});
+                float2 a = __fmul2_rn(q2[0], kf[0]);
 #pragma unroll
-            for (int j = 1; j < V2; ++j) a = __ffma2_rn(q2[j], kf[j], a);
-            part[i] = a.x + a.y;
+                for (int j = 1; j < V2; ++j) a = __ffma2_rn(q2[j], kf[j], a);
+                part[i] = a.x + a.y;
+            }
         }
         int rsel;
         const float dot = reduce_rows<RS, LR>(part, c, rsel);
@@ -365,7 +380,8 @@ __global__ void __launch_bounds__(kDecodeThreads)
             float logit;
             if constexpr (QUANT) {
                 const float2 ms = *reinterpret_cast<const float2*>(ring + stage * STAGEB + r * ROWE + D);
-                logit = fmaf(ms.x, dot, ms.y * qsum) * scale;
+                // codes arrive as 1024 + c (cvt16x2, KvU8): dot = q.c + 1024 * sum(q)
+                logit = fmaf(ms.x, dot, fmaf(-kBiasU8, ms.x, ms.y) * qsum) * scale;
             } else {
                 logit = dot * scale;
             }
@@ -440,7 +456,7 @@ __global__ void __launch_bounds__(kDecodeThreads)
                     const float2 a2 = make_float2(a, a);
 #pragma unroll
                     for (int j = 0; j < V2; ++j) acc[j] = __ffma2_rn(a2, vf[j], acc[j]);
-                    bsum = fmaf(w, ms.y, bsum);
+                    bsum = fmaf(w, fmaf(-kBiasU8, ms.x, ms.y), bsum);  // biased codes
                 } else {
                     const float2 w2 = make_float2(w, w);
 #pragma unroll
@@ -461,7 +477,7 @@ __global__ void __launch_bounds__(kDecodeThreads)
                         const float2 a2 = make_float2(a, a);
 #pragma unroll
                         for (int j = 0; j < V2; ++j) acc[j] = __ffma2_rn(a2, vf[j], acc[j]);
-                        bsum = fmaf(w, ms.y, bsum);
+                        bsum = fmaf(w, fmaf(-kBiasU8, ms.x, ms.y), bsum);  // biased codes
                     } else {
                         const float2 w2 = make_float2(w, w);
 #pragma unroll
