@@ -2,6 +2,8 @@
 // reference's error semantics, the device cache object, kernel selection and
 // launch, host-buffer step, and the measurement hooks used by bench.py.
 #include <algorithm>
+#include <mutex>
+#include <map>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -157,6 +159,8 @@ struct skv_cache {
     int64_t attend_launches = 0;
     uint64_t algo_bytes = 0;
     int last_hg = 0, last_grid = 0, last_occ = 0;
+    const void* attr_func = nullptr;  // attend kernel whose smem attribute was last set
+    size_t attr_smem = 0;
     size_t last_smem = 0;
 };
 
@@ -399,11 +403,35 @@ skv_status pick_attend(skv_cache* c, int m, const DecodeLaunch** dl_out, size_t*
     if (!chosen)
         return fail(SKV_ERR_UNSUPPORTED, "no attend kernel fits (heads %d, m %d, shared memory %d)", c->d.heads, m,
                     c->max_smem);
-    SKV_CUDA(cudaFuncSetAttribute(chosen->func, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(chosen_smem)));
-    int occ = 0;
-    SKV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chosen->func, skvd::kDecodeThreads, chosen_smem));
-    c->last_occ = occ;
+    // The attribute costs host time on every launch: it is set per function
+    // (all caches share it) and only ever grows, which keeps concurrent
+    // callers safe; the occupancy (reported, not used) is recomputed when this
+    // cache's launch size changes.
+    {
+        static std::mutex mu;
+        static std::map<const void*, size_t> set_smem;
+        std::lock_guard<std::mutex> lock(mu);
+        size_t& cur = set_smem[chosen->func];
+        if (chosen_smem > cur) {
+            SKV_CUDA(cudaFuncSetAttribute(chosen->func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(chosen_smem)));
+            cur = chosen_smem;
+        }
+    }
+    if (c->attr_func != chosen->func || c->attr_smem != chosen_smem) {
+        cudaFuncAttributes fa{};
+        SKV_CUDA(cudaFuncGetAttributes(&fa, chosen->func));
+        int smem_sm = 0, reserved = 0;
+        SKV_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, c->d.device));
+        SKV_CUDA(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, c->d.device));
+        const size_t per = chosen_smem + fa.sharedSizeBytes + static_cast<size_t>(reserved);
+        int occ = static_cast<int>(static_cast<size_t>(smem_sm) / per);
+        occ = std::min(occ, 2048 / skvd::kDecodeThreads);
+        if (fa.numRegs > 0) occ = std::min(occ, 65536 / (fa.numRegs * skvd::kDecodeThreads));
+        c->last_occ = occ;
+        c->attr_func = chosen->func;
+        c->attr_smem = chosen_smem;
+    }
     *dl_out = chosen;
     *smem_out = chosen_smem;
     return SKV_OK;

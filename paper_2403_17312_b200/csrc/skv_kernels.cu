@@ -2,6 +2,7 @@
 // decode kernel: batched swa_select / top_k, fp64 quantize / dequantize,
 // cache writes (append with fake-quant) and reads.
 #include <algorithm>
+#include <mutex>
 
 #include "skv_internal.h"
 #include "skv_select.cuh"
@@ -400,9 +401,18 @@ using namespace skvd;
 cudaError_t launch_select(const SelectParams& p, int batch, bool pdl, cudaStream_t st, int layers) {
     const int nc = (p.select && !p.dense) ? p.n - p.k : 0;
     const size_t smem = select_smem(nc);
-    cudaError_t e = cudaFuncSetAttribute(swa_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
+    static std::mutex mu;  // the attribute only grows: concurrent callers stay safe
+    static size_t set_smem = 0;
+    cudaError_t e = cudaSuccess;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (smem > set_smem) {
+            e = cudaFuncSetAttribute(swa_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+            set_smem = smem;
+        }
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(batch, layers);
     cfg.blockDim = dim3(kSelectThreads);
