@@ -595,6 +595,8 @@ skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok
         // 0.88->0.79), which keep the separate select kernel.
         if (select_key_bytes(sel) > std::min<size_t>(dl->ring_bytes, 2048 * 8)) fused = false;
         if (c->reduce) fused = false;  // the step row is summed across head shards first
+        static const bool no_tail = std::getenv("SKV_NO_TAIL") != nullptr;  // A/B tuning
+        if (no_tail) fused = false;
     }
     const size_t lt = static_cast<size_t>(layer) * c->d.batch * c->d.capacity;
     skvd::AttendParams p{};

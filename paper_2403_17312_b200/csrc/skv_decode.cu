@@ -64,9 +64,7 @@ const DecodeLaunch* find_decode(int kv_dtype, int q_dtype, int hg) {
 
 cudaError_t launch_attend(const DecodeLaunch& dl, const AttendParams& p, int grid_g, size_t smem, bool pdl,
                           cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(dl.func, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
+    // the dynamic-smem attribute was raised by pick_attend (skv_capi.cu)
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid_g, p.B);
     cfg.blockDim = dim3(kDecodeThreads);
@@ -78,7 +76,7 @@ cudaError_t launch_attend(const DecodeLaunch& dl, const AttendParams& p, int gri
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
     void* args[] = {const_cast<AttendParams*>(&p)};
-    e = cudaLaunchKernelExC(&cfg, dl.func, args);
+    const cudaError_t e = cudaLaunchKernelExC(&cfg, dl.func, args);
     count_launch();
     return e;
 }
