@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <mutex>
 
@@ -48,7 +49,8 @@ constexpr int kFThreads = 448;  // warps 0..3 control / epilogue, 4..11 rows, 12
 
 struct FlashParams {
     int s, H, HD;
-    int Z, nqt;       // work items: Z x nqt query tiles
+    int Z, nqt;       // work items: Z x nqt query tiles of (sequence, head) z0 .. z0 + Z - 1
+    int z0;
     int s_pad;        // nqt * 128: row stride of mrow
     float c1;         // log2(e) / sqrt(D): exp(x / sqrt(D)) = exp2(x * c1)
     float* mrow;      // [Z][s_pad] row max of S = Q K^T over the causal keys (pass 1)
@@ -274,7 +276,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
             const uint64_t pol = policy_evict_first();
             int g = 0, n = 0;
             for (int it = first; it < last; ++it, ++n) {
-                const int qt = p.nqt - 1 - it % p.nqt, z = it / p.nqt;
+                const int qt = p.nqt - 1 - it % p.nqt, z = p.z0 + it / p.nqt;
                 const int b = z / p.H, xq = (z % p.H) * 128;
                 const int T = qt + 1;
                 const int qb = n & 1;
@@ -378,7 +380,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
         const uint32_t tl = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
         int g = 0, n = 0;
         for (int it = first; it < last; ++it, ++n) {
-            const int qt = p.nqt - 1 - it % p.nqt, z = it / p.nqt;
+            const int qt = p.nqt - 1 - it % p.nqt, z = p.z0 + it / p.nqt;
             const int T = qt + 1;
             const int r = qt * kFTile + rl;
             const int qb = n & 1;
@@ -498,7 +500,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
         const uint32_t tl = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
         int n = 0;
         for (int it = first; it < last; ++it, ++n) {
-            const int qt = p.nqt - 1 - it % p.nqt, z = it / p.nqt;
+            const int qt = p.nqt - 1 - it % p.nqt, z = p.z0 + it / p.nqt;
             const int r = qt * kFTile + rl;
             const bool valid = r < p.s;
             const int ob = n & 1;
@@ -622,7 +624,10 @@ template <bool BF16, bool STATS>
 cudaError_t run_flash(const CUtensorMap& mq, const CUtensorMap& mkv, const FlashParams& p, cudaStream_t st) {
     constexpr int smem = FlashSmem<BF16, STATS>::kBytes;
     const void* fn = reinterpret_cast<const void*>(&flash_prefill_kernel<BF16, STATS>);
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    static std::once_flag once;  // a constant size: set the attribute once per instantiation
+    static cudaError_t attr = cudaSuccess;
+    std::call_once(once, [&] { attr = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
+    cudaError_t e = attr;
     if (e != cudaSuccess) return e;
     void* args[] = {const_cast<CUtensorMap*>(&mq), const_cast<CUtensorMap*>(&mkv), const_cast<FlashParams*>(&p)};
     int dev = 0, sms = 0;
@@ -635,6 +640,7 @@ cudaError_t run_flash(const CUtensorMap& mq, const CUtensorMap& mkv, const Flash
 }
 
 size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
 
 }  // namespace
 
@@ -678,6 +684,7 @@ cudaError_t launch_prefill(bool bf16, bool out_f32, const void* kv, const void* 
     p.out_f32 = out_f32 ? 1 : 0;
     p.wlast = wlast;
     p.below = below;
+    p.z0 = 0;
     e = bf16 ? run_flash<true, true>(mq, mkv, p, st) : run_flash<false, true>(mq, mkv, p, st);
     if (e != cudaSuccess) return e;
     e = bf16 ? run_flash<true, false>(mq, mkv, p, st) : run_flash<false, false>(mq, mkv, p, st);
