@@ -557,3 +557,9 @@ cudaError_t launch_cache_read(int kv_dtype, const uint8_t* kv, float* out, int H
 }
 
 }  // namespace skv_impl
+
+#ifdef SKV_SELECT_TRACE
+extern "C" int skv_debug_select_trace(long long* out) {
+    return static_cast<int>(cudaMemcpyFromSymbol(out, skvd::g_sel_trace, sizeof(long long) * 16));
+}
+#endif

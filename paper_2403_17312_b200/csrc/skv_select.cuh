@@ -66,10 +66,38 @@ struct SelectScratch {
 // threads synchronised on named barrier BAR, sequence b. keys: shared memory
 // for n-k order keys. Weight partials are read through L2 (__ldcg): in the
 // attend tail they come from sibling CTAs of the same grid.
+// Stage importance[0, nc) into shared memory as fp64, several loads in
+// flight per thread.
+template <int NT>
+__device__ __forceinline__ void stage_candidates(double* kd, const double* imp, int nc, int tid) {
+    int i = tid;
+    for (; i + 3 * NT < nc; i += 4 * NT) {
+        const double a = imp[i], b = imp[i + NT], c = imp[i + 2 * NT], d = imp[i + 3 * NT];
+        kd[i] = a;
+        kd[i + NT] = b;
+        kd[i + 2 * NT] = c;
+        kd[i + 3 * NT] = d;
+    }
+    for (; i < nc; i += NT) kd[i] = imp[i];
+}
+
+#ifdef SKV_SELECT_TRACE
+#define SEL_TRACE(i) \
+    if (tid == 0 && b == 0) g_sel_trace[i] = clock64();
+#else
+#define SEL_TRACE(i)
+#endif
+
 template <int NT, int BAR>
 __device__ void fold_and_select(const SelectParams& p, int b, int tid, TopkSmem<NT>& s, uint64_t* keys,
                                 SelectScratch<NT>& sc) {
     double* imp = p.imp + static_cast<size_t>(b) * p.imp_ld;
+    // top-k candidates [0, nc): staged as fp64 in the key buffer, keyed in place
+    const bool topk = p.select && !p.dense && p.variant != 2 && p.variant != 3;
+    const int nc = topk ? p.n - p.k : 0;
+    double* kd = reinterpret_cast<double*>(keys);
+    SEL_TRACE(0);
+    constexpr int R = 4;  // folded positions per thread held in registers (fast path)
     if (p.apply) {
         const float* wp = p.wpart + static_cast<size_t>(b) * p.G * p.m_prev;
         const int* tp = p.tok_prev ? p.tok_prev + static_cast<size_t>(b) * p.tok_prev_ld : nullptr;
@@ -86,12 +114,46 @@ __device__ void fold_and_select(const SelectParams& p, int b, int tid, TopkSmem<
             for (int pos = tid; pos < p.m_prev; pos += NT) wo[pos] = row(pos);
             return;
         }
+        const bool assign_all = p.apply == 2;
         double vmax = 0.0;
-        for (int pos = tid; pos < p.m_prev; pos += NT) {
-            const double v = row(pos);
-            const int t = tp ? tp[pos] : pos;
-            imp[t] = (p.apply == 2 || t == p.cur_tok) ? v : imp[t] + v;
-            vmax = v > vmax ? v : vmax;
+        double v[R];
+        if (p.m_prev <= R * NT) {
+            // Fast path: every global load of the fold (weight partials, old
+            // importance of the folded tokens) and the candidate staging is
+            // issued before the first barrier -- one memory round trip.
+            int t[R];
+            double old[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int pos = tid + r * NT;
+                v[r] = 0.0;
+                t[r] = -1;
+                old[r] = 0.0;
+                if (pos < p.m_prev) {
+                    t[r] = tp ? tp[pos] : pos;
+                    v[r] = row(pos);
+                    if (!assign_all && t[r] != p.cur_tok) old[r] = imp[t[r]];
+                }
+            }
+            stage_candidates<NT>(kd, imp, nc, tid);
+            named_sync(BAR, NT);  // staged candidates complete; every old value read
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if (t[r] < 0) continue;
+                const double nv = (assign_all || t[r] == p.cur_tok) ? v[r] : old[r] + v[r];
+                imp[t[r]] = nv;
+                if (t[r] < nc) kd[t[r]] = nv;
+                vmax = v[r] > vmax ? v[r] : vmax;
+            }
+        } else {
+            for (int pos = tid; pos < p.m_prev; pos += NT) {
+                const double w = row(pos);
+                const int t = tp ? tp[pos] : pos;
+                imp[t] = (assign_all || t == p.cur_tok) ? w : imp[t] + w;
+                vmax = w > vmax ? w : vmax;
+            }
+            named_sync(BAR, NT);  // the folded importance is visible to the staging
+            stage_candidates<NT>(kd, imp, nc, tid);
         }
         if (p.sp_n > 0) {
             // attention_sparsity (attention.hpp:275-310) of the head-summed step
@@ -108,7 +170,12 @@ __device__ void fold_and_select(const SelectParams& p, int b, int tid, TopkSmem<
             for (int w = 0; w < NT / 32; ++w) mx = sc.red_max[w] > mx ? sc.red_max[w] : mx;
             const double thr = 0.01 * mx;
             int below = 0;
-            for (int pos = tid; pos < p.m_prev; pos += NT) below += row(pos) < thr;
+            if (p.m_prev <= R * NT) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) below += (tid + r * NT < p.m_prev) && v[r] < thr;
+            } else {
+                for (int pos = tid; pos < p.m_prev; pos += NT) below += row(pos) < thr;
+            }
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) below += __shfl_xor_sync(0xffffffffu, below, off);
             if (lane == 0) sc.red_cnt[warp] = below;
@@ -120,9 +187,11 @@ __device__ void fold_and_select(const SelectParams& p, int b, int tid, TopkSmem<
                 p.sparsity[b] = static_cast<double>(sparse) / static_cast<double>(p.sp_n);
             }
         }
+    } else {
+        stage_candidates<NT>(kd, imp, nc, tid);
     }
     if (!p.select) return;
-    named_sync(BAR, NT);  // the folded importance (this thread block's writes) is visible
+    named_sync(BAR, NT);  // the fold and the staged candidates are complete
     int* o = p.idx + static_cast<size_t>(b) * p.idx_ld;
     if (p.variant == 2) {  // local_attention_mask (attention.hpp:247-256): the last m tokens
         for (int i = tid; i < p.m; i += NT) o[i] = p.n - p.m + i;
@@ -137,10 +206,12 @@ __device__ void fold_and_select(const SelectParams& p, int b, int tid, TopkSmem<
         for (int i = tid; i < p.m; i += NT) o[i] = i;
         return;
     }
-    const int nc = p.n - p.k;
-    for (int i = tid; i < nc; i += NT) keys[i] = order_key(imp[i]);
+    SEL_TRACE(1);
+    for (int i = tid; i < nc; i += NT) keys[i] = order_key(kd[i]);  // in place, same thread
     named_sync(BAR, NT);
+    SEL_TRACE(2);
     block_topk<NT, BAR>(keys, nc, p.k, o, s, tid);                  // global picks, ascending
+    SEL_TRACE(3);
     for (int i = tid; i < p.k; i += NT) o[p.k + i] = p.n - p.k + i;  // local window
 }
 

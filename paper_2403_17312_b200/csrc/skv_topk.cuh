@@ -12,6 +12,10 @@
 
 namespace skvd {
 
+#ifdef SKV_SELECT_TRACE  // phase timestamps of sequence 0 (debug builds only)
+__device__ long long g_sel_trace[16];
+#endif
+
 template <int NT>
 struct TopkSmem {
     uint32_t hist[256];
@@ -73,11 +77,17 @@ __device__ void block_topk(const uint64_t* keys, int nc, int k, int* out, TopkSm
     }
     prefix = kand & mask;
     int remaining = k;
+#ifdef SKV_SELECT_TRACE
+    int npass = 0;
+#endif
     for (int shift = top; shift >= 0; shift -= 8) {
+#ifdef SKV_SELECT_TRACE
+        ++npass;
+#endif
         for (int i = tid; i < 256; i += NT) s.hist[i] = 0;
         named_sync(BAR, NT);
-        // warp-aggregated histogram: lanes with the same digit add once, so
-        // a crowded bin costs one shared atomic per warp, not one per lane
+#ifdef SKV_TOPK_MATCH
+        // warp-aggregated histogram: lanes with the same digit add once
         for (int i0 = tid - lane; i0 < nc; i0 += NT) {
             const int i = i0 + lane;
             const uint64_t key = i < nc ? keys[i] : 0;
@@ -86,6 +96,25 @@ __device__ void block_topk(const uint64_t* keys, int nc, int k, int* out, TopkSm
             const unsigned peers = __match_any_sync(0xffffffffu, bin);
             if (take && lane == __ffs(peers) - 1) atomicAdd(&s.hist[bin], static_cast<unsigned>(__popc(peers)));
         }
+#else
+        // Plain shared atomics, four keys in flight per thread. (Below the
+        // common prefix the digits are spread, so same-bin conflicts are rare;
+        // __match_any_sync aggregation measured ~2x slower per pass.)
+        {
+            int i = tid;
+            for (; i + 3 * NT < nc; i += 4 * NT) {
+                const uint64_t k0 = keys[i], k1 = keys[i + NT], k2 = keys[i + 2 * NT], k3 = keys[i + 3 * NT];
+                if ((k0 & mask) == prefix) atomicAdd(&s.hist[(k0 >> shift) & 255u], 1u);
+                if ((k1 & mask) == prefix) atomicAdd(&s.hist[(k1 >> shift) & 255u], 1u);
+                if ((k2 & mask) == prefix) atomicAdd(&s.hist[(k2 >> shift) & 255u], 1u);
+                if ((k3 & mask) == prefix) atomicAdd(&s.hist[(k3 >> shift) & 255u], 1u);
+            }
+            for (; i < nc; i += NT) {
+                const uint64_t key = keys[i];
+                if ((key & mask) == prefix) atomicAdd(&s.hist[(key >> shift) & 255u], 1u);
+            }
+        }
+#endif
         named_sync(BAR, NT);
         if (warp == 0) {
             // lane l owns bins 255-8l .. 255-8l-7 (descending).
@@ -131,6 +160,9 @@ __device__ void block_topk(const uint64_t* keys, int nc, int k, int* out, TopkSm
         remaining = s.remaining;
         if (s.done) break;
     }
+#ifdef SKV_SELECT_TRACE
+    if (tid == 0 && blockIdx.x == 0) { g_sel_trace[8] = npass; g_sel_trace[9] = top; g_sel_trace[10] = clock64(); }
+#endif
     // Order-preserving compaction. Element i is selected iff its masked key
     // is above the threshold prefix, or equal to it and among the first
     // `remaining` such elements by index.
