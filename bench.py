@@ -328,6 +328,10 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks: several ranks on one GPU need gloo and a shared device
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    if "BENCH_DEVICE" in os.environ:
+        local = int(os.environ["BENCH_DEVICE"])
 
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
@@ -346,7 +350,10 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     from paper_2403_17312_b200 import api
     from paper_2403_17312_b200.shard import dist_reducer, head_shard_range, max_over_ranks, shard_range
