@@ -230,6 +230,7 @@ def run_config5(args, cfg, rank: int, world: int):
     import torch
 
     from paper_2403_17312_b200 import api
+    from paper_2403_17312_b200.shard import max_over_ranks
 
     L, B, H, s = cfg["L"], cfg["B"], cfg["H"], cfg["s"]
     h = H * D
@@ -277,6 +278,8 @@ def run_config5(args, cfg, rank: int, world: int):
             n += 1
             cache.swa_decode_step(n, RATIO, qin[i % 4], knew[i], vnew[i], out)
         torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         moved = recomputed = 0
         e0.record()
@@ -285,7 +288,7 @@ def run_config5(args, cfg, rank: int, world: int):
             cache.swa_decode_step(n, RATIO, qin[i % 4], knew[i], vnew[i], out)
         e1.record()
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
+        ms = max_over_ranks(e0.elapsed_time(e1), device="cuda")  # the slowest rank
         if phase > 1:
             acts = [cache.last_actions(l) for l in range(L)]
             moved = sum(len(a["offload"]) + len(a["reload"]) for al in acts for a in al)
@@ -336,13 +339,6 @@ def main():
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return
-    if args.config == 5:
-        import torch
-
-        torch.cuda.set_device(local)
-        run_config5(args, cfg, rank, world)
-        return
-
     import torch
 
     torch.cuda.set_device(local)
@@ -354,6 +350,11 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+    if args.config == 5:
+        run_config5(args, cfg, rank, world)
+        if dist:
+            dist.destroy_process_group()
+        return
 
     from paper_2403_17312_b200 import api
     from paper_2403_17312_b200.shard import dist_reducer, head_shard_range, max_over_ranks, shard_range
