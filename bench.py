@@ -524,7 +524,7 @@ def main():
         per = L * B * H * D * qh.element_size()
         e2e = {"value": seqs * e2e_steps / (e2e_ms / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": 3 * per, "d2h_bytes_per_step": per,
-               "path": "skv_swa_decode_step_host (pinned host q/k/v in, out back; 4 layer chunks pipelined over h2d/d2h copy streams)"}
+               "path": "skv_swa_decode_step_host (pinned host q/k/v in, out back; 2 layer chunks pipelined over h2d/d2h copy streams)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_only:
