@@ -268,6 +268,12 @@ skv_status skv_gemm_tn(const void* A, const void* Bt, float* C, int M, int N, in
 skv_status skv_device_alloc(int device, size_t bytes, void** out);
 skv_status skv_device_free(void* ptr);
 skv_status skv_copy(void* dst, const void* src, size_t bytes, void* stream);
+/* Pinned (page-locked, device-mapped) host memory for the *_host entry
+ * points, whose copies overlap compute only from pinned buffers; and a
+ * stream synchronisation for hosts without the CUDA runtime. */
+skv_status skv_host_alloc(size_t bytes, void** out);
+skv_status skv_host_free(void* ptr);
+skv_status skv_stream_synchronize(void* stream);
 
 /* ---- measurement hooks (bench.py) ----------------------------------------
  * While enabled, every decode-kernel launch on a cache is bracketed by CUDA

@@ -101,6 +101,9 @@ def _declare(lib):
         "skv_device_alloc": (I, [I, SZ, P]),
         "skv_device_free": (I, [P]),
         "skv_copy": (I, [P, P, SZ, P]),
+        "skv_host_alloc": (I, [SZ, P]),
+        "skv_host_free": (I, [P]),
+        "skv_stream_synchronize": (I, [P]),
         "skv_profile_enable": (I, [P, I]),
         "skv_profile_read": (I, [P, P, P, P]),
         "skv_profile_attend_chain": (I, [P, I, D, P, P, P, P, I, P, P]),

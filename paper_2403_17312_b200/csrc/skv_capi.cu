@@ -1341,6 +1341,28 @@ skv_status skv_copy(void* dst, const void* src, size_t bytes, void* stream) {
     return SKV_OK;
 }
 
+skv_status skv_host_alloc(size_t bytes, void** out) {
+    SKV_REQUIRE(out != nullptr, "skv_host_alloc: null output");
+    *out = nullptr;
+    if (bytes == 0) return SKV_OK;
+    if (cudaHostAlloc(out, bytes, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
+        cudaGetLastError();
+        *out = nullptr;
+        return fail(SKV_ERR_OOM, "skv_host_alloc: cannot pin %zu bytes", bytes);
+    }
+    return SKV_OK;
+}
+
+skv_status skv_host_free(void* ptr) {
+    if (ptr) SKV_CUDA(cudaFreeHost(ptr));
+    return SKV_OK;
+}
+
+skv_status skv_stream_synchronize(void* stream) {
+    SKV_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    return SKV_OK;
+}
+
 skv_status skv_profile_enable(skv_cache* c, int enable) {
     SKV_REQUIRE(c != nullptr, "null cache");
     DeviceGuard guard(c->d.device);

@@ -5,7 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2403_17312_b200 import api
 
 L, B, H, D, s = 32, 64, 32, 128, int(os.environ.get("PS", 512))
-c = api.SwaCache(L, B, H, D, s + 64, kv_dtype="f16")
+c = api.SwaCache(L, B, H, D, s + 160, kv_dtype="f16")
 g = torch.Generator(device="cuda").manual_seed(0)
 for l in range(L):
     k = torch.randn(B, s, H, D, device="cuda", generator=g).half()
@@ -42,3 +42,18 @@ e1.record(); torch.cuda.synchronize()
 dms = e0.elapsed_time(e1) / 30
 print(f"chunks={os.environ.get('SKV_HOST_CHUNKS', 'default')}: e2e {ms:.3f} ms/step ({B/ms*1e3:.0f} tok/s)  "
       f"copies-only {cms:.3f} ms  device-only {dms:.3f} ms")
+# host enqueue cost per call (no synchronisation): if it approaches the
+# step time the GPU waits on the host
+import time
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(30):
+    n += 1; c.swa_decode_step(n, 0.2, qd, kd, vd, od)
+t1 = time.perf_counter()
+torch.cuda.synchronize()
+t2 = time.perf_counter()
+for _ in range(30):
+    n += 1; c.swa_decode_step_host(n, 0.2, qh, kh, vh, oh)
+t3 = time.perf_counter()
+torch.cuda.synchronize()
+print(f"host enqueue per call: device step {(t1 - t0) / 30 * 1e3:.3f} ms, host-buffer step {(t3 - t2) / 30 * 1e3:.3f} ms")

@@ -20,3 +20,24 @@ def test_cpp_dropin_matches_reference():
             pytest.skip("reference headers absent and no prebuilt tests/cpp/build/test_shim")
     r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ALL OK" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_cpp_host_decode_loop():
+    """A C++ host (tests/cpp/decode_loop.cpp) runs the device-resident decode
+    through include/skv/b200.hpp with pinned host buffers -- no Python on the
+    path -- and its host-buffer steps agree bit for bit with the device-buffer
+    steps of a twin cache (outputs and importance)."""
+    import json
+
+    exe = os.path.join(HERE, "cpp", "build", "decode_loop")
+    if not os.path.exists(exe):
+        if os.path.isdir("/root/reference/proj/include"):
+            subprocess.run(["make", "-s", "-C", os.path.join(HERE, "cpp")], check=True)
+        else:
+            pytest.skip("reference headers absent and no prebuilt tests/cpp/build/decode_loop")
+    r = subprocess.run([exe, "4", "64", "32", "512", "12"], capture_output=True, text=True, timeout=600)
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert line["mismatched_steps"] == 0 and line["mismatched_layers"] == 0, line
+    assert line["e2e_tokens_per_s"] > 0
