@@ -49,8 +49,7 @@ constexpr int kFThreads = 448;  // warps 0..3 control / epilogue, 4..11 rows, 12
 
 struct FlashParams {
     int s, H, HD;
-    int Z, nqt;       // work items: Z x nqt query tiles of (sequence, head) z0 .. z0 + Z - 1
-    int z0;
+    int Z, nqt;       // work items: Z x nqt query tiles
     int s_pad;        // nqt * 128: row stride of mrow
     float c1;         // log2(e) / sqrt(D): exp(x / sqrt(D)) = exp2(x * c1)
     float* mrow;      // [Z][s_pad] row max of S = Q K^T over the causal keys (pass 1)
@@ -276,7 +275,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
             const uint64_t pol = policy_evict_first();
             int g = 0, n = 0;
             for (int it = first; it < last; ++it, ++n) {
-                const int qt = p.nqt - 1 - it % p.nqt, z = p.z0 + it / p.nqt;
+                const int qt = p.nqt - 1 - it % p.nqt, z = it / p.nqt;
                 const int b = z / p.H, xq = (z % p.H) * 128;
                 const int T = qt + 1;
                 const int qb = n & 1;
@@ -380,7 +379,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
         const uint32_t tl = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
         int g = 0, n = 0;
         for (int it = first; it < last; ++it, ++n) {
-            const int qt = p.nqt - 1 - it % p.nqt, z = p.z0 + it / p.nqt;
+            const int qt = p.nqt - 1 - it % p.nqt, z = it / p.nqt;
             const int T = qt + 1;
             const int r = qt * kFTile + rl;
             const int qb = n & 1;
@@ -500,7 +499,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
         const uint32_t tl = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
         int n = 0;
         for (int it = first; it < last; ++it, ++n) {
-            const int qt = p.nqt - 1 - it % p.nqt, z = p.z0 + it / p.nqt;
+            const int qt = p.nqt - 1 - it % p.nqt, z = it / p.nqt;
             const int r = qt * kFTile + rl;
             const bool valid = r < p.s;
             const int ob = n & 1;
@@ -684,7 +683,6 @@ cudaError_t launch_prefill(bool bf16, bool out_f32, const void* kv, const void* 
     p.out_f32 = out_f32 ? 1 : 0;
     p.wlast = wlast;
     p.below = below;
-    p.z0 = 0;
     e = bf16 ? run_flash<true, true>(mq, mkv, p, st) : run_flash<false, true>(mq, mkv, p, st);
     if (e != cudaSuccess) return e;
     e = bf16 ? run_flash<true, false>(mq, mkv, p, st) : run_flash<false, false>(mq, mkv, p, st);
