@@ -321,6 +321,8 @@ def main():
                     help="attention variant (engine.hpp:531-569); dense = the full-KV decode baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--head-shards", type=int, default=0,
+                    help="batch x head mesh: head shards per batch group (0: all ranks when B < world, else 1)")
     ap.add_argument("--no-centre", action="store_true",
                     help="time the first K decode steps instead of centring them on the config's decode")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no clocks/baseline/e2e)")
@@ -357,19 +359,22 @@ def main():
         return
 
     from paper_2403_17312_b200 import api
-    from paper_2403_17312_b200.shard import dist_reducer, head_shard_range, max_over_ranks, shard_range
+    from paper_2403_17312_b200.shard import dist_reducer, head_groups, head_shard_range, max_over_ranks, mesh_coords
 
     L, B, H, s = cfg["L"], cfg["B"], cfg["H"], cfg["s"]
-    # fewer sequences than GPUs (config 1): shard the heads, one fp64 all-reduce
-    # of the step row per layer-step (strong scaling). Otherwise weak scaling:
-    # every rank owns cfg["B"] sequences of the world*B global batch.
-    head_shard = world > 1 and B < world
+    # batch x head mesh: world = batch groups x head shards. Each batch group
+    # owns cfg["B"] sequences; its head shards split the heads and all-reduce
+    # the fp64 step row once per layer-step. Default: head shards only when
+    # there are fewer sequences than GPUs (config 1: strong scaling), else
+    # pure batch sharding with no collective (weak scaling).
+    head_shards = args.head_shards or (world if B < world else 1)
+    bi, hi, n_bgroups = mesh_coords(world, rank, head_shards)
+    groups = head_groups(world, head_shards) if dist else [None]
+    head_shard = head_shards > 1
+    b0 = bi * B
     if head_shard:
-        b0 = 0
-        h0, H = head_shard_range(cfg["H"], world, rank)
-    else:
-        b0, _ = shard_range(world * cfg["B"], world, rank)
-    seqs = B if head_shard else world * B  # sequences decoded by the whole job per step
+        h0, H = head_shard_range(cfg["H"], head_shards, hi)
+    seqs = n_bgroups * B  # sequences decoded by the whole job per step
     W, K = args.warmup, args.steps
     if not args.no_centre:
         W, _ = timed_window(cfg, W, K)
@@ -379,7 +384,7 @@ def main():
     cache = api.SwaCache(L, B, H, D, ncap, kv_dtype=cfg["kv"], q_dtype=cfg["q"], device=local)
     cache.set_variant(args.variant)
     if head_shard:
-        cache.set_head_shard(h0, cfg["H"], dist_reducer())
+        cache.set_head_shard(h0, cfg["H"], dist_reducer(groups[bi]))
 
     sampler = ClockSampler(local) if not args.profile_only else None
     if sampler:
@@ -541,7 +546,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
             "warmup_requested": args.warmup,
             "ms_per_step": elapsed_ms / K, "higher_is_better": True,
-            "scaling": "strong" if head_shard else "weak",
+            "scaling": "strong" if (head_shard and n_bgroups == 1) else "weak",
             "vs_baseline": None, "dtype": cfg["kv"], "data": "synthetic (torch.randn K/V/q, seeded)",
             "config": {"workload": cfg["name"], "variant": args.variant, "per_gpu_batch": B, "global_batch": seqs, "layers": L,
                        "heads": H, "head_dim": D, "ratio": RATIO, "n_range": [n_first, n_first + K - 1],
@@ -549,8 +554,9 @@ def main():
                                          f"(n = {s + 1}..{s + cfg['decode']}): step cost is linear in n, so the "
                                          "window's mean is the whole decode's; earlier steps are untimed warm-up")
                        if cfg.get("decode") and not args.no_centre else "steady state at the config's KV length",
-                       "parallelism": (f"head-sharded x{world} ({H} of {cfg['H']} heads per GPU; one fp64 "
-                                       "all-reduce of the step row per layer-step over NCCL)") if head_shard
+                       "parallelism": (f"batch x{n_bgroups} x head x{head_shards} ({B} sequences, {H} of {cfg['H']} "
+                                       "heads per GPU; one fp64 all-reduce of the step row per layer-step within "
+                                       "each batch group)") if head_shard
                        else f"batch-sharded x{world} (no collective)", "rank0_batch_offset": b0,
                        "l2": ("inputs larger than L2 (per-step KV gather >> 126 MB)" if args.config != 1 else
                               "config 1 is the latency-bound parity case: its 3.4 MB/step fit in L2")},

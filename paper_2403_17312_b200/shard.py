@@ -59,6 +59,24 @@ def head_shard_range(heads: int, world: int, rank: int) -> tuple[int, int]:
     return shard_range(heads, world, rank)
 
 
+def mesh_coords(world: int, rank: int, head_shards: int) -> tuple[int, int, int]:
+    """batch x head mesh: world = batch_groups * head_shards; rank ->
+    (batch group, head shard, batch groups). The head shards of one batch
+    group are consecutive ranks (one NVSwitch hop either way on a B200 box)."""
+    if head_shards < 1 or world % head_shards:
+        raise ValueError(f"{head_shards} head shards do not divide {world} ranks")
+    return rank // head_shards, rank % head_shards, world // head_shards
+
+
+def head_groups(world: int, head_shards: int):
+    """One process group per batch group over its head shards (every rank
+    must call this, in the same order). Returns the list, index = batch group."""
+    if head_shards == 1:
+        return [None] * world
+    return [dist.new_group(list(range(g * head_shards, (g + 1) * head_shards)))
+            for g in range(world // head_shards)]
+
+
 def dist_reducer(group=None):
     """The head-shard exchange (SwaCache.set_head_shard): one SUM all-reduce
     of the fp64 step row across the process group. NCCL (over NVLink on a

@@ -185,3 +185,13 @@ def test_head_sharded_decode_equals_unsharded(tmp_path, port):
         sel = got["sel"][j]
         assert np.array_equal(sel[sel >= 0], idx), j
         np.testing.assert_allclose(got["out"][j], attn, rtol=1e-12, atol=1e-14)
+
+
+def test_mesh_coords():
+    from paper_2403_17312_b200.shard import mesh_coords
+
+    assert [mesh_coords(8, r, 2) for r in range(8)] == [(r // 2, r % 2, 4) for r in range(8)]
+    assert [mesh_coords(4, r, 4) for r in range(4)] == [(0, r, 1) for r in range(4)]
+    assert mesh_coords(8, 5, 1) == (5, 0, 8)
+    with pytest.raises(ValueError):
+        mesh_coords(8, 0, 3)
