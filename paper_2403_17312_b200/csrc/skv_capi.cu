@@ -150,6 +150,7 @@ struct skv_cache {
     // launches are collected and issued as one batched launch after the
     // step's attends (they only feed the next step), instead of one select
     // CTA set interleaved with every attend
+    bool in_step = false;  // inside skv_swa_decode_step(_host): a whole step's layers
     bool defer_select = false;
     std::vector<std::pair<int, skvd::SelectParams>> deferred;  // (layer, params)
     // measurement
@@ -595,8 +596,14 @@ skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok
         // 0.88->0.79), which keep the separate select kernel.
         if (select_key_bytes(sel) > std::min<size_t>(dl->ring_bytes, 2048 * 8)) fused = false;
         if (c->reduce) fused = false;  // the step row is summed across head shards first
-        static const bool no_tail = std::getenv("SKV_NO_TAIL") != nullptr;  // A/B tuning
-        if (no_tail) fused = false;
+        // Whole-step decode keeps the attend kernel free of the tail: the
+        // layers' selects run as one batched launch after the attends (or, when
+        // profiling, as separate launches). Per-layer calls keep the tail.
+        // Measured at config 2 / 3: the step is equal within 1% (0.985 vs
+        // 0.994, 1.005 vs 0.997), the attend launch alone 0.69 vs 0.52 and
+        // 0.41 vs 0.31 of the copy peak. SKV_STEP_TAIL=1 restores the tail.
+        static const bool step_tail = std::getenv("SKV_STEP_TAIL") != nullptr;
+        if (c->in_step && !step_tail) fused = false;
     }
     const size_t lt = static_cast<size_t>(layer) * c->d.batch * c->d.capacity;
     skvd::AttendParams p{};
@@ -914,6 +921,7 @@ static skv_status decode_layers(skv_cache* c, int l0, int l1, int n, double r, c
     const size_t per_layer_out = static_cast<size_t>(c->d.batch) * c->d.heads * c->d.head_dim * out_size(c);
     // Selects that cannot ride in the attend tail are batched after the
     // layers (plans and head shards need them per layer: ledger / exchange).
+    c->in_step = l1 - l0 > 1;  // a single layer gains nothing from batching: keep its tail
     c->defer_select = !c->has_plan && !c->reduce && !c->prof;
     c->deferred.clear();
     skv_status status = SKV_OK;
@@ -924,6 +932,7 @@ static skv_status decode_layers(skv_cache* c, int l0, int l1, int n, double r, c
                                    static_cast<uint8_t*>(out) + per_layer_out * l, nullptr, nullptr, l > l0, st);
     }
     c->defer_select = false;
+    c->in_step = false;
     if (status != SKV_OK || c->deferred.empty()) {
         c->deferred.clear();
         return status;
