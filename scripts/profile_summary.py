@@ -77,6 +77,13 @@ def main():
                "algorithmic (cold, isolated launch).", "", "| metric | value |", "|---|---|"]
         md += [f"| {k} | {res[k]} |" for k in KEYS if k in res]
         md.append("")
+    rep = g("select_c2.ncu-rep")
+    if os.path.exists(rep):
+        res, name = full(rep)
+        md += [f"## Select, config 2 (`{name.split('(')[0]}`): the step's batched fold + selection "
+               "(grid = sequences x layers)", "", "| metric | value |", "|---|---|"]
+        md += [f"| {k} | {res[k]} |" for k in KEYS if k in res]
+        md.append("")
     rep = g("prefill.ncu-rep")
     if os.path.exists(rep):
         res, name = full(rep)
