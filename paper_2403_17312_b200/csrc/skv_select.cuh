@@ -18,9 +18,10 @@
 namespace skvd {
 
 #ifndef SKV_SELECT_THREADS
-#define SKV_SELECT_THREADS 256
+#define SKV_SELECT_THREADS 128
 #endif
-// standalone select width (256 measured best: it must fit beside attend CTAs)
+// standalone / batched select width: 128 measured best for the batched per-step launch
+// (sequences x layers CTAs: more resident per SM; 64 / 256 / 512 were slower overall)
 constexpr int kSelectThreads = SKV_SELECT_THREADS;
 
 struct SelectParams {
