@@ -146,6 +146,7 @@ struct skv_cache {
     void* reduce_user = nullptr;
     int head_offset = 0, total_heads = 0;
     double* xbuf = nullptr;  // [B][Ncap] step rows / prefill seed rows, then [B] prefill sparsity
+    uint64_t* gkeys = nullptr;  // [L][B][Ncap] top-k keys of long contexts (lazily)
     // whole-step decode with separate select kernels: the layers' fold+select
     // launches are collected and issued as one batched launch after the
     // step's attends (they only feed the next step), instead of one select
@@ -290,6 +291,7 @@ skv_status skv_cache_destroy(skv_cache* c) {
     cudaFree(c->rec_m);
     cudaFree(c->stage);
     cudaFree(c->xbuf);
+    cudaFree(c->gkeys);
     for (auto* v : {&c->ev_in, &c->ev_comp, &c->ev_out})
         for (cudaEvent_t e : *v) cudaEventDestroy(e);
     if (c->h2d) cudaStreamDestroy(c->h2d);
@@ -522,8 +524,19 @@ skv_status make_select_params(skv_cache* c, int layer, int apply, const int* tok
     if (n_next > 0 && n_next <= c->d.capacity) {
         StepShape s;
         if (skv_status e = step_shape(c, n_next, r_next, &s)) return e;
-        if (!s.dense && static_cast<size_t>(n_next - s.k) * 8 + 8192 > static_cast<size_t>(c->max_smem))
-            return fail(SKV_ERR_UNSUPPORTED, "swa_select: %d candidates exceed shared memory", n_next - s.k);
+        if (!s.dense && c->variant != SKV_VARIANT_LOCAL && c->variant != SKV_VARIANT_STRIDED &&
+            static_cast<size_t>(n_next - s.k) * 8 + 8192 > static_cast<size_t>(c->max_smem)) {
+            // long context: the candidates' keys go to global scratch shaped like the importance
+            if (!c->gkeys) {
+                const size_t bytes = static_cast<size_t>(c->d.layers) * c->d.batch * c->d.capacity * 8;
+                if (cudaMalloc(reinterpret_cast<void**>(&c->gkeys), bytes) != cudaSuccess) {
+                    cudaGetLastError();
+                    return fail(SKV_ERR_OOM, "swa_select: cannot allocate %zu bytes of key scratch", bytes);
+                }
+                c->device_bytes += bytes;
+            }
+            p.gkeys = c->gkeys + static_cast<size_t>(layer) * c->d.batch * c->d.capacity;
+        }
         p.select = 1;
         p.n = n_next;
         p.k = s.k;

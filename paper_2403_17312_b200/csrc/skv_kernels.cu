@@ -224,12 +224,13 @@ __global__ void __launch_bounds__(kSelectThreads) swa_select_kernel(const Select
     __shared__ SelectScratch<kSelectThreads> scratch;
     pdl_launch_dependents();
     if (p.pdl_wait) pdl_wait();
-    if (blockIdx.y == 0) {
+    const long long y = blockIdx.y;
+    if (p.gkeys) keys = p.gkeys + (y * p.ls_imp + static_cast<long long>(blockIdx.x) * p.imp_ld);
+    if (y == 0) {
         fold_and_select<kSelectThreads, 1>(p, blockIdx.x, threadIdx.x, s, keys, scratch);
         return;
     }
     SelectParams q = p;  // layer blockIdx.y of a batched launch
-    const long long y = blockIdx.y;
     q.imp += y * p.ls_imp;
     q.wpart += y * p.ls_wpart;
     q.idx += y * p.ls_idx;
@@ -399,7 +400,7 @@ namespace skv_impl {
 using namespace skvd;
 
 cudaError_t launch_select(const SelectParams& p, int batch, bool pdl, cudaStream_t st, int layers) {
-    const int nc = (p.select && !p.dense) ? p.n - p.k : 0;
+    const int nc = (p.select && !p.dense && !p.gkeys) ? p.n - p.k : 0;
     const size_t smem = select_smem(nc);
     static std::mutex mu;  // the attribute only grows: concurrent callers stay safe
     static size_t set_smem = 0;

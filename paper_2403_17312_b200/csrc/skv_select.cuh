@@ -51,6 +51,9 @@ struct SelectParams {
     // several layers in one launch (blockIdx.y = layer offset): element
     // strides of imp, wpart, idx/tok_prev and sparsity per layer (0: one layer)
     long long ls_imp, ls_wpart, ls_idx, ls_sp;
+    // long contexts: the candidates' keys live in global scratch laid out like
+    // imp ([layers][B][imp_ld], same strides) instead of shared memory
+    uint64_t* gkeys;
 };
 
 __host__ __device__ inline size_t select_smem(int nc) {

@@ -435,3 +435,54 @@ def test_full_size_properties(api, port, shape):
     sel = api.swa_select(cuda(imp), n, 0.2).all.cpu().numpy()
     for b in (0, B // 2 + 1, B - 1):
         assert np.array_equal(sel[b], port.swa_select(imp[b], n, 0.2)[0])
+
+
+def test_long_context_select(api, port):
+    """n - k beyond shared memory (~28k candidates): the top-k keys move to a
+    global scratch buffer. Seeded by the tensor-core prefill (the decode
+    kernel's dense seed keeps all n weights in shared memory), the decode
+    trajectory matches the oracle through the per-layer path, and the
+    whole-step path (batched select over the global keys) matches the
+    per-layer path bit for bit."""
+    D, s, steps, r = 128, 36000, 3, 0.2
+    rng = np.random.default_rng(36000)
+    H = 2
+    kv = round_to(rng.standard_normal((1, s + steps, 2, H, D)), "f16")
+    qp = round_to(rng.standard_normal((1, s, H, D)) * 0.5, "f16")
+    qs = round_to(rng.standard_normal((steps, 1, H, D)) * 1.5, "f16")
+    cache = api.SwaCache(1, 1, H, D, s + steps, kv_dtype="f16")
+    cache.append_tokens(0, 0, 0, cuda(kv[:, :s, 0], torch.float16), cuda(kv[:, :s, 1], torch.float16))
+    cache.prefill_layer(0, cuda(qp, torch.float16))
+    seq = OracleSeq(port, H, D, s + steps)
+    for t in range(s):
+        seq.append(t, kv[0, t, 0], kv[0, t, 1])
+    seq.seed(s, qp[0, s - 1])
+    np.testing.assert_allclose(cache.importance(0, s).cpu().numpy()[0], seq.importance(s), rtol=1e-4, atol=1e-7)
+    for j in range(steps):
+        n = s + j + 1
+        imp_pre = seq.importance(n - 1)
+        out, idx, _ = cache.swa_decode_layer(0, n, r, cuda(qs[j], torch.float16), cuda(kv[:, n - 1, 0], torch.float16),
+                                             cuda(kv[:, n - 1, 1], torch.float16), return_indices=True)
+        seq.append(n - 1, kv[0, n - 1, 0], kv[0, n - 1, 1])
+        attn, _, oidx = seq.step(n, r, qs[j][0])
+        got = idx.cpu().numpy()[0]
+        assert np.array_equal(got, oidx) or selection_flip_is_tie(got, oidx, imp_pre, n, api.swa_window_k(n, r))
+        if np.array_equal(got, oidx):
+            assert_close(out.float().cpu().numpy()[0], attn, TOL["f16"], f"long context step {j}")
+    L, B = 2, 2
+    g = torch.Generator(device="cuda").manual_seed(5)
+    kvt = torch.randn((L, B, s, 2, H, D), generator=g, device="cuda").half()
+    q, kn, vn = (torch.randn((L, B, H, D), generator=g, device="cuda").half() for _ in range(3))
+    caches = [api.SwaCache(L, B, H, D, s + 3, kv_dtype="f16") for _ in range(2)]
+    for c in caches:
+        for l in range(L):
+            c.append_tokens(l, 0, 0, kvt[l, :, :, 0].contiguous(), kvt[l, :, :, 1].contiguous())
+            c.prefill_layer(l, kvt[l, :, :, 0].contiguous())  # any prompt queries: both caches see the same
+    for n in (s + 1, s + 2):
+        a = caches[0].swa_decode_step(n, 0.2, q, kn, vn)
+        b = torch.stack([caches[1].swa_decode_layer(l, n, 0.2, q[l].contiguous(), kn[l].contiguous(),
+                                                    vn[l].contiguous())[0] for l in range(L)])
+        torch.cuda.synchronize()
+        assert torch.equal(a, b)
+        for l in range(L):
+            assert torch.equal(caches[0].importance(l, n), caches[1].importance(l, n))
