@@ -147,6 +147,8 @@ struct skv_cache {
     int head_offset = 0, total_heads = 0;
     double* xbuf = nullptr;  // [B][Ncap] step rows / prefill seed rows, then [B] prefill sparsity
     uint64_t* gkeys = nullptr;  // [L][B][Ncap] top-k keys of long contexts (lazily)
+    int* gtok = nullptr;        // [B][H][Ncap] attend token lists of long selections (lazily)
+    float* gwts = nullptr;      // [B][H][Ncap] their logits / weights
     // whole-step decode with separate select kernels: the layers' fold+select
     // launches are collected and issued as one batched launch after the
     // step's attends (they only feed the next step), instead of one select
@@ -292,6 +294,8 @@ skv_status skv_cache_destroy(skv_cache* c) {
     cudaFree(c->stage);
     cudaFree(c->xbuf);
     cudaFree(c->gkeys);
+    cudaFree(c->gtok);
+    cudaFree(c->gwts);
     for (auto* v : {&c->ev_in, &c->ev_comp, &c->ev_out})
         for (cudaEvent_t e : *v) cudaEventDestroy(e);
     if (c->h2d) cudaStreamDestroy(c->h2d);
@@ -375,34 +379,43 @@ namespace {
 // smaller than one wave. So: the largest group that still gives >= half an
 // SM's worth of CTAs per SM count; for tiny batches the smallest group (most
 // parallelism). SKV_HG overrides (tuning).
-skv_status pick_attend(skv_cache* c, int m, const DecodeLaunch** dl_out, size_t* smem_out) {
+//
+// Selections too long for any head group's shared-memory token list and
+// weights (m beyond ~24 k) run with both in global scratch (gmem).
+skv_status pick_attend(skv_cache* c, int m, const DecodeLaunch** dl_out, size_t* smem_out, bool* gmem_out) {
     static const int env_hg = [] {
         const char* s = std::getenv("SKV_HG");
         return s ? std::atoi(s) : 0;
     }();
     const int cands[4] = {8, 4, 2, 1};
     const DecodeLaunch* chosen = nullptr;
-    const DecodeLaunch* smallest = nullptr;
-    size_t chosen_smem = 0, smallest_smem = 0;
-    for (int hg : cands) {
-        if (c->d.heads % hg != 0) continue;
-        if (env_hg && hg != env_hg) continue;
-        const DecodeLaunch* dl = find_decode(c->d.kv_dtype, c->d.q_dtype, hg);
-        if (!dl) continue;
-        const size_t smem = dl->smem(m);
-        if (smem > static_cast<size_t>(c->max_smem)) continue;
-        smallest = dl;
-        smallest_smem = smem;
-        const long long ctas = static_cast<long long>(c->d.batch) * (c->d.heads / hg);
-        if (!chosen && 2 * ctas >= c->num_sms) {
-            chosen = dl;
-            chosen_smem = smem;
+    size_t chosen_smem = 0;
+    bool gmem = false;
+    for (int pass = 0; pass < 2 && !chosen; ++pass) {
+        gmem = pass == 1;
+        const DecodeLaunch* smallest = nullptr;
+        size_t smallest_smem = 0;
+        for (int hg : cands) {
+            if (c->d.heads % hg != 0) continue;
+            if (env_hg && hg != env_hg) continue;
+            const DecodeLaunch* dl = find_decode(c->d.kv_dtype, c->d.q_dtype, hg);
+            if (!dl) continue;
+            const size_t smem = dl->smem(m, gmem);
+            if (smem > static_cast<size_t>(c->max_smem)) continue;
+            smallest = dl;
+            smallest_smem = smem;
+            const long long ctas = static_cast<long long>(c->d.batch) * (c->d.heads / hg);
+            if (!chosen && 2 * ctas >= c->num_sms) {
+                chosen = dl;
+                chosen_smem = smem;
+            }
+        }
+        if (!chosen) {
+            chosen = smallest;
+            chosen_smem = smallest_smem;
         }
     }
-    if (!chosen) {
-        chosen = smallest;
-        chosen_smem = smallest_smem;
-    }
+    *gmem_out = gmem;
     if (!chosen)
         return fail(SKV_ERR_UNSUPPORTED, "no attend kernel fits (heads %d, m %d, shared memory %d)", c->d.heads, m,
                     c->max_smem);
@@ -595,7 +608,17 @@ skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok
                            float* w_out, bool pdl, cudaStream_t st, int* G_out, const FoldSpec& fold = FoldSpec{}) {
     const DecodeLaunch* dl = nullptr;
     size_t smem = 0;
-    if (skv_status s = pick_attend(c, m, &dl, &smem)) return s;
+    bool gmem = false;
+    if (skv_status s = pick_attend(c, m, &dl, &smem, &gmem)) return s;
+    if (gmem && !c->gtok) {  // long selection: token list + weights in global scratch
+        const size_t cells = static_cast<size_t>(c->d.batch) * c->d.heads * c->d.capacity;
+        if (cudaMalloc(reinterpret_cast<void**>(&c->gtok), cells * 4) != cudaSuccess ||
+            cudaMalloc(reinterpret_cast<void**>(&c->gwts), cells * 4) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(SKV_ERR_OOM, "attend: cannot allocate %zu bytes of long-selection scratch", 2 * cells * 4);
+        }
+        c->device_bytes += 2 * cells * 4;
+    }
     const int G = c->d.heads / dl->hg;
     skvd::SelectParams sel{};
     bool fused = fold.apply != 0;
@@ -640,6 +663,10 @@ skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok
     p.out_f32 = c->d.out_f32 ? 1 : 0;
     p.pdl_wait = 0;  // inputs are complete before the first (non-PDL) launch of a call
     p.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c->d.head_dim)));
+    if (gmem) {
+        p.gtok = c->gtok;
+        p.gwts = c->gwts;
+    }
     if (fused) {
         p.fold = 1;
         p.sel = sel;

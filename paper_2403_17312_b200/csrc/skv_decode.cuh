@@ -72,6 +72,10 @@ struct AttendParams {
     // (fold_and_select, skv_select.cuh) -- no separate select launch.
     int fold;
     unsigned* counters;  // [B], zero between launches
+    // Long selections: the token list and the logits / weights live in global
+    // scratch instead of shared memory ([B][G][Ncap] ids, [B][G][HG][Ncap] f32)
+    int* gtok;
+    float* gwts;
     SelectParams sel;    // imp / wpart / apply / cur_tok / sparsity / next selection; tok_prev = this CTA's list
 };
 
@@ -105,9 +109,11 @@ struct DecodeSmem {
     size_t ring, bars, tok, wts, topk, scratch, flag, total;
 };
 
-// Shared-memory carve-up; identical on host (launch size) and device.
+// Shared-memory carve-up; identical on host (launch size) and device. gmem:
+// the token list and the weights are in global scratch (long selections).
 template <class KV, int HG>
-__host__ __device__ inline DecodeSmem decode_smem(int m) {
+__host__ __device__ inline DecodeSmem decode_smem(int m, bool gmem = false) {
+    if (gmem) m = 0;
     using C = DecodeCfg<KV, HG>;
     DecodeSmem s;
     size_t o = 0;
@@ -171,13 +177,16 @@ __global__ void __launch_bounds__(kDecodeThreads)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int g = blockIdx.x, b = blockIdx.y, G = gridDim.x;
     const int H = p.H, n = p.n, m = p.m;
-    const DecodeSmem L = decode_smem<KV, HG>(m);
+    const bool gmem = p.gtok != nullptr;
+    const DecodeSmem L = decode_smem<KV, HG>(m, gmem);
 
     uint8_t* ring = smem + L.ring;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
     uint64_t* empty = full + S;
-    int* tok = reinterpret_cast<int*>(smem + L.tok);
-    float* wts = reinterpret_cast<float*>(smem + L.wts);  // [HG][m]
+    int* tok = gmem ? p.gtok + (static_cast<size_t>(b) * gridDim.x + g) * p.Ncap
+                    : reinterpret_cast<int*>(smem + L.tok);
+    float* wts = gmem ? p.gwts + (static_cast<size_t>(b) * gridDim.x + g) * HG * p.Ncap
+                      : reinterpret_cast<float*>(smem + L.wts);  // [HG][m]
 
     // Let the next kernel in the stream (the select kernel) get scheduled now;
     // it waits for this grid's completion before touching our outputs.

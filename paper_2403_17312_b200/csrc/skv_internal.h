@@ -56,7 +56,7 @@ cudaError_t launch_recompute_gather(const uint8_t* x, long long x_seq, long long
 // Fused decode kernel: one instantiation per (kv dtype, q dtype, HG).
 struct DecodeLaunch {
     const void* func;
-    size_t (*smem)(int m);
+    size_t (*smem)(int m, bool gmem);  // gmem: token list + weights in global scratch
     int hg;
     size_t ring_bytes;  // shared-memory ring (reused for the tail's selection keys)
 };

@@ -486,3 +486,29 @@ def test_long_context_select(api, port):
         assert torch.equal(a, b)
         for l in range(L):
             assert torch.equal(caches[0].importance(l, n), caches[1].importance(l, n))
+
+
+def test_long_selection_global_scratch(api, port):
+    """Selections longer than any shared-memory token list / weight buffer
+    (m = n = 36k: the dense prefill seed and a dense r = 1 decode step) run
+    with both in global scratch and match the oracle."""
+    D, s, H = 128, 36000, 2
+    rng = np.random.default_rng(361)
+    kv = round_to(rng.standard_normal((1, s + 1, 2, H, D)), "f16")
+    q = round_to(rng.standard_normal((2, 1, H, D)) * 1.5, "f16")
+    cache = api.SwaCache(1, 1, H, D, s + 1, kv_dtype="f16")
+    cache.append_tokens(0, 0, 0, cuda(kv[:, :s, 0], torch.float16), cuda(kv[:, :s, 1], torch.float16))
+    seed_out = cache.prefill_seed(0, s, cuda(q[0], torch.float16)).float().cpu().numpy()[0]
+    seq = OracleSeq(port, H, D, s + 1)
+    for t in range(s):
+        seq.append(t, kv[0, t, 0], kv[0, t, 1])
+    assert_close(seed_out, seq.seed(s, q[0][0]), TOL["f16"], "dense seed, m = 36000")
+    np.testing.assert_allclose(cache.importance(0, s).cpu().numpy()[0], seq.importance(s), rtol=1e-4, atol=1e-7)
+    n = s + 1
+    out, idx, _ = cache.swa_decode_layer(0, n, 1.0, cuda(q[1], torch.float16), cuda(kv[:, s, 0], torch.float16),
+                                         cuda(kv[:, s, 1], torch.float16), return_indices=True)
+    seq.append(s, kv[0, s, 0], kv[0, s, 1])
+    attn, _, oidx = seq.step(n, 1.0, q[1][0])
+    assert np.array_equal(idx.cpu().numpy()[0], oidx)
+    assert_close(out.float().cpu().numpy()[0], attn, TOL["f16"], "dense decode, m = 36001")
+    np.testing.assert_allclose(cache.importance(0, n).cpu().numpy()[0], seq.importance(n), rtol=1e-4, atol=1e-7)
