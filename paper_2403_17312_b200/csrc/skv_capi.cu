@@ -1124,10 +1124,18 @@ skv_status skv_swa_select(const double* importance, int batch, int64_t ld, int n
     if (!dense) {
         SKV_REQUIRE(importance != nullptr, "swa_select: importance length must be n-1");
         SKV_REQUIRE(ld >= n - 1, "swa_select: row stride shorter than n-1");
-        if (static_cast<size_t>(n - k) * 8 + 8192 > 220 * 1024)
-            return fail(SKV_ERR_UNSUPPORTED, "swa_select: %d candidates exceed shared memory", n - static_cast<int>(k));
+    }
+    // long rows: the candidates' keys go to a stream-ordered scratch
+    // ([batch][ld], the importance layout) instead of shared memory
+    const bool long_row = !dense && static_cast<size_t>(n - k) * 8 + 8192 > 220 * 1024;
+    uint64_t* gkeys = nullptr;
+    if (long_row && cudaMallocAsync(reinterpret_cast<void**>(&gkeys), static_cast<size_t>(batch) * ld * 8,
+                                    as_stream(stream)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(SKV_ERR_OOM, "swa_select: cannot allocate key scratch for %d candidates", n - static_cast<int>(k));
     }
     skvd::SelectParams p{};
+    p.gkeys = gkeys;
     p.imp = const_cast<double*>(importance);
     p.imp_ld = ld;
     p.select = 1;
@@ -1139,6 +1147,7 @@ skv_status skv_swa_select(const double* importance, int batch, int64_t ld, int n
     p.idx_ld = m;
     p.variant = SKV_VARIANT_SWA;
     SKV_CUDA(launch_select(p, batch, false, as_stream(stream)));
+    if (gkeys) SKV_CUDA(cudaFreeAsync(gkeys, as_stream(stream)));
     return SKV_OK;
 }
 

@@ -67,9 +67,12 @@ def test_swa_select_golden(api, golden):
         assert np.array_equal(got, want), (n, r)
 
 
-def test_swa_select_batched(api, port):
+@pytest.mark.parametrize("n", [1024, 40000])
+def test_swa_select_batched(api, port, n):
+    """swa_select on caller importance rows, ties included (values rounded to
+    1e-3); n = 40000 puts the keys in global scratch."""
     rng = np.random.default_rng(9)
-    B, n = 8, 1024
+    B = 8
     imp = np.round(rng.random((B, n + 7)) * 1000) / 1000.0
     sel = api.swa_select(cuda(imp), n, 0.2)
     for b in range(B):
