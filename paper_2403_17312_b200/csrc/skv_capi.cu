@@ -1156,8 +1156,6 @@ skv_status skv_top_k_indices(const double* v, int batch, int64_t ld, int len, in
     SKV_REQUIRE(batch >= 1 && ld >= len, "top_k_indices: bad batch layout");
     if (k == 0) return SKV_OK;
     SKV_REQUIRE(v != nullptr && out != nullptr, "top_k_indices: null argument");
-    if (static_cast<size_t>(len) * 8 + 8192 > 220 * 1024)
-        return fail(SKV_ERR_UNSUPPORTED, "top_k_indices: length %d exceeds shared memory", len);
     SKV_CUDA(launch_top_k(v, batch, ld, len, k, out, as_stream(stream)));
     return SKV_OK;
 }

@@ -241,11 +241,14 @@ __global__ void __launch_bounds__(kSelectThreads) swa_select_kernel(const Select
 
 // top_k_indices (matrix.hpp:162-176) per row.
 __global__ void __launch_bounds__(kSelThreads)
-    top_k_kernel(const double* __restrict__ v, long long ld, int len, int k, int* __restrict__ out) {
+    top_k_kernel(const double* __restrict__ v, long long ld, int len, int k, int* __restrict__ out,
+                 uint64_t* gkeys) {
     extern __shared__ __align__(128) uint8_t smem[];
     TopkSmem<kSelThreads>& s = *reinterpret_cast<TopkSmem<kSelThreads>*>(smem);
-    uint64_t* keys = reinterpret_cast<uint64_t*>(smem + align_up(sizeof(TopkSmem<kSelThreads>), 16));
     const int b = blockIdx.x, tid = threadIdx.x;
+    // keys in shared memory, or in the caller-row-shaped global scratch for long rows
+    uint64_t* keys = gkeys ? gkeys + static_cast<size_t>(b) * ld
+                           : reinterpret_cast<uint64_t*>(smem + align_up(sizeof(TopkSmem<kSelThreads>), 16));
     const double* row = v + static_cast<size_t>(b) * ld;
     for (int i = tid; i < len; i += kSelThreads) keys[i] = order_key(row[i]);
     named_sync(1, kSelThreads);
@@ -477,13 +480,21 @@ cudaError_t launch_transpose_kv_weights(const void* wk, const void* wv, void* bt
 
 cudaError_t launch_top_k(const double* v, int batch, long long ld, int len, int k, int* out,
                          cudaStream_t st) {
-    const size_t smem = align_up(sizeof(TopkSmem<kSelThreads>), 16) + static_cast<size_t>(len) * 8;
-    cudaError_t e = cudaFuncSetAttribute(top_k_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    const bool long_row = static_cast<size_t>(len) * 8 + 8192 > 220 * 1024;
+    const size_t smem = align_up(sizeof(TopkSmem<kSelThreads>), 16) + (long_row ? 0 : static_cast<size_t>(len) * 8);
+    uint64_t* gkeys = nullptr;
+    cudaError_t e = cudaSuccess;
+    if (long_row) {
+        e = cudaMallocAsync(reinterpret_cast<void**>(&gkeys), static_cast<size_t>(batch) * ld * 8, st);
+        if (e != cudaSuccess) return e;
+    }
+    e = cudaFuncSetAttribute(top_k_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    top_k_kernel<<<batch, kSelThreads, smem, st>>>(v, ld, len, k, out);
+    top_k_kernel<<<batch, kSelThreads, smem, st>>>(v, ld, len, k, out, gkeys);
     count_launch();
-    return cudaGetLastError();
+    e = cudaGetLastError();
+    if (gkeys) cudaFreeAsync(gkeys, st);
+    return e;
 }
 
 cudaError_t launch_quantize(const double* x, long long len, long long cs, uint32_t bits,

@@ -50,7 +50,7 @@ def test_top_k_golden(api, golden):
 
 def test_top_k_random_large(api, port):
     rng = np.random.default_rng(5)
-    for ln, k in [(922, 102), (3686, 410), (20000, 1), (5000, 5000), (1, 1), (4096, 2048)]:
+    for ln, k in [(922, 102), (3686, 410), (20000, 1), (5000, 5000), (1, 1), (4096, 2048), (60000, 3000)]:
         v = rng.standard_normal(ln)
         v[rng.integers(0, ln, ln // 4)] = 0.5  # mass ties
         v[:3] = -0.0
