@@ -164,8 +164,15 @@ __device__ __forceinline__ float reduce_rows(float (&v)[RS], int c, int& row) {
     return v[0];
 }
 
+// CTAs per SM the register budget must allow (ptxas otherwise picked
+// budgets that spilled): 3 for 16/32-bit rows, 2 for INT8 (wider stages).
+template <class KV>
+constexpr int attend_min_blocks() {
+    return KV::QUANT ? 2 : 3;
+}
+
 template <class KV, class QT, int HG>
-__global__ void __launch_bounds__(kDecodeThreads)
+__global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
     swa_attend_kernel(const AttendParams p) {
     using C = DecodeCfg<KV, HG>;
     constexpr int D = C::D, VE = C::VE, V2 = C::V2, LR = C::LR, RPW = C::RPW, SLOTS = C::SLOTS;
