@@ -25,11 +25,14 @@
 #include <stdexcept>
 #include <string>
 #include <vector>
+#include <utility>
 
 #include "skv/attention.hpp"
 #include "skv/common.hpp"
 #include "skv/matrix.hpp"
 #include "skv/quant.hpp"
+#include "skv/memsim.hpp"
+#include "skv/scheduler.hpp"
 #include "skv_b200.h"
 
 namespace skv::b200 {
@@ -118,6 +121,15 @@ class DeviceCache {
     // given stream, e.g. with ncclAllReduce.
     void set_head_shard(int head_offset, int total_heads, skv_reduce_fn reduce, void* user) {
         check(skv_cache_set_head_shard(c_, head_offset, total_heads, reduce, user));
+    }
+    // KvLedger / scheduler (memsim.hpp:72-215, scheduler.hpp:28-381) on the device
+    void set_plan(const skv_plan& plan) { check(skv_cache_set_plan(c_, &plan)); }
+    void ledger_set(int layer, int b0, int nb, int len, const std::uint8_t* tiers, void* st = nullptr) {
+        check(skv_ledger_set(c_, layer, b0, nb, len, tiers, st));
+    }
+    void step_actions(int layer, int j, const int32_t* selected, int m, int k, bool apply, int32_t* lists,
+                      int32_t* counts, void* st = nullptr) {
+        check(skv_step_actions(c_, layer, j, selected, m, k, apply ? 1 : 0, lists, counts, st));
     }
 
   private:
@@ -288,6 +300,78 @@ inline StepAttentionResult swa_attention(AttentionState& state, const Matrix& q_
     StepAttentionResult res = b200::attend_over_indices(state, q_step, sel.all());
     res.selection = std::move(sel);
     return res;
+}
+
+// attention.hpp:91-117: softmax(q k^T / sqrt(D)) v per query row, causal =
+// row i sees keys 0..i; returns (attn, aw). Each row is one attend over its
+// (causal) key range on a one-head fp32 cache: results match the fp64
+// reference within 1e-5 relative. head_dim 128 only (the compiled kernels).
+inline std::pair<Matrix, Matrix> dense_attention(const Matrix& q, const Matrix& k, const Matrix& v, bool causal) {
+    require(q.cols == k.cols && k.rows == v.rows && k.cols == v.cols, "dense_attention: shape mismatch");
+    require(!causal || q.rows <= k.rows, "dense_attention: causal needs rows <= keys");
+    const std::size_t sq = q.rows, sk = k.rows, D = q.cols;
+    std::pair<Matrix, Matrix> res{Matrix(sq, v.cols), Matrix(sq, sk)};
+    if (sq == 0 || sk == 0) return res;
+    DeviceCache cache(1, 1, 1, static_cast<int>(D), static_cast<int>(sk), SKV_F32, SKV_F32, 0, true);
+    std::vector<float> kf(sk * D), vf(sk * D);
+    for (std::size_t i = 0; i < sk * D; ++i) {
+        kf[i] = static_cast<float>(k.data[i]);
+        vf[i] = static_cast<float>(v.data[i]);
+    }
+    DeviceBuffer dk(kf.size() * 4), dv(vf.size() * 4), dq(D * 4), dout(D * 4), didx(sk * 4), dw(sk * 4);
+    dk.upload(kf.data(), kf.size() * 4);
+    dv.upload(vf.data(), vf.size() * 4);
+    cache.append_tokens(0, 0, 1, 0, static_cast<int>(sk), dk.get(), dv.get());
+    std::vector<int32_t> idx(sk);
+    for (std::size_t i = 0; i < sk; ++i) idx[i] = static_cast<int32_t>(i);
+    didx.upload(idx.data(), sk * 4);
+    std::vector<float> qf(D), out(D), w(sk);
+    for (std::size_t r = 0; r < sq; ++r) {
+        const std::size_t n = causal ? r + 1 : sk;
+        for (std::size_t d = 0; d < D; ++d) qf[d] = static_cast<float>(q.at(r, d));
+        dq.upload(qf.data(), D * 4);
+        cache.attend_over_indices(0, static_cast<int>(n), didx.as<int32_t>(), static_cast<int>(n), dq.get(),
+                                  dout.get(), dw.as<float>());
+        dout.download(out.data(), D * 4);
+        dw.download(w.data(), n * 4);
+        for (std::size_t d = 0; d < v.cols; ++d) res.first.at(r, d) = out[d];
+        for (std::size_t t = 0; t < n; ++t) res.second.at(r, t) = w[t];
+    }
+    return res;
+}
+
+// scheduler.hpp:320-381 on the reference's own types: the ledger row of
+// `layer` and the selection go to a one-sequence device cache, the device
+// kernel derives the four lists (the ones skv_swa_decode_step applies).
+inline StepActions step_actions(const SchedulePlan& plan, std::size_t j, const SparseSelection& selection,
+                                const KvLedger& ledger, std::size_t layer, const CostParams& p) {
+    require(j < p.output_len, "step_actions: step beyond output length");
+    require(layer < ledger.layers(), "KvLedger: layer out of range");
+    const std::size_t cap = p.input_len + j + 1;
+    DeviceCache cache(static_cast<int>(layer) + 1, 1, 1, 128, static_cast<int>(cap), SKV_F16, SKV_F16);
+    skv_plan pl{plan.alpha, plan.beta, static_cast<int64_t>(plan.p1), static_cast<int64_t>(plan.p2),
+                plan.recompute_enabled ? 1 : 0, static_cast<int64_t>(p.input_len),
+                static_cast<int64_t>(p.output_len)};
+    cache.set_plan(pl);
+    std::vector<std::uint8_t> tiers(cap, 255);
+    for (std::size_t t = 0; t < cap; ++t)
+        if (ledger.exists(layer, t)) tiers[t] = static_cast<std::uint8_t>(ledger.tier(layer, t));
+    cache.ledger_set(static_cast<int>(layer), 0, 1, static_cast<int>(cap), tiers.data());
+    const IndexList all = selection.all();
+    std::vector<int32_t> sel(all.begin(), all.end());
+    DeviceBuffer dsel(std::max<std::size_t>(sel.size(), 1) * 4);
+    if (!sel.empty()) dsel.upload(sel.data(), sel.size() * 4);
+    std::vector<int32_t> lists(4 * cap), counts(4);
+    cache.step_actions(static_cast<int>(layer), static_cast<int>(j), dsel.as<int32_t>(), static_cast<int>(sel.size()),
+                       static_cast<int>(selection.k), false, lists.data(), counts.data());
+    check(skv_stream_synchronize(nullptr));
+    StepActions a;
+    // phase_of_step (scheduler.hpp:52-60)
+    a.phase = j < plan.p1 ? 1 : ((j < plan.p2 || !plan.recompute_enabled) ? 2 : 3);
+    IndexList* out[4] = {&a.offload, &a.delete_tokens, &a.reload, &a.recompute};
+    for (int l = 0; l < 4; ++l)
+        for (int i = 0; i < counts[l]; ++i) out[l]->push_back(static_cast<std::size_t>(lists[l * cap + i]));
+    return a;
 }
 
 }  // namespace skv::b200

@@ -9,6 +9,8 @@
 #include "skv/attention.hpp"
 #include "skv/b200.hpp"
 #include "skv/quant.hpp"
+#include "skv/scheduler.hpp"
+#include "skv/memsim.hpp"
 
 using namespace skv;
 
@@ -93,6 +95,67 @@ int main() {
             for (std::size_t i = 0; i < ref.attention_accum[h].size(); ++i)
                 acc_err = std::max(acc_err, std::abs(ref.attention_accum[h][i] - dev.attention_accum[h][i]));
         CHECK(acc_err <= 1e-5, "accumulators step %d err %g", step, acc_err);
+    }
+    // dense_attention (attention.hpp:91-117): causal and full, fp32 device vs fp64
+    for (bool causal : {true, false}) {
+        const std::size_t rows = 70, Dd = 128;
+        Matrix qm(rows, Dd), km(rows, Dd), vm(rows, Dd);
+        for (double& x : qm.data) x = static_cast<float>(rng.normal() * 0.5);
+        for (double& x : km.data) x = static_cast<float>(rng.normal());
+        for (double& x : vm.data) x = static_cast<float>(rng.normal());
+        const auto a = dense_attention(qm, km, vm, causal);
+        const auto b = b200::dense_attention(qm, km, vm, causal);
+        const double e1 = rel_err(b.first, a.first);
+        double e2 = 0;
+        for (std::size_t i = 0; i < a.second.data.size(); ++i)
+            e2 = std::max(e2, std::abs(a.second.data[i] - b.second.data[i]));
+        CHECK(e1 <= 1e-5 && e2 <= 1e-5, "dense_attention causal=%d attn %g aw %g", causal, e1, e2);
+    }
+    // step_actions (scheduler.hpp:320-381) on the reference KvLedger / SchedulePlan
+    for (int rep = 0; rep < 40; ++rep) {
+        CostParams cp;
+        cp.hidden = 64;
+        cp.layers = 2;
+        cp.batch = 1;
+        cp.input_len = 60 + rng.integer(60);
+        cp.output_len = 40;
+        cp.ratio = 0.2;
+        cp.device_capacity = 1ull << 40;
+        const std::size_t j = rng.integer(cp.output_len);
+        const std::size_t layer = rng.integer(2);
+        const std::size_t existing = cp.input_len + j;
+        KvLedger ledger(2, cp.device_capacity);
+        for (std::size_t t = 0; t < existing; ++t) ledger.store_new(layer, t, 64);
+        IndexList off, del;
+        for (std::size_t t = 0; t < existing; ++t) {
+            const double u = rng.uniform();
+            if (u < 0.3) off.push_back(t);
+        }
+        ledger.offload(layer, off);
+        for (const std::size_t t : off)
+            if (rng.uniform() < 0.3) del.push_back(t);
+        ledger.erase(layer, del);
+        SchedulePlan plan;
+        // valid plans only (validate_plan, scheduler.hpp:41-49): pure device, or 0 <= p1 < p2 <= n
+        plan.alpha = 0.05 + rng.uniform() * 0.6;
+        plan.beta = 0.05 + rng.uniform() * 0.5;
+        if (rep % 8 == 0) {
+            plan.p1 = plan.p2 = cp.output_len;
+        } else {
+            plan.p1 = rng.integer(cp.output_len);
+            plan.p2 = plan.p1 + 1 + rng.integer(cp.output_len - plan.p1);
+        }
+        plan.recompute_enabled = rep % 3 != 0;
+        Vector imp(existing);
+        for (double& x : imp) x = rng.uniform();
+        const SparseSelection sel = swa_select(imp, existing + 1, 0.2);
+        const StepActions a = step_actions(plan, j, sel, ledger, layer, cp);
+        const StepActions b = b200::step_actions(plan, j, sel, ledger, layer, cp);
+        CHECK(a.phase == b.phase && a.offload == b.offload && a.delete_tokens == b.delete_tokens &&
+                  a.reload == b.reload && a.recompute == b.recompute,
+              "step_actions rep %d (phase %d/%d, offload %zu/%zu, delete %zu/%zu, reload %zu/%zu, recompute %zu/%zu)",
+              rep, a.phase, b.phase, a.offload.size(), b.offload.size(), a.delete_tokens.size(),
+              b.delete_tokens.size(), a.reload.size(), b.reload.size(), a.recompute.size(), b.recompute.size());
     }
     // error semantics: reference exception classes
     bool threw = false;
