@@ -442,5 +442,35 @@ class SwaCache:
         return ms.value, n.value, b.value
 
 
+# ---- attention.hpp:91-117 ---------------------------------------------------
+def dense_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal: bool):
+    """softmax(q k^T / sqrt(D)) v per query row (causal: row i sees keys
+    0..i) -> (attn [sq, D], aw [sq, sk]) fp32, like the reference's pair.
+    Each row is one attend over its key range on a one-head fp32 cache
+    (head_dim 128); for the batched causal prefill of a cache use
+    SwaCache.prefill_layer (tensor cores)."""
+    sq, D = q.shape
+    sk = k.shape[0]
+    if k.shape != (sk, D) or v.shape != (sk, D):
+        raise ContractViolation("dense_attention: shape mismatch")
+    if causal and sq > sk:
+        raise ContractViolation("dense_attention: causal needs rows <= keys")
+    dev = q.device
+    cache = SwaCache(1, 1, 1, D, sk, kv_dtype="f32", device=dev.index, out_f32=True)
+    f = lambda t: t.to(device=dev, dtype=torch.float32).contiguous()  # noqa: E731
+    cache.append_tokens(0, 0, 0, f(k).reshape(1, sk, 1, D), f(v).reshape(1, sk, 1, D))
+    idx = torch.arange(sk, dtype=torch.int32, device=dev)
+    attn = torch.empty((sq, D), dtype=torch.float32, device=dev)
+    aw = torch.zeros((sq, sk), dtype=torch.float32, device=dev)
+    qf = f(q)
+    for r in range(sq):
+        n = r + 1 if causal else sk
+        out, w = cache.attend_over_indices(0, n, idx[:n], qf[r].reshape(1, 1, D), return_weights=True)
+        attn[r] = out[0, 0]
+        aw[r, :n] = w[0, 0]
+    cache.close()
+    return attn, aw
+
+
 def launch_count() -> int:
     return lib().skv_launch_count()

@@ -515,3 +515,16 @@ def test_long_selection_global_scratch(api, port):
     assert np.array_equal(idx.cpu().numpy()[0], oidx)
     assert_close(out.float().cpu().numpy()[0], attn, TOL["f16"], "dense decode, m = 36001")
     np.testing.assert_allclose(cache.importance(0, n).cpu().numpy()[0], seq.importance(n), rtol=1e-4, atol=1e-7)
+
+
+@pytest.mark.parametrize("causal", [True, False])
+def test_dense_attention(api, port, causal):
+    """dense_attention (attention.hpp:91-117) through the C ABI vs the oracle:
+    outputs and the full weight matrix within the fp32 tolerance."""
+    rng = np.random.default_rng(17)
+    s, D = 90, 128
+    q, k, v = (rng.standard_normal((s, D)) * sc for sc in (0.5, 1.0, 1.0))
+    attn, aw = api.dense_attention(cuda(q), cuda(k), cuda(v), causal)
+    r_attn, r_aw = port.dense_attention(q, k, v, causal)
+    assert_close(attn.cpu().numpy(), r_attn, TOL["f32"], "dense_attention attn")
+    np.testing.assert_allclose(aw.cpu().numpy(), r_aw, rtol=1e-5, atol=1e-7)
