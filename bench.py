@@ -174,6 +174,18 @@ def attend_algo_bytes(cfg, n: int) -> int:
     return B * (H * D * 2 * eq + 2 * H * D * eq + 2 * H * row + 2 * (m - 1) * H * row)
 
 
+def cpu_model() -> str:
+    """The host CPU the baseline ran on (SURVEY §8 d: state T and the CPU)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(cfg, n_mid: int, budget_s: float = 15.0):
     """The reference's own swa_attention (oracle/_ref, compiled from the
     reference headers) -- else the oracle port -- on all host cores, one
@@ -193,7 +205,7 @@ def cpu_baseline(cfg, n_mid: int, budget_s: float = 15.0):
             "sample": f"{items} (sequence, layer) decode items (append + swa_attention) at n={n_mid}..{n_mid + 15} "
                       f"(rounds of 16, state trimmed between rounds), H={H}, D={D}, r={RATIO}, fp64, {threads} "
                       f"share-nothing threads; tokens/s = items / slowest thread's busy seconds / L={cfg['L']}",
-            "seconds": t}
+            "seconds": t, "cpu_model": cpu_model()}
 
 
 def run_reference(args, cfg, rank: int, world: int):
