@@ -404,9 +404,10 @@ def main():
     # ---- prompt: random K/V for s tokens per layer, then Engine::prefill's
     # attention (engine.hpp:485-529) on the tensor cores: causal attention of
     # all s prompt queries, the accumulator seeded with the last row
-    # (engine.hpp:508-512). INT8 caches take the last-row seed only.
+    # (engine.hpp:508-512). INT8 caches are dequantised to fp16 for it (and
+    # re-seeded on the exact dequantisation); fp32 (config 1) takes the seed only.
     g = torch.Generator(device="cuda").manual_seed(2403_17312 + args.config * 1000 + rank)
-    tc_prefill = cfg["kv"] in ("f16", "bf16")
+    tc_prefill = cfg["kv"] in ("f16", "bf16") or (cfg["kv"] == "u8" and cfg["q"] == "f16")
     pf_ms, pf_events = 0.0, []
     for l in range(L):
         chunk = max(1, min(B, (1 << 30) // (s * H * D * 2)))
@@ -443,7 +444,9 @@ def main():
             pass
         prefill = {"ms_per_layer": pf_ms, "layers": L, "prompt_tokens_per_s": seqs * s / (pf_ms / 1000.0),
                    "tflops": tf, "peak_tflops": bf16_peak, "frac": (tf / bf16_peak) if bf16_peak else None,
-                   "kernel": "skvd::flash_prefill_kernel (max pass + P.V pass) + prefill_seed_kernel",
+                   "kernel": "skvd::flash_prefill_kernel (max pass + P.V pass) + prefill_seed_kernel"
+                             + (" (INT8: dequant_layer_f16_kernel first, then the exact dense re-seed of the last "
+                                "row on the decode kernel)" if cfg["kv"] == "u8" else ""),
                    "note": "causal dense attention of the prompt per layer (skv_prefill_layer), mean over "
                            "layers 2..L; flops = 4 B H s(s+1)/2 D (the two causal GEMMs; the kernel "
                            "recomputes QK^T once more for the exact row max)"}

@@ -883,12 +883,18 @@ skv_status skv_prefill_layer(skv_cache* c, int layer, int s, const void* q, void
     SKV_REQUIRE(layer >= 0 && layer < c->d.layers, "KvLedger: layer out of range");
     SKV_REQUIRE(s >= 1 && s <= c->d.capacity, "prefill: prompt length out of range");
     SKV_REQUIRE(q != nullptr && out != nullptr, "prefill: null argument");
-    if (!(c->d.kv_dtype == c->d.q_dtype && (c->d.q_dtype == SKV_F16 || c->d.q_dtype == SKV_BF16)))
-        return fail(SKV_ERR_UNSUPPORTED, "prefill: tensor-core prefill needs an fp16/bf16 cache");
+    // INT8 caches (fp16 queries): the layer is dequantised to fp16 for the
+    // tensor cores; the seed row (and the last query's output) is then redone
+    // by the decode kernel on the exact fp32 dequantisation.
+    const bool int8 = c->d.kv_dtype == SKV_U8 && c->d.q_dtype == SKV_F16;
+    if (!int8 && !(c->d.kv_dtype == c->d.q_dtype && (c->d.q_dtype == SKV_F16 || c->d.q_dtype == SKV_BF16)))
+        return fail(SKV_ERR_UNSUPPORTED, "prefill: tensor-core prefill needs an fp16/bf16 cache or INT8 with fp16 q");
     DeviceGuard guard(c->d.device);
     const cudaStream_t st = as_stream(stream);
     const int B = c->d.batch, H = c->d.heads;
-    const size_t want = prefill_scratch_bytes(B, H, s);
+    const size_t base_scratch = (prefill_scratch_bytes(B, H, s) + 255) / 256 * 256;
+    const size_t deq_bytes = int8 ? static_cast<size_t>(B) * s * 2 * H * c->d.head_dim * 2 : 0;
+    const size_t want = base_scratch + deq_bytes;
     if (c->pf_bytes < want) {
         SKV_CUDA(cudaStreamSynchronize(st));
         cudaFree(c->pf_scratch);
@@ -911,21 +917,46 @@ skv_status skv_prefill_layer(skv_cache* c, int layer, int s, const void* q, void
     const size_t lay = static_cast<size_t>(layer);
     double* imp = c->imp + lay * B * c->d.capacity;
     double* psp = c->pf_sparsity + lay * B;
+    const void* kv = c->kv + lay * c->layer_bytes;
+    int kv_ncap = c->d.capacity;
+    if (int8) {
+        uint8_t* deq = c->pf_scratch + base_scratch;
+        SKV_CUDA(launch_dequant_layer_f16(c->kv + lay * c->layer_bytes, deq, H, c->d.capacity, B, s, st));
+        kv = deq;
+        kv_ncap = s;
+    }
     if (c->reduce) {
         // head shards: seed rows and the sparsity share (local sum / all heads)
         // into xbuf, summed across the shards, then into the importance
         double* xs = c->xbuf + static_cast<size_t>(B) * c->d.capacity;
-        SKV_CUDA(launch_prefill(c->d.q_dtype == SKV_BF16, c->d.out_f32 != 0, c->kv + lay * c->layer_bytes, q, out,
-                                c->xbuf, c->d.capacity, xs, B, H, c->d.head_dim, c->d.capacity, s, c->pf_scratch, st,
-                                c->total_heads));
+        SKV_CUDA(launch_prefill(c->d.q_dtype == SKV_BF16, c->d.out_f32 != 0, kv, q, out, c->xbuf, c->d.capacity, xs,
+                                B, H, c->d.head_dim, kv_ncap, s, c->pf_scratch, st, c->total_heads));
         if (skv_status e = c->reduce(c->xbuf, static_cast<size_t>(B) * (c->d.capacity + 1), st, c->reduce_user))
             return fail(e, "head-shard reduce failed (%d)", static_cast<int>(e));
         SKV_CUDA(cudaMemcpy2DAsync(imp, c->d.capacity * 8, c->xbuf, c->d.capacity * 8, static_cast<size_t>(s) * 8,
                                    B, cudaMemcpyDeviceToDevice, st));
         SKV_CUDA(cudaMemcpyAsync(psp, xs, static_cast<size_t>(B) * 8, cudaMemcpyDeviceToDevice, st));
     } else {
-        SKV_CUDA(launch_prefill(c->d.q_dtype == SKV_BF16, c->d.out_f32 != 0, c->kv + lay * c->layer_bytes, q, out,
-                                imp, c->d.capacity, psp, B, H, c->d.head_dim, c->d.capacity, s, c->pf_scratch, st));
+        SKV_CUDA(launch_prefill(c->d.q_dtype == SKV_BF16, c->d.out_f32 != 0, kv, q, out, imp, c->d.capacity, psp, B,
+                                H, c->d.head_dim, kv_ncap, s, c->pf_scratch, st));
+    }
+    if (int8) {
+        // exact seed (engine.hpp:508-512) and last-row output from the fp32
+        // dequantisation: the decode kernel's dense attend of query s-1
+        const size_t row = static_cast<size_t>(H) * c->d.head_dim * 2;  // fp16 q row [H][D]
+        const size_t orow = static_cast<size_t>(H) * c->d.head_dim * out_size(c);
+        uint8_t* qlast = c->pf_scratch + base_scratch;  // the fp16 copy is no longer needed
+        uint8_t* olast = qlast + static_cast<size_t>(B) * row;
+        SKV_CUDA(cudaMemcpy2DAsync(qlast, row, static_cast<const uint8_t*>(q) + (s - 1) * row, s * row, row, B,
+                                   cudaMemcpyDeviceToDevice, st));
+        int G = 0;
+        FoldSpec fold;
+        fold.apply = 2;
+        if (skv_status e = launch_attend_c(c, layer, s, s, nullptr, 0, false, qlast, nullptr, nullptr, olast, nullptr,
+                                           nullptr, false, st, &G, fold))
+            return e;
+        SKV_CUDA(cudaMemcpy2DAsync(static_cast<uint8_t*>(out) + (s - 1) * orow, s * orow, olast, orow, orow, B,
+                                   cudaMemcpyDeviceToDevice, st));
     }
     c->pend_n[layer] = -1;  // importance changed: any pending selection is stale
     return SKV_OK;

@@ -49,6 +49,8 @@ cudaError_t launch_prefill(bool bf16, bool out_f32, const void* kv, const void* 
                            long long imp_ld, double* psp, int B, int H, int D, int Ncap, int s, uint8_t* scratch,
                            cudaStream_t st, int h_div = 0);
 size_t prefill_scratch_bytes(int B, int H, int s);
+// INT8 cache layer -> fp16 [B][s][2][H][D] for the tensor-core prefill
+cudaError_t launch_dequant_layer_f16(const uint8_t* kv, void* out, int H, int Ncap, int B, int s, cudaStream_t st);
 cudaError_t launch_recompute_gather(const uint8_t* x, long long x_seq, long long x_row, const int* lists,
                                     const int* counts, long long list_ld, uint8_t* A, int2* rowmap, int* m_out,
                                     int B, cudaStream_t st);

@@ -396,6 +396,32 @@ __global__ void cache_read_kernel(const uint8_t* __restrict__ kv, float* __restr
     }
 }
 
+// INT8 layer -> fp16 [B][s][2][H][D] (the token-major layout the tensor-core
+// prefill's TMA maps read), x = scale * code + bias per (token, K|V, head).
+__global__ void dequant_layer_f16_kernel(const uint8_t* __restrict__ kv, __half* __restrict__ out, int H, int Ncap,
+                                         int B, int s) {
+    constexpr int D = kHeadDim;
+    const long long rows = static_cast<long long>(B) * s * 2 * H;
+    const long long r = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) / (D / 8);
+    const int c = static_cast<int>(threadIdx.x % (D / 8)) * 8;  // 8 codes per thread
+    if (r >= rows) return;
+    const int h = static_cast<int>(r % H);
+    const int which = static_cast<int>((r / H) % 2);
+    const int t = static_cast<int>((r / (2 * H)) % s);
+    const int b = static_cast<int>(r / (2LL * H * s));
+    const size_t tok = static_cast<size_t>(b) * Ncap + t;
+    const uint8_t* row = kv + ((tok * 2 + which) * H + h) * static_cast<size_t>(kv_row_bytes<KvU8>());
+    const float2 ms = *reinterpret_cast<const float2*>(row + D);
+    const uint2 codes = *reinterpret_cast<const uint2*>(row + c);  // rows are 8-byte aligned (136 B)
+    const uint8_t* cb = reinterpret_cast<const uint8_t*>(&codes);
+    __half2 o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        o[i] = __floats2half2_rn(fmaf(ms.x, static_cast<float>(cb[2 * i]), ms.y),
+                                 fmaf(ms.x, static_cast<float>(cb[2 * i + 1]), ms.y));
+    *reinterpret_cast<uint4*>(out + r * D + c) = *reinterpret_cast<const uint4*>(o);
+}
+
 }  // namespace skvd
 
 // ============================================================ launchers
@@ -575,3 +601,13 @@ extern "C" int skv_debug_select_trace(long long* out) {
     return static_cast<int>(cudaMemcpyFromSymbol(out, skvd::g_sel_trace, sizeof(long long) * 16));
 }
 #endif
+
+namespace skv_impl {
+cudaError_t launch_dequant_layer_f16(const uint8_t* kv, void* out, int H, int Ncap, int B, int s, cudaStream_t st) {
+    const long long threads = static_cast<long long>(B) * s * 2 * H * (skvd::kHeadDim / 8);
+    skvd::dequant_layer_f16_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(
+        kv, static_cast<__half*>(out), H, Ncap, B, s);
+    count_launch();
+    return cudaGetLastError();
+}
+}  // namespace skv_impl

@@ -117,12 +117,45 @@ def test_prefill_then_decode(api, port):
             assert_close(out[b], attn, TOL[dt], f"decode after prefill step {j}")
 
 
-def test_prefill_rejects_int8_and_bad_shapes(api):
-    c = api.SwaCache(1, 1, 2, 128, 64, kv_dtype="u8", q_dtype="f16")
+def test_prefill_rejects_unsupported_and_bad_shapes(api):
+    c = api.SwaCache(1, 1, 2, 128, 64, kv_dtype="u8", q_dtype="f32")  # INT8 needs fp16 queries
     with pytest.raises(api.Unsupported):
-        c.prefill_layer(0, torch.zeros((1, 8, 2, 128), dtype=torch.float16, device="cuda"))
+        c.prefill_layer(0, torch.zeros((1, 8, 2, 128), dtype=torch.float32, device="cuda"))
     c = api.SwaCache(1, 1, 2, 128, 64, kv_dtype="f16")
     with pytest.raises(api.ContractViolation):
         c.prefill_layer(0, torch.zeros((1, 65, 2, 128), dtype=torch.float16, device="cuda"))
     with pytest.raises(api.ContractViolation):
         c.prefill_sparsity(0)
+
+
+def test_prefill_int8(api, port):
+    """INT8 KV (fp16 queries): the layer is dequantised to fp16 for the tensor
+    cores; the seed row and the last query's output are redone on the exact
+    dequantisation. Reference: dense_attention on the fake-quantised K/V
+    (engine.hpp:469-483 groups of D per (token, head))."""
+    B, H, s, D = 2, 4, 300, 128
+    rng = np.random.default_rng(88)
+    k = round_to(rng.standard_normal((B, s, H, D)), "f16")
+    v = round_to(rng.standard_normal((B, s, H, D)), "f16")
+    q = round_to(rng.standard_normal((B, s, H, D)) * 0.5, "f16")
+
+    def fake_quant(x):
+        flat = np.ascontiguousarray(x).reshape(-1)
+        c, sc, z = port.quantize(flat, 8, D)
+        return port.dequantize(c, D, sc, z).reshape(x.shape)
+
+    kq, vq = fake_quant(k), fake_quant(v)
+    cache = api.SwaCache(1, B, H, D, s + 4, kv_dtype="u8", q_dtype="f16")
+    cache.append_tokens(0, 0, 0, cuda(k, torch.float16), cuda(v, torch.float16))
+    out = cache.prefill_layer(0, cuda(q, torch.float16)).float().cpu().numpy()
+    imp = cache.importance(0, s).cpu().numpy()
+    sp = cache.prefill_sparsity(0).cpu().numpy()
+    for b in range(B):
+        seed_row, sp_ref = np.zeros(s), 0.0
+        for h in range(H):
+            attn, aw = port.dense_attention(q[b, :, h], kq[b, :, h], vq[b, :, h], True)
+            assert_close(out[b, :, h], attn, TOL["u8"], f"int8 prefill b{b} h{h}")
+            seed_row += aw[s - 1]
+            sp_ref += port.attention_sparsity(aw, 0.01, True)
+        np.testing.assert_allclose(imp[b], seed_row, rtol=1e-4, atol=1e-7)
+        assert abs(sp[b] - sp_ref / H) <= 2e-3, (b, sp[b], sp_ref / H)
