@@ -4,7 +4,8 @@ import os, sys, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2403_17312_b200 import api
 
-L, B, H, D, s = 32, 64, 32, 128, int(os.environ.get("PS", 512))
+L, B, H, D, s = (int(os.environ.get("PL", 32)), int(os.environ.get("PB", 64)), int(os.environ.get("PH", 32)), 128,
+              int(os.environ.get("PS", 512)))
 c = api.SwaCache(L, B, H, D, s + 160, kv_dtype="f16")
 g = torch.Generator(device="cuda").manual_seed(0)
 for l in range(L):
