@@ -231,6 +231,22 @@ def run_reference(args, cfg, rank: int, world: int):
     print(json.dumps(line), flush=True)
 
 
+def schedule_estimate(plan: dict, phases: dict, out_len: int, seqs: int) -> dict:
+    """The whole out_len-step decode under solve_plan's schedule (steps
+    [0, p1) Phase I, [p1, p2) Phase II, [p2, n) Phase III), priced with the
+    per-step times measured above from step 0 of each phase. An estimate: a
+    step's cost grows with the context, and the phases are timed at its start."""
+    p1 = min(int(plan.get("p1", out_len)), out_len)
+    p2 = min(max(int(plan.get("p2", out_len)), p1), out_len)
+    if not plan.get("recompute_enabled", True):  # phase_of_step: no Phase III without recomputation
+        p2 = out_len
+    spans = {"phase1": p1, "phase2": p2 - p1, "phase3": out_len - p2}
+    sec = sum(spans[k] * phases[k]["ms_per_step"] / 1000.0 for k in spans if spans[k] and k in phases)
+    return {"steps_per_phase": spans, "est_decode_seconds": sec,
+            "est_tokens_per_s": seqs * out_len / sec if sec > 0 else None,
+            "note": "per-phase step times from this run x solve_plan's phase lengths (start-of-phase costs)"}
+
+
 def run_config5(args, cfg, rank: int, world: int):
     """BASELINE config 5: the three-phase caching / eviction / recomputation
     schedule. solve_plan (host, scheduler.hpp:207-303) picks (alpha, beta, p1,
@@ -318,7 +334,8 @@ def run_config5(args, cfg, rank: int, world: int):
                            "device_kv_budget_bytes": budget, "plan": plan, "predicted": pred,
                            "note": "value = Phase I; Phase II/III time the same steps with the host tier, "
                                    "movement and tcgen05 recomputation active from step 0"},
-                "phases": phases}
+                "phases": phases,
+                "schedule": schedule_estimate(plan, phases, cfg["out_len"], world * B)}
         print(json.dumps(line), flush=True)
 
 
