@@ -141,7 +141,11 @@ skv_status skv_attend_over_indices(skv_cache* cache, int layer, int n, const int
 /* ---- standalone primitives on device buffers ----------------------------- */
 /* swa_select (attention.hpp:142-171) for `batch` rows of importance
  * (row stride ld): writes SparseSelection::all() ascending to idx_out
- * [batch][m]; *m_out = m (host). */
+ * [batch][m]; *m_out = m (host). Rows of more than ~27 k candidates keep
+ * their keys in a stream-ordered device scratch (cudaMallocAsync) instead of
+ * shared memory; the same holds for skv_top_k_indices. Lengths are not
+ * capped by the decode path either: long selections move the attend's token
+ * list and weights to global scratch. */
 skv_status skv_swa_select(const double* importance, int batch, int64_t ld, int n, double r,
                           int32_t* idx_out, int32_t* m_out, void* stream);
 /* top_k_indices (matrix.hpp:162-176) per row: out [batch][k] ascending. */
