@@ -372,8 +372,14 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
         const int rows = min(T, m - base) * HG;
         const uint8_t* st = ring + stage * STAGEB + lane_off;
         uint4 raw[RS];
+        if (rows == T * HG) {
 #pragma unroll
-        for (int i = 0; i < RS; ++i) raw[i] = ld16(st + i * SLOTS * ROWE);
+            for (int i = 0; i < RS; ++i) raw[i] = ld16(st + i * SLOTS * ROWE);
+        } else {  // last chunk: rows past it were not copied this round
+#pragma unroll
+            for (int i = 0; i < RS; ++i)
+                raw[i] = slot + i * SLOTS < rows ? ld16(st + i * SLOTS * ROWE) : make_uint4(0u, 0u, 0u, 0u);
+        }
         float part[RS];
 #pragma unroll
         for (int i = 0; i < RS; ++i) {
