@@ -68,3 +68,21 @@ def test_argument_errors_map_to_reference_classes(lib):
         check(lib.skv_top_k_indices(None, 1, 4, 4, 5, None, None))  # k exceeds length
     with pytest.raises(ContractViolation):
         check(lib.skv_quantize(None, 6, 3, 0, None, None, None, None))  # bits
+
+
+def test_header_is_plain_c(tmp_path):
+    """include/skv_b200.h is the FFI boundary for any host language: it must
+    compile as strict C99 (no C++ in the signatures) and a C program must
+    link against the library's exports."""
+    src = tmp_path / "use.c"
+    src.write_text('#include "skv_b200.h"\n'
+                   "int main(void) {\n"
+                   "    skv_cache_desc d = {1, 1, 8, 128, 64, SKV_F16, SKV_F16, 0, 0};\n"
+                   "    (void)d;\n"
+                   "    return skv_swa_window_k(512, 0.2) == 51 ? 0 : 1;\n"
+                   "}\n")
+    exe = tmp_path / "use"
+    lib_dir = os.path.join(ROOT, "paper_2403_17312_b200")
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    str(src), "-o", str(exe), "-L", lib_dir, "-lskv_b200", f"-Wl,-rpath,{lib_dir}"], check=True)
+    assert subprocess.run([str(exe)]).returncode == 0  # swa_window_k is host code: no GPU needed
