@@ -98,3 +98,33 @@ def test_head_sharded_equals_unsharded(tmp_path, world, backend):
     mp.start_processes(_worker, args=(world, _free_port(), backend, str(tmp_path)), nprocs=world,
                        start_method="spawn")
     _check(want, [torch.load(os.path.join(tmp_path, f"rank{r}.pt")) for r in range(world)])
+
+
+def test_head_shard_argument_errors():
+    from paper_2403_17312_b200 import api
+
+    c = api.SwaCache(1, 1, 4, 128, 32, kv_dtype="f16")
+    with pytest.raises(api.ContractViolation):  # heads [6, 10) do not fit in 8
+        c.set_head_shard(6, 8, lambda buf, st: None)
+    with pytest.raises(api.ContractViolation):  # fewer total heads than this shard holds
+        c.set_head_shard(0, 2, lambda buf, st: None)
+    c.set_head_shard(4, 8, lambda buf, st: None)
+    c.set_head_shard(0, 0, None)  # back to unsharded
+
+
+def test_head_shard_reduce_failure_surfaces():
+    """A failing reduce fails the calling entry point (no silent fallback)."""
+    from paper_2403_17312_b200 import api
+
+    B, H, D, s = 1, 4, 128, 16
+    c = api.SwaCache(1, B, H, D, s + 1, kv_dtype="f16")
+    kv = torch.randn(B, s, H, D, device="cuda").half()
+    c.append_tokens(0, 0, 0, kv, kv)
+
+    def broken(buf, st):
+        raise RuntimeError("link down")
+
+    c.set_head_shard(0, 2 * H, broken)
+    with pytest.raises(Exception):
+        c.prefill_seed(0, s, torch.randn(B, H, D, device="cuda").half())
+        torch.cuda.synchronize()
