@@ -397,6 +397,11 @@ def main():
     # there are fewer sequences than GPUs (config 1: strong scaling), else
     # pure batch sharding with no collective (weak scaling).
     head_shards = args.head_shards or (world if B < world else 1)
+    if args.head_shards > 1:
+        # an explicit mesh keeps the per-GPU work of the batch-sharded config:
+        # each batch group owns B x head_shards sequences (config 3 over 8 GPUs
+        # with --head-shards 2: 4 groups x 32 sequences = the BASELINE b=128)
+        B = B * head_shards
     bi, hi, n_bgroups = mesh_coords(world, rank, head_shards)
     groups = head_groups(world, head_shards) if dist else [None]
     head_shard = head_shards > 1
