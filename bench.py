@@ -63,6 +63,28 @@ def timed_window(cfg, W: int, K: int):
     return n_first - s - 1, n_first
 
 
+def mesh_workload(cfg_B: int, world: int, rank: int, head_shards_arg: int) -> dict:
+    """The per-GPU / whole-job workload of a run on `world` ranks.
+
+    world = batch groups x head shards. Default (head_shards_arg 0): head
+    shards only when there are fewer sequences than GPUs (config 1: every rank
+    holds some heads of the same sequence), else pure batch sharding (each
+    rank its own cfg_B sequences, no collective). An explicit --head-shards K
+    with several batch groups keeps the per-GPU work of the batch-sharded
+    config: each group owns cfg_B x K sequences (config 3 over 8 GPUs with
+    K = 2: 4 groups x 32 sequences = BASELINE b=128). With a single batch
+    group the batch stays cfg_B. scaling is "strong" exactly when the job's
+    global batch equals the one-GPU batch (fixed total work), else "weak"."""
+    from paper_2403_17312_b200.shard import mesh_coords
+
+    head_shards = head_shards_arg or (world if cfg_B < world else 1)
+    bi, hi, n_bgroups = mesh_coords(world, rank, head_shards)
+    B = cfg_B * head_shards if (head_shards_arg > 1 and n_bgroups > 1) else cfg_B
+    seqs = n_bgroups * B
+    scaling = "strong" if (world > 1 and seqs == cfg_B) else "weak"
+    return dict(B=B, head_shards=head_shards, bi=bi, hi=hi, n_bgroups=n_bgroups, seqs=seqs, scaling=scaling)
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -208,6 +230,79 @@ def cpu_baseline(cfg, n_mid: int, budget_s: float = 15.0):
             "seconds": t, "cpu_model": cpu_model()}
 
 
+def parity_leg(api, cache, cfg, n: int, step_inputs, out, H: int, B: int, torch):
+    """After every timed region: one more decode step of the benchmarked cache
+    through the product path (skv_swa_decode_step), with sequences {0, B-1} x
+    layers {0, L-1} checked against the CPU oracle (oracle/skv_oracle.c, the
+    checker -- never the thing measured) from the device state right before
+    the step: the pending selection bit-exact (attention.hpp:142-171), the
+    attention output within the north_star tolerance (attention.hpp:183-231)
+    and the folded importance (attention.hpp:219-227, 77-85) within 1e-4.
+    Returns (n after the step, the JSON object)."""
+    import numpy as np
+
+    from oracle import Oracle
+
+    tol = {"f32": 1e-5, "f16": 1e-3, "bf16": 1e-3, "u8": 1e-3}[cfg["kv"]]
+    L = cfg["L"]
+    port = Oracle("port")
+    n1 = n + 1
+    layers, seqs_ = sorted({0, L - 1}), sorted({0, B - 1})
+    pre = {}
+    for l in layers:
+        sel = cache.pending_selection(l, n1, RATIO).cpu().numpy()
+        imp = cache.importance(l, n).cpu().numpy()
+        for b in seqs_:
+            kv = cache.read(l, b, 1, 0, n)[0].double().cpu().numpy()  # [n][2][H][D] as stored
+            pre[(l, b)] = (sel[b], imp[b], kv)
+    q, k, v = step_inputs
+    cache.swa_decode_step(n1, RATIO, q, k, v, out)
+    torch.cuda.synchronize()
+    outs = out.float().cpu().numpy()
+    qd, kd, vd = (t.double().cpu().numpy() for t in (q, k, v))
+    idx_mismatch = ties = 0
+    worst_err = worst_imp = 0.0
+    for l in layers:
+        imp_post = cache.importance(l, n1).cpu().numpy()
+        for b in seqs_:
+            sel, imp, kv = pre[(l, b)]
+            keys = np.zeros((H, n1, 128))
+            vals = np.zeros((H, n1, 128))
+            keys[:, :n] = kv[:, 0].transpose(1, 0, 2)
+            vals[:, :n] = kv[:, 1].transpose(1, 0, 2)
+            kn, vn = kd[l, b], vd[l, b]
+            if cfg["kv"] == "u8":  # engine.hpp:469-483 fake-quant of the appended token
+                def fq(x):
+                    c, sc, z = port.quantize(np.ascontiguousarray(x).reshape(-1), 8, 128)
+                    return port.dequantize(c, 128, sc, z).reshape(x.shape)
+                kn, vn = fq(kn), fq(vn)
+            keys[:, n], vals[:, n] = kn, vn
+            acc = np.zeros((H, n1))
+            acc[0, :n] = imp  # the head sum is what selects; the fold adds aw to it
+            attn, aw, oidx = port.swa_attention(keys, vals, acc, qd[l, b], RATIO, n1)
+            if not np.array_equal(sel, oidx):
+                kk = api.swa_window_k(n1, RATIO)
+                cand = imp[: n1 - kk]
+                kth = np.sort(cand)[::-1][kk - 1]
+                diff = set(int(x) for x in sel) ^ set(int(x) for x in oidx)
+                if all(t < n1 - kk and abs(cand[t] - kth) <= 1e-6 * abs(kth) for t in diff):
+                    ties += 1
+                else:
+                    idx_mismatch += 1
+                continue
+            scale = np.abs(attn).max(axis=-1, keepdims=True)
+            worst_err = max(worst_err, float((np.abs(outs[l, b] - attn) / (tol * (np.abs(attn) + scale))).max()))
+            want = imp.copy()
+            want = np.concatenate([want, [0.0]]) + aw
+            worst_imp = max(worst_imp, float((np.abs(imp_post[b] - want) / (np.abs(want) + 1e-7)).max()))
+    return n1, {"checked": f"sequences {seqs_} x layers {layers} of the benchmarked cache, one extra decode step "
+                           f"at n={n1} through skv_swa_decode_step after the timed region",
+                "oracle": "oracle/skv_oracle.c (fp64 restatement pinned to the compiled reference)",
+                "idx_mismatch": idx_mismatch, "tie_flips": ties, "max_err_over_tol": worst_err,
+                "tol": tol, "importance_max_rel_err": worst_imp, "importance_tol": 1e-4,
+                "ok": idx_mismatch == 0 and worst_err < 1.0 and worst_imp <= 1e-4}
+
+
 def run_reference(args, cfg, rank: int, world: int):
     """--impl reference: the reference CPU implementation on this box's cores."""
     if rank != 0:
@@ -349,6 +444,7 @@ def main():
     ap.add_argument("--variant", default="swa", choices=["swa", "dense", "local", "strided"],
                     help="attention variant (engine.hpp:531-569); dense = the full-KV decode baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the post-run oracle check")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--head-shards", type=int, default=0,
                     help="batch x head mesh: head shards per batch group (0: all ranks when B < world, else 1)")
@@ -388,7 +484,7 @@ def main():
         return
 
     from paper_2403_17312_b200 import api
-    from paper_2403_17312_b200.shard import dist_reducer, head_groups, head_shard_range, max_over_ranks, mesh_coords
+    from paper_2403_17312_b200.shard import dist_reducer, head_groups, head_shard_range, max_over_ranks
 
     L, B, H, s = cfg["L"], cfg["B"], cfg["H"], cfg["s"]
     # batch x head mesh: world = batch groups x head shards. Each batch group
@@ -396,24 +492,20 @@ def main():
     # the fp64 step row once per layer-step. Default: head shards only when
     # there are fewer sequences than GPUs (config 1: strong scaling), else
     # pure batch sharding with no collective (weak scaling).
-    head_shards = args.head_shards or (world if B < world else 1)
-    if args.head_shards > 1:
-        # an explicit mesh keeps the per-GPU work of the batch-sharded config:
-        # each batch group owns B x head_shards sequences (config 3 over 8 GPUs
-        # with --head-shards 2: 4 groups x 32 sequences = the BASELINE b=128)
-        B = B * head_shards
-    bi, hi, n_bgroups = mesh_coords(world, rank, head_shards)
+    mw = mesh_workload(B, world, rank, args.head_shards)
+    B, head_shards, bi, hi, n_bgroups, seqs = (mw[k] for k in ("B", "head_shards", "bi", "hi", "n_bgroups", "seqs"))
     groups = head_groups(world, head_shards) if dist else [None]
     head_shard = head_shards > 1
     b0 = bi * B
     if head_shard:
         h0, H = head_shard_range(cfg["H"], head_shards, hi)
-    seqs = n_bgroups * B  # sequences decoded by the whole job per step
     W, K = args.warmup, args.steps
-    if not args.no_centre:
-        W, _ = timed_window(cfg, W, K)
+    # centring (default): untimed context steps first, so the K timed steps sit
+    # on the middle of the config's decode; the requested W warm-up steps
+    # follow them unchanged
+    prep = 0 if args.no_centre else timed_window(cfg, W, K)[0] - W
     e2e_steps = 0 if (args.no_e2e or args.profile_only) else max(3, min(K, 50))
-    ncap = s + W + K + min(K, 10) + e2e_steps + (2 if e2e_steps else 0) + 1
+    ncap = s + prep + W + K + min(K, 10) + e2e_steps + (2 if e2e_steps else 0) + 2
     qdt = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[cfg["q"]]
     cache = api.SwaCache(L, B, H, D, ncap, kv_dtype=cfg["kv"], q_dtype=cfg["q"], device=local)
     cache.set_variant(args.variant)
@@ -472,14 +564,14 @@ def main():
                    "note": "causal dense attention of the prompt per layer (skv_prefill_layer), mean over "
                            "layers 2..L; flops = 4 B H s(s+1)/2 D (the two causal GEMMs; the kernel "
                            "recomputes QK^T once more for the exact row max)"}
-    pool = min(W + K, 8)
+    pool = min(prep + W + K, 8)
     inputs = [tuple(torch.randn((L, B, H, D), generator=g, device="cuda", dtype=qdt) for _ in range(3))
               for _ in range(pool)]
     out = torch.empty((L, B, H, D), device="cuda", dtype=qdt)
     torch.cuda.synchronize()
 
     n = s
-    for i in range(W):
+    for i in range(prep + W):  # context steps, then the W warm-up steps
         n += 1
         q, k, v = inputs[i % pool]
         cache.swa_decode_step(n, RATIO, q, k, v, out)
@@ -500,7 +592,7 @@ def main():
     ev0.record(stream)
     for i in range(K):
         n += 1
-        q, k, v = inputs[(W + i) % pool]
+        q, k, v = inputs[(prep + W + i) % pool]
         cache.swa_decode_step(n, RATIO, q, k, v, out)
     ev1.record(stream)
     torch.cuda.synchronize()
@@ -517,7 +609,7 @@ def main():
     cache.profile(True)
     for i in range(kern_steps):
         n += 1
-        q, k, v = inputs[(W + K + i) % pool]
+        q, k, v = inputs[(prep + W + K + i) % pool]
         cache.swa_decode_step(n, RATIO, q, k, v, out)
     torch.cuda.synchronize()
     kern_ms, kern_n, algo = cache.profile_read()
@@ -569,8 +661,11 @@ def main():
                "path": "skv_swa_decode_step_host (pinned host q/k/v in, out back; 2 layer chunks pipelined over h2d/d2h copy streams)"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile_only:
-        cpu = cpu_baseline(cfg, n_first + K // 2)
+    parity = None
+    if not args.profile_only and not args.no_parity:
+        n, parity = parity_leg(api, cache, cfg, n, inputs[0], out, H, B, torch)
+    if rank == 0 and not args.no_cpu_baseline and not args.profile_only:
+        cpu = cpu_baseline(cfg, n_first + K // 2)  # rank 0's host cores, at every N
 
     traffic = {}
     try:  # DRAM bytes of one attend launch from the committed ncu --set full capture (scripts/profile_round.sh)
@@ -581,15 +676,16 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-            "warmup_requested": args.warmup,
             "ms_per_step": elapsed_ms / K, "higher_is_better": True,
-            "scaling": "strong" if (head_shard and n_bgroups == 1) else "weak",
+            "scaling": mw["scaling"],
             "vs_baseline": None, "dtype": cfg["kv"], "data": "synthetic (torch.randn K/V/q, seeded)",
             "config": {"workload": cfg["name"], "variant": args.variant, "per_gpu_batch": B, "global_batch": seqs, "layers": L,
+                       "context_prep_steps": prep,
                        "heads": H, "head_dim": D, "ratio": RATIO, "n_range": [n_first, n_first + K - 1],
                        "decode_window": (f"timed steps centred on the {cfg['decode']}-step decode "
                                          f"(n = {s + 1}..{s + cfg['decode']}): step cost is linear in n, so the "
-                                         "window's mean is the whole decode's; earlier steps are untimed warm-up")
+                                         "window's mean is the whole decode's; the context_prep_steps decode steps "
+                                         "before the W warm-up steps are untimed state preparation")
                        if cfg.get("decode") and not args.no_centre else "steady state at the config's KV length",
                        "parallelism": (f"batch x{n_bgroups} x head x{head_shards} ({B} sequences, {H} of {cfg['H']} "
                                        "heads per GPU; one fp64 all-reduce of the step row per layer-step within "
@@ -613,7 +709,7 @@ def main():
                          "step_achieved": step_achieved, "step_frac": step_achieved / peak,
                          "step_note": "attend algorithmic bytes of the timed region / timed region "
                                       "(includes select kernels and launch gaps; layers chained with PDL)"},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "prefill": prefill,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "prefill": prefill, "parity": parity,
             "profile_capture": {"n_first": n_first, "attend_algo_bytes_first_step": attend_algo_bytes(cfg, n_first),
                                 "note": "--profile-only: ncu --profile-from-start off sees the timed region only; "
                                         "attend launch i of it is layer i % L of step n_first + i // L"}

@@ -254,6 +254,8 @@ struct StagedState {
 
 // attention.hpp:183-231: same contract and state mutation as the reference
 // (per-head accumulators grow to n and gain w at the selected positions).
+// Indices may come in any order and repeat: every occurrence is one softmax
+// term and adds its own weight, exactly as the reference loops over them.
 inline StepAttentionResult attend_over_indices(AttentionState& state, const Matrix& q_step,
                                                const IndexList& indices) {
     const std::size_t n = state.tokens();
@@ -302,16 +304,21 @@ inline StepAttentionResult swa_attention(AttentionState& state, const Matrix& q_
     return res;
 }
 
-// attention.hpp:91-117: softmax(q k^T / sqrt(D)) v per query row, causal =
-// row i sees keys 0..i; returns (attn, aw). Each row is one attend over its
-// (causal) key range on a one-head fp32 cache: results match the fp64
-// reference within 1e-5 relative. head_dim 128 only (the compiled kernels).
+// attention.hpp:91-117: softmax(q k^T / sqrt(D)) v per query row; returns
+// (attn, aw). The causal mask is aligned to the bottom-right corner as in the
+// reference (:98-103): row i sees keys j <= i + (k.rows - q.rows). Same checks,
+// messages and order as the reference; a causal row with no visible key fails
+// like softmax_rows (matrix.hpp:145). Each row is one attend over its key
+// range on a one-head fp32 cache: results match the fp64 reference within
+// 1e-5 relative. head_dim 128 only (the compiled kernels).
 inline std::pair<Matrix, Matrix> dense_attention(const Matrix& q, const Matrix& k, const Matrix& v, bool causal) {
-    require(q.cols == k.cols && k.rows == v.rows && k.cols == v.cols, "dense_attention: shape mismatch");
-    require(!causal || q.rows <= k.rows, "dense_attention: causal needs rows <= keys");
+    require(q.cols == k.cols && k.cols == v.cols, "dense_attention: head_dim mismatch");
+    require(k.rows == v.rows, "dense_attention: key/value length mismatch");
+    require(q.rows > 0 && k.rows > 0, "dense_attention: empty input");
     const std::size_t sq = q.rows, sk = k.rows, D = q.cols;
+    const std::ptrdiff_t off = static_cast<std::ptrdiff_t>(sk) - static_cast<std::ptrdiff_t>(sq);
+    require(!causal || off >= 0, "softmax_rows: row has no finite entry");
     std::pair<Matrix, Matrix> res{Matrix(sq, v.cols), Matrix(sq, sk)};
-    if (sq == 0 || sk == 0) return res;
     DeviceCache cache(1, 1, 1, static_cast<int>(D), static_cast<int>(sk), SKV_F32, SKV_F32, 0, true);
     std::vector<float> kf(sk * D), vf(sk * D);
     for (std::size_t i = 0; i < sk * D; ++i) {
@@ -327,7 +334,7 @@ inline std::pair<Matrix, Matrix> dense_attention(const Matrix& q, const Matrix& 
     didx.upload(idx.data(), sk * 4);
     std::vector<float> qf(D), out(D), w(sk);
     for (std::size_t r = 0; r < sq; ++r) {
-        const std::size_t n = causal ? r + 1 : sk;
+        const std::size_t n = causal ? r + 1 + static_cast<std::size_t>(off) : sk;
         for (std::size_t d = 0; d < D; ++d) qf[d] = static_cast<float>(q.at(r, d));
         dq.upload(qf.data(), D * 4);
         cache.attend_over_indices(0, static_cast<int>(n), didx.as<int32_t>(), static_cast<int>(n), dq.get(),

@@ -133,8 +133,10 @@ skv_status skv_swa_decode_step_host(skv_cache* cache, int n, double r, const voi
                                     const void* k_host, const void* v_host, void* out_host,
                                     void* stream);
 
-/* attend_over_indices (attention.hpp:183-231) with caller-chosen ascending
- * indices (device int32 [B][m], each < n); importance[idx] += w. */
+/* attend_over_indices (attention.hpp:183-231) with caller-chosen indices
+ * (device int32 [B][m], each < n, any order, repeats allowed: each occurrence
+ * is one softmax term and adds its own weight, importance[idx] += w, as the
+ * reference loops over them). w_out holds the weights per occurrence. */
 skv_status skv_attend_over_indices(skv_cache* cache, int layer, int n, const int32_t* idx,
                                    int m, const void* q, void* out, float* w_out, void* stream);
 
@@ -173,6 +175,12 @@ skv_status skv_cache_set_variant(skv_cache* cache, int variant, int stride);
 /* Selection size m (and its window k) of a step at length n for the cache's
  * variant: what idx_out / w_out of skv_swa_decode_layer hold. */
 skv_status skv_selection_size(const skv_cache* cache, int n, double r, int32_t* m, int32_t* k);
+/* The selection the next decode step of `layer` will attend at length n
+ * with ratio r (SparseSelection::all(), attention.hpp:31-38), made by the
+ * previous step's select kernel: idx_out [B][m] int32 ascending (any memory),
+ * *m_out = m. SKV_ERR_CONTRACT when no selection for (n, r) is pending. */
+skv_status skv_pending_selection(const skv_cache* cache, int layer, int n, double r, int32_t* idx_out,
+                                 int32_t* m_out, void* stream);
 /* attention_sparsity(new_aw_row, 0.01) (attention.hpp:275-310) of each
  * sequence's last decode step of `layer`; dst [nb] fp64 (host or device). */
 skv_status skv_sparsity_get(const skv_cache* cache, int layer, int b0, int nb, double* dst, void* stream);

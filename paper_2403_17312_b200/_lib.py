@@ -93,6 +93,7 @@ def _declare(lib):
         "skv_cache_set_head_shard": (I, [P, I, I, REDUCE_FN, P]),
         "skv_selection_size": (I, [P, I, D, P, P]),
         "skv_sparsity_get": (I, [P, I, I, I, P, P]),
+        "skv_pending_selection": (I, [P, I, I, D, P, P, P]),
         "skv_ledger_set": (I, [P, I, I, I, I, P, P]),
         "skv_ledger_get": (I, [P, I, I, I, I, P, P]),
         "skv_step_actions": (I, [P, I, I, P, I, I, I, P, P, P]),

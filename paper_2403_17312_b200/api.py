@@ -338,7 +338,8 @@ class SwaCache:
                                              C.c_void_p(out.data_ptr()), s))
         return out
 
-    # attend_over_indices (attention.hpp:183-231)
+    # attend_over_indices (attention.hpp:183-231): any order, duplicates allowed
+    # (each occurrence is one softmax term and adds its weight, as in the reference)
     def attend_over_indices(self, layer: int, n: int, idx: torch.Tensor, q: torch.Tensor,
                             return_weights: bool = False):
         idx = idx.to(torch.int32).contiguous()
@@ -363,6 +364,15 @@ class SwaCache:
         m, k = C.c_int32(), C.c_int32()
         check(lib().skv_selection_size(self._h, n, r, C.byref(m), C.byref(k)))
         return m.value, k.value
+
+    def pending_selection(self, layer: int, n: int, r: float) -> torch.Tensor:
+        """SparseSelection::all() the next decode step of `layer` attends at
+        (n, r): int32 [B, m] ascending (selected one step ahead)."""
+        m, _ = self.selection_size(n, r)
+        out = torch.empty((self.batch, max(m, 1)), dtype=torch.int32, device=self.dev)
+        mo = C.c_int32()
+        check(lib().skv_pending_selection(self._h, layer, n, r, _ptr(out), C.byref(mo), _stream(out)))
+        return out[:, :mo.value]
 
     def sparsity(self, layer: int) -> torch.Tensor:
         # attention_sparsity of each sequence's last step row (attention.hpp:275-310)
@@ -444,17 +454,25 @@ class SwaCache:
 
 # ---- attention.hpp:91-117 ---------------------------------------------------
 def dense_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal: bool):
-    """softmax(q k^T / sqrt(D)) v per query row (causal: row i sees keys
-    0..i) -> (attn [sq, D], aw [sq, sk]) fp32, like the reference's pair.
-    Each row is one attend over its key range on a one-head fp32 cache
-    (head_dim 128); for the batched causal prefill of a cache use
+    """softmax(q k^T / sqrt(D)) v per query row -> (attn [sq, D], aw [sq, sk])
+    fp32, like the reference's pair (attention.hpp:91-117). The causal mask is
+    aligned to the bottom-right corner as in the reference (:98-103): row i
+    sees keys j <= i + (sk - sq). Same checks and messages as the reference,
+    in its order; a causal row with no visible key fails like softmax_rows
+    (matrix.hpp:145). Each row is one attend over its key range on a one-head
+    fp32 cache (head_dim 128); for the batched causal prefill of a cache use
     SwaCache.prefill_layer (tensor cores)."""
     sq, D = q.shape
-    sk = k.shape[0]
-    if k.shape != (sk, D) or v.shape != (sk, D):
-        raise ContractViolation("dense_attention: shape mismatch")
-    if causal and sq > sk:
-        raise ContractViolation("dense_attention: causal needs rows <= keys")
+    sk, Dk = k.shape
+    if D != Dk or v.shape[1] != Dk:
+        raise ContractViolation("dense_attention: head_dim mismatch")
+    if v.shape[0] != sk:
+        raise ContractViolation("dense_attention: key/value length mismatch")
+    if sq == 0 or sk == 0:
+        raise ContractViolation("dense_attention: empty input")
+    off = sk - sq
+    if causal and off < 0:
+        raise ContractViolation("softmax_rows: row has no finite entry")
     dev = q.device
     cache = SwaCache(1, 1, 1, D, sk, kv_dtype="f32", device=dev.index, out_f32=True)
     f = lambda t: t.to(device=dev, dtype=torch.float32).contiguous()  # noqa: E731
@@ -464,7 +482,7 @@ def dense_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal: b
     aw = torch.zeros((sq, sk), dtype=torch.float32, device=dev)
     qf = f(q)
     for r in range(sq):
-        n = r + 1 if causal else sk
+        n = r + 1 + off if causal else sk
         out, w = cache.attend_over_indices(0, n, idx[:n], qf[r].reshape(1, 1, D), return_weights=True)
         attn[r] = out[0, 0]
         aw[r, :n] = w[0, 0]

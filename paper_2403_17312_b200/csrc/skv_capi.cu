@@ -149,6 +149,7 @@ struct skv_cache {
     uint64_t* gkeys = nullptr;  // [L][B][Ncap] top-k keys of long contexts (lazily)
     int* gtok = nullptr;        // [B][H][Ncap] attend token lists of long selections (lazily)
     float* gwts = nullptr;      // [B][H][Ncap] their logits / weights
+    double* frow = nullptr;     // [B][Ncap] step-row scratch of attend_over_indices with unsorted / repeated indices
     // whole-step decode with separate select kernels: the layers' fold+select
     // launches are collected and issued as one batched launch after the
     // step's attends (they only feed the next step), instead of one select
@@ -296,6 +297,7 @@ skv_status skv_cache_destroy(skv_cache* c) {
     cudaFree(c->gkeys);
     cudaFree(c->gtok);
     cudaFree(c->gwts);
+    cudaFree(c->frow);
     for (auto* v : {&c->ev_in, &c->ev_comp, &c->ev_out})
         for (cudaEvent_t e : *v) cudaEventDestroy(e);
     if (c->h2d) cudaStreamDestroy(c->h2d);
@@ -694,6 +696,10 @@ skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok
         SKV_CUDA(cudaEventRecord(e0, st));
         pdl = false;
     }
+    // Long selections share one [B][G][Ncap] token-list / weight scratch
+    // across layers: a PDL-overlapped predecessor could still be using it,
+    // so such launches wait for the previous grid to finish.
+    if (gmem) pdl = false;
     SKV_CUDA(launch_attend(*dl, p, grid_g, smem, pdl, st));
     c->algo_bytes += attend_algo_bytes(c, m, append);
     c->attend_launches += 1;
@@ -1005,6 +1011,8 @@ static skv_status decode_layers(skv_cache* c, int l0, int l1, int n, double r, c
     c->defer_select = false;
     c->in_step = false;
     if (status != SKV_OK || c->deferred.empty()) {
+        // a failed step leaves its deferred selections uncomputed: drop them
+        for (const auto& d : c->deferred) c->pend_n[d.first] = -1;
         c->deferred.clear();
         return status;
     }
@@ -1023,8 +1031,13 @@ static skv_status decode_layers(skv_cache* c, int l0, int l1, int n, double r, c
     p.ls_idx = static_cast<long long>(c->d.batch) * c->d.capacity;
     p.ls_sp = c->d.batch;
     p.pdl_wait = 0;
+    const std::vector<std::pair<int, skvd::SelectParams>> pending = std::move(c->deferred);
     c->deferred.clear();
-    SKV_CUDA(launch_select(p, c->d.batch, false, st, cnt));
+    const cudaError_t le = launch_select(p, c->d.batch, false, st, cnt);
+    if (le != cudaSuccess) {
+        for (const auto& d : pending) c->pend_n[d.first] = -1;
+        return fail(SKV_ERR_CUDA, "decode_step: batched select launch: %s", cudaGetErrorString(le));
+    }
     return SKV_OK;
 }
 
@@ -1121,24 +1134,53 @@ skv_status skv_attend_over_indices(skv_cache* c, int layer, int n, const int32_t
     SKV_REQUIRE(idx && q && out, "attend_over_indices: null argument");
     DeviceGuard guard(c->d.device);
     const cudaStream_t st = as_stream(stream);
-    // The reference validates every index (attention.hpp:186-192); the
-    // importance fold additionally needs them unique (ascending, as sel.all()).
+    // The reference validates every index (attention.hpp:186-192). Indices
+    // may come in any order and repeat (the reference loops over them as
+    // given): each occurrence is its own softmax term and adds its own weight.
     std::vector<int32_t> h(static_cast<size_t>(c->d.batch) * m);
     SKV_CUDA(cudaMemcpyAsync(h.data(), idx, h.size() * 4, cudaMemcpyDefault, st));
     SKV_CUDA(cudaStreamSynchronize(st));
+    bool ascending = true;
     for (int b = 0; b < c->d.batch; ++b)
         for (int i = 0; i < m; ++i) {
             const int32_t t = h[static_cast<size_t>(b) * m + i];
             SKV_REQUIRE(t >= 0 && t < n, "attend_over_indices: index out of range");
-            SKV_REQUIRE(i == 0 || t > h[static_cast<size_t>(b) * m + i - 1],
-                        "attend_over_indices: indices must be strictly ascending");
+            if (i > 0 && t <= h[static_cast<size_t>(b) * m + i - 1]) ascending = false;
         }
     int G = 0;
     FoldSpec fold;
     fold.apply = 1;  // acc[idx] += w (attention.hpp:219-227)
     fold.sp_n = n;
-    return launch_attend_c(c, layer, n, m, idx, m, false, q, nullptr, nullptr, out, nullptr, w_out, false, st, &G,
-                           fold);
+    if (ascending)  // unique positions: the attend tail / select kernel folds them in place
+        return launch_attend_c(c, layer, n, m, idx, m, false, q, nullptr, nullptr, out, nullptr, w_out, false, st,
+                               &G, fold);
+    // any order / repeats: attend without the fold, then scatter the per-
+    // position head sums into the step row with fp64 atomics and fold that
+    if (skv_status e = launch_attend_c(c, layer, n, m, idx, m, false, q, nullptr, nullptr, out, nullptr, w_out, false,
+                                       st, &G, FoldSpec{}))
+        return e;
+    if (!c->frow) {
+        const size_t bytes = static_cast<size_t>(c->d.batch) * c->d.capacity * 8;
+        if (cudaMalloc(reinterpret_cast<void**>(&c->frow), bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(SKV_ERR_OOM, "attend_over_indices: cannot allocate %zu bytes of step-row scratch", bytes);
+        }
+        c->device_bytes += bytes;
+    }
+    const size_t lt = static_cast<size_t>(layer) * c->d.batch;
+    const double* ws = nullptr;
+    if (c->reduce) {  // head shards: the per-position head sums are summed across the shards first
+        if (skv_status e = launch_select_c(c, layer, 1, idx, m, m, G, -1, 0, 0.0, false, st, 0, c->xbuf, nullptr))
+            return e;
+        if (skv_status e = c->reduce(c->xbuf, static_cast<size_t>(c->d.batch) * m, st, c->reduce_user))
+            return fail(e, "head-shard reduce failed (%d)", static_cast<int>(e));
+        ws = c->xbuf;
+    }
+    SKV_CUDA(launch_scatter_fold(c->imp + lt * c->d.capacity, c->d.capacity,
+                                 c->wpart + lt * c->d.heads * c->d.capacity, G, m, idx, m, ws, n, c->sparsity + lt,
+                                 c->frow, c->d.batch, st));
+    c->pend_n[layer] = -1;  // importance changed: any pending selection is stale
+    return SKV_OK;
 }
 
 skv_status skv_swa_select(const double* importance, int batch, int64_t ld, int n, double r, int32_t* idx_out,
@@ -1158,7 +1200,10 @@ skv_status skv_swa_select(const double* importance, int batch, int64_t ld, int n
     }
     // long rows: the candidates' keys go to a stream-ordered scratch
     // ([batch][ld], the importance layout) instead of shared memory
-    const bool long_row = !dense && static_cast<size_t>(n - k) * 8 + 8192 > 220 * 1024;
+    int dev = 0, max_smem = 0;
+    SKV_CUDA(cudaGetDevice(&dev));
+    SKV_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    const bool long_row = !dense && static_cast<size_t>(n - k) * 8 + 8192 > static_cast<size_t>(max_smem);
     uint64_t* gkeys = nullptr;
     if (long_row && cudaMallocAsync(reinterpret_cast<void**>(&gkeys), static_cast<size_t>(batch) * ld * 8,
                                     as_stream(stream)) != cudaSuccess) {
@@ -1177,8 +1222,9 @@ skv_status skv_swa_select(const double* importance, int batch, int64_t ld, int n
     p.idx = idx_out;
     p.idx_ld = m;
     p.variant = SKV_VARIANT_SWA;
-    SKV_CUDA(launch_select(p, batch, false, as_stream(stream)));
-    if (gkeys) SKV_CUDA(cudaFreeAsync(gkeys, as_stream(stream)));
+    const cudaError_t le = launch_select(p, batch, false, as_stream(stream));
+    if (gkeys) cudaFreeAsync(gkeys, as_stream(stream));  // freed on the failure path too
+    if (le != cudaSuccess) return fail(SKV_ERR_CUDA, "swa_select: %s", cudaGetErrorString(le));
     return SKV_OK;
 }
 
@@ -1310,6 +1356,21 @@ skv_status skv_selection_size(const skv_cache* c, int n, double r, int32_t* m, i
     if (skv_status e = step_shape(c, n, r, &s)) return e;
     if (m) *m = s.m;
     if (k) *k = s.k;
+    return SKV_OK;
+}
+
+skv_status skv_pending_selection(const skv_cache* c, int layer, int n, double r, int32_t* idx_out, int32_t* m_out,
+                                 void* stream) {
+    SKV_REQUIRE(c != nullptr && idx_out != nullptr, "pending selection: null argument");
+    SKV_REQUIRE(layer >= 0 && layer < c->d.layers, "KvLedger: layer out of range");
+    SKV_REQUIRE(c->pend_n[layer] == n && c->pend_r[layer] == r,
+                "pending selection: no selection was made for this (n, r) on this layer");
+    StepShape s;
+    if (skv_status e = step_shape(c, n, r, &s)) return e;
+    DeviceGuard guard(c->d.device);
+    SKV_CUDA(cudaMemcpy2DAsync(idx_out, static_cast<size_t>(s.m) * 4, layer_idx(c, layer), c->d.capacity * 4,
+                               static_cast<size_t>(s.m) * 4, c->d.batch, cudaMemcpyDefault, as_stream(stream)));
+    if (m_out) *m_out = s.m;
     return SKV_OK;
 }
 

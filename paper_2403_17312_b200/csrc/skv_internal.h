@@ -16,6 +16,9 @@ namespace skv_impl {
 void count_launch();
 
 cudaError_t launch_select(const skvd::SelectParams& p, int batch, bool pdl, cudaStream_t st, int layers = 1);
+cudaError_t launch_scatter_fold(double* imp, long long imp_ld, const float* wpart, int G, int m, const int* tok,
+                                long long tok_ld, const double* wsum, int n, double* sparsity, double* rows, int batch,
+                                cudaStream_t st);
 cudaError_t launch_ledger(const skvd::LedgerParams& p, int batch, bool pdl, cudaStream_t st);
 cudaError_t launch_transpose_kv_weights(const void* wk, const void* wv, void* bt, int h, cudaStream_t st);
 cudaError_t launch_move(const skvd::MoveParams& p, int batch, int max_tokens, bool pdl, cudaStream_t st);

@@ -239,6 +239,63 @@ __global__ void __launch_bounds__(kSelectThreads) swa_select_kernel(const Select
     fold_and_select<kSelectThreads, 1>(q, blockIdx.x, threadIdx.x, s, keys, scratch);
 }
 
+// attend_over_indices' accumulator update for an arbitrary index list (any
+// order, repeats; attention.hpp:219-227): every occurrence adds its weight.
+// One CTA per sequence: the head-summed step row new_aw_row (length n, zeros
+// off-selection) is scattered into a scratch row with fp64 atomics, then
+// added to the importance, and attention_sparsity (attention.hpp:275-310) of
+// that row is recorded.
+__global__ void __launch_bounds__(256) scatter_fold_kernel(double* imp, long long imp_ld, const float* wpart, int G,
+                                                           int m, const int* tok, long long tok_ld,
+                                                           const double* wsum, int n, double* sparsity,
+                                                           double* rows) {
+    constexpr int NT = 256;
+    __shared__ double red_max[NT / 32];
+    __shared__ int red_cnt[NT / 32];
+    const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double* row = rows + static_cast<size_t>(b) * imp_ld;
+    double* im = imp + static_cast<size_t>(b) * imp_ld;
+    for (int t = tid; t < n; t += NT) row[t] = 0.0;
+    __syncthreads();
+    for (int pos = tid; pos < m; pos += NT) {
+        double v = 0.0;
+        if (wsum) {
+            v = wsum[static_cast<size_t>(b) * m + pos];
+        } else {
+            for (int g = 0; g < G; ++g) v += static_cast<double>(wpart[(static_cast<size_t>(b) * G + g) * m + pos]);
+        }
+        atomicAdd(row + tok[static_cast<size_t>(b) * tok_ld + pos], v);
+    }
+    __syncthreads();
+    double mx = 0.0;
+    for (int t = tid; t < n; t += NT) {
+        const double v = row[t];
+        im[t] += v;
+        mx = v > mx ? v : mx;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, mx, off);
+        mx = o > mx ? o : mx;
+    }
+    if (lane == 0) red_max[warp] = mx;
+    __syncthreads();
+    mx = 0.0;
+    for (int w = 0; w < NT / 32; ++w) mx = red_max[w] > mx ? red_max[w] : mx;
+    const double thr = 0.01 * mx;
+    int below = 0;
+    for (int t = tid; t < n; t += NT) below += row[t] < thr;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) below += __shfl_xor_sync(0xffffffffu, below, off);
+    if (lane == 0) red_cnt[warp] = below;
+    __syncthreads();
+    if (tid == 0) {
+        int cnt = 0;
+        for (int w = 0; w < NT / 32; ++w) cnt += red_cnt[w];
+        sparsity[b] = static_cast<double>(mx == 0.0 ? n : cnt) / static_cast<double>(n);
+    }
+}
+
 // top_k_indices (matrix.hpp:162-176) per row.
 __global__ void __launch_bounds__(kSelThreads)
     top_k_kernel(const double* __restrict__ v, long long ld, int len, int k, int* __restrict__ out,
@@ -458,6 +515,14 @@ cudaError_t launch_select(const SelectParams& p, int batch, bool pdl, cudaStream
     return e;
 }
 
+cudaError_t launch_scatter_fold(double* imp, long long imp_ld, const float* wpart, int G, int m, const int* tok,
+                                long long tok_ld, const double* wsum, int n, double* sparsity, double* rows, int batch,
+                                cudaStream_t st) {
+    scatter_fold_kernel<<<batch, 256, 0, st>>>(imp, imp_ld, wpart, G, m, tok, tok_ld, wsum, n, sparsity, rows);
+    count_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_ledger(const LedgerParams& p, int batch, bool pdl, cudaStream_t st) {
     const size_t smem = static_cast<size_t>(p.existing > 0 ? p.existing : 0) * 2 + 16;
     cudaError_t e = cudaFuncSetAttribute(ledger_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -506,10 +571,13 @@ cudaError_t launch_transpose_kv_weights(const void* wk, const void* wv, void* bt
 
 cudaError_t launch_top_k(const double* v, int batch, long long ld, int len, int k, int* out,
                          cudaStream_t st) {
-    const bool long_row = static_cast<size_t>(len) * 8 + 8192 > 220 * 1024;
+    int dev = 0, max_smem = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e != cudaSuccess) return e;
+    const bool long_row = static_cast<size_t>(len) * 8 + 8192 > static_cast<size_t>(max_smem);
     const size_t smem = align_up(sizeof(TopkSmem<kSelThreads>), 16) + (long_row ? 0 : static_cast<size_t>(len) * 8);
     uint64_t* gkeys = nullptr;
-    cudaError_t e = cudaSuccess;
     if (long_row) {
         e = cudaMallocAsync(reinterpret_cast<void**>(&gkeys), static_cast<size_t>(batch) * ld * 8, st);
         if (e != cudaSuccess) return e;

@@ -96,20 +96,82 @@ int main() {
                 acc_err = std::max(acc_err, std::abs(ref.attention_accum[h][i] - dev.attention_accum[h][i]));
         CHECK(acc_err <= 1e-5, "accumulators step %d err %g", step, acc_err);
     }
-    // dense_attention (attention.hpp:91-117): causal and full, fp32 device vs fp64
-    for (bool causal : {true, false}) {
-        const std::size_t rows = 70, Dd = 128;
-        Matrix qm(rows, Dd), km(rows, Dd), vm(rows, Dd);
-        for (double& x : qm.data) x = static_cast<float>(rng.normal() * 0.5);
-        for (double& x : km.data) x = static_cast<float>(rng.normal());
-        for (double& x : vm.data) x = static_cast<float>(rng.normal());
-        const auto a = dense_attention(qm, km, vm, causal);
-        const auto b = b200::dense_attention(qm, km, vm, causal);
-        const double e1 = rel_err(b.first, a.first);
-        double e2 = 0;
-        for (std::size_t i = 0; i < a.second.data.size(); ++i)
-            e2 = std::max(e2, std::abs(a.second.data[i] - b.second.data[i]));
-        CHECK(e1 <= 1e-5 && e2 <= 1e-5, "dense_attention causal=%d attn %g aw %g", causal, e1, e2);
+    // dense_attention (attention.hpp:91-117): causal (bottom-right aligned,
+    // :98-103) and full, square and non-square, fp32 device vs fp64
+    for (bool causal : {true, false})
+        for (std::size_t sq : {1, 17, 70})
+            for (std::size_t sk : {70, 128}) {
+                const std::size_t Dd = 128;
+                Matrix qm(sq, Dd), km(sk, Dd), vm(sk, Dd);
+                for (double& x : qm.data) x = static_cast<float>(rng.normal() * 0.5);
+                for (double& x : km.data) x = static_cast<float>(rng.normal());
+                for (double& x : vm.data) x = static_cast<float>(rng.normal());
+                const auto a = dense_attention(qm, km, vm, causal);
+                const auto b = b200::dense_attention(qm, km, vm, causal);
+                const double e1 = rel_err(b.first, a.first);
+                double e2 = 0;
+                for (std::size_t i = 0; i < a.second.data.size(); ++i)
+                    e2 = std::max(e2, std::abs(a.second.data[i] - b.second.data[i]));
+                CHECK(e1 <= 1e-5 && e2 <= 1e-5, "dense_attention causal=%d sq=%zu sk=%zu attn %g aw %g", causal, sq,
+                      sk, e1, e2);
+            }
+    // dense_attention contract: empty input and a causal row with no key throw
+    // the reference's ContractViolation
+    {
+        const Matrix e0(0, 128), k1(5, 128), q9(9, 128);
+        for (int which = 0; which < 3; ++which) {
+            int ref_threw = 0, dev_threw = 0;
+            const Matrix& qq = which == 2 ? q9 : (which == 0 ? e0 : k1);
+            const Matrix& kk = which == 1 ? e0 : k1;
+            const Matrix& vv = which == 1 ? e0 : k1;
+            try {
+                dense_attention(qq, kk, vv, true);
+            } catch (const ContractViolation&) {
+                ref_threw = 1;
+            }
+            try {
+                b200::dense_attention(qq, kk, vv, true);
+            } catch (const ContractViolation&) {
+                dev_threw = 1;
+            }
+            CHECK(ref_threw == 1 && dev_threw == 1, "dense_attention contract case %d: ref %d dev %d", which,
+                  ref_threw, dev_threw);
+        }
+    }
+    // attend_over_indices (attention.hpp:183-231) with unsorted and repeated
+    // indices: every occurrence is a softmax term and adds its own weight
+    for (int rep = 0; rep < 6; ++rep) {
+        AttentionState ra(H, D), da(H, D);
+        const std::size_t nt = 90 + rng.integer(60);
+        for (std::size_t t = 0; t < nt; ++t) {
+            for (double& x : kr.data) x = static_cast<float>(rng.normal());
+            for (double& x : vr.data) x = static_cast<float>(rng.normal());
+            ra.append_token(kr, vr);
+            da.append_token(kr, vr);
+        }
+        for (std::size_t h = 0; h < H; ++h) {
+            ra.attention_accum[h].assign(nt - 1 - rep % 3, 0.0);
+            for (double& a : ra.attention_accum[h]) a = rng.uniform();
+            da.attention_accum[h] = ra.attention_accum[h];
+        }
+        IndexList idx;
+        const std::size_t m = 5 + rng.integer(40);
+        for (std::size_t i = 0; i < m; ++i) idx.push_back(rng.integer(nt));
+        if (rep % 2 == 0) idx.push_back(idx.front());  // a guaranteed repeat
+        for (double& x : q.data) x = static_cast<float>(rng.normal());
+        const StepAttentionResult a = attend_over_indices(ra, q, idx);
+        const StepAttentionResult b = b200::attend_over_indices(da, q, idx);
+        const double e = rel_err(b.attn, a.attn);
+        double acc_err = 0, row_err = 0;
+        for (std::size_t h = 0; h < H; ++h) {
+            CHECK(ra.attention_accum[h].size() == da.attention_accum[h].size(), "acc size rep %d", rep);
+            for (std::size_t i = 0; i < ra.attention_accum[h].size(); ++i)
+                acc_err = std::max(acc_err, std::abs(ra.attention_accum[h][i] - da.attention_accum[h][i]));
+        }
+        for (std::size_t i = 0; i < a.new_aw_row.size(); ++i)
+            row_err = std::max(row_err, std::abs(a.new_aw_row[i] - b.new_aw_row[i]));
+        CHECK(e <= 1e-5 && acc_err <= 1e-5 && row_err <= 1e-5 && a.new_aw_row.size() == b.new_aw_row.size(),
+              "attend_over_indices unsorted/repeated rep %d: attn %g acc %g row %g", rep, e, acc_err, row_err);
     }
     // step_actions (scheduler.hpp:320-381) on the reference KvLedger / SchedulePlan
     for (int rep = 0; rep < 40; ++rep) {

@@ -25,6 +25,14 @@ def assert_close(got, ref, tol, what=""):
                              f"got {got[tuple(i)]!r} ref {ref[tuple(i)]!r}; max err {err.max():.3e}")
 
 
+def err_over_tol(got, ref, tol) -> float:
+    """Worst |g - r| / (tol (|r| + max|r|)) over the elements (< 1 passes)."""
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    scale = np.abs(ref).max(axis=-1, keepdims=True) if ref.ndim else abs(ref)
+    return float((np.abs(got - ref) / (tol * (np.abs(ref) + scale))).max())
+
+
 def round_to(x: np.ndarray, dtype: str) -> np.ndarray:
     """Round fp64 data to the device storage dtype and back, so oracle and
     device see identical input values."""

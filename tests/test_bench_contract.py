@@ -37,3 +37,19 @@ def test_algo_bytes_config2():
     H, B, row = 32, 64, 256
     want = B * (H * 128 * 2 * 2 + 2 * H * 128 * 2 + 2 * H * row + 2 * 153 * H * row)
     assert bench.attend_algo_bytes(cfg, 768) == want
+
+
+@pytest.mark.parametrize("cfg_B,world,hs,want_B,want_seqs,want_scaling", [
+    (64, 1, 0, 64, 64, "weak"),     # config 2 on one GPU
+    (64, 8, 0, 64, 512, "weak"),    # batch-sharded: each GPU its own 64 sequences
+    (1, 8, 0, 1, 1, "strong"),      # config 1: head shards over 8 GPUs, one sequence
+    (1, 8, 8, 1, 1, "strong"),      # the same mesh named explicitly: same workload
+    (16, 8, 2, 32, 128, "weak"),    # config 3: 4 groups x 32 sequences = b=128
+    (16, 2, 2, 16, 16, "strong"),   # one group over 2 head shards: the 1-GPU batch
+])
+def test_mesh_workload(cfg_B, world, hs, want_B, want_seqs, want_scaling):
+    """the implicit and explicit forms of the same mesh decode the
+    same sequences, and `scaling` follows whether the global batch grew."""
+    for rank in range(world):
+        mw = bench.mesh_workload(cfg_B, world, rank, hs)
+        assert (mw["B"], mw["seqs"], mw["scaling"]) == (want_B, want_seqs, want_scaling)

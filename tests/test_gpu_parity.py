@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 import torch
 
-from skv_testlib import TOL, OracleSeq, assert_close, round_to, selection_flip_is_tie
+from skv_testlib import TOL, OracleSeq, assert_close, err_over_tol, round_to, selection_flip_is_tie
 
 pytestmark = pytest.mark.gpu
 
@@ -141,18 +141,18 @@ def test_attend_over_indices_errors(api):
     with pytest.raises(api.ContractViolation):
         cache.attend_over_indices(0, 8, torch.tensor([[1, 9]], device="cuda"), q)  # index >= n
     with pytest.raises(api.ContractViolation):
-        cache.attend_over_indices(0, 8, torch.tensor([[3, 1]], device="cuda"), q)  # not ascending
-    with pytest.raises(api.ContractViolation):
         cache.attend_over_indices(0, 0, torch.tensor([[0]], device="cuda"), q)  # empty cache
     with pytest.raises(api.ContractViolation):
         cache.attend_over_indices(3, 8, torch.tensor([[0]], device="cuda"), q)  # layer out of range
 
 
 # ------------------------------------------------------------ decode trajectory
-def run_trajectory(api, port, dt, B, H, s, steps, r, seed, q_dt=None, check_every=1, L=1, layer=None):
+def run_trajectory(api, port, dt, B, H, s, steps, r, seed, q_dt=None, check_every=1, L=1, layer=None,
+                   out_f32=None, stats=None):
     """Prefill s tokens, seed the accumulator from the dense last row, then
     `steps` decode steps (append -> select -> attend), all compared to the
-    oracle. Returns the number of tolerated tie flips."""
+    oracle. Returns the number of tolerated tie flips; `stats` (a dict) gets
+    the worst output error as a fraction of its tolerance bound."""
     rng = np.random.default_rng(seed)
     D = 128
     quant = dt == "u8"
@@ -161,9 +161,11 @@ def run_trajectory(api, port, dt, B, H, s, steps, r, seed, q_dt=None, check_ever
     layer = L - 1 if layer is None else layer
     kv = round_to(rng.standard_normal((B, ncap, 2, H, D)), qdt)
     qs = round_to(rng.standard_normal((steps + 1, B, H, D)) * 1.5, qdt)
-    cache = api.SwaCache(L, B, H, D, ncap, kv_dtype=dt, q_dtype=qdt, out_f32=qdt == "bf16")
+    out_f32 = qdt == "bf16" if out_f32 is None else out_f32
+    cache = api.SwaCache(L, B, H, D, ncap, kv_dtype=dt, q_dtype=qdt, out_f32=out_f32)
     cache.append_tokens(layer, 0, 0, cuda(kv[:, :s, 0], TD[qdt]), cuda(kv[:, :s, 1], TD[qdt]))
     seqs = [OracleSeq(port, H, D, ncap, quant) for _ in range(B)]
+    worst = 0.0
     for b in range(B):
         for t in range(s):
             seqs[b].append(t, kv[b, t, 0], kv[b, t, 1])
@@ -194,6 +196,7 @@ def run_trajectory(api, port, dt, B, H, s, steps, r, seed, q_dt=None, check_ever
                 resync.append(b)
                 continue
             assert_close(out[b], attn, TOL[dt], f"attn step {j} seq {b}")
+            worst = max(worst, err_over_tol(out[b], attn, TOL[dt]))
         if resync or (j % check_every == 0) or j == steps - 1:
             imp = cache.importance(layer, n).cpu().numpy()
             for b in range(B):
@@ -207,6 +210,8 @@ def run_trajectory(api, port, dt, B, H, s, steps, r, seed, q_dt=None, check_ever
                 for b in resync:
                     full[b] = seqs[b].importance(n)
                 cache.set_importance(layer, cuda(full))
+    if stats is not None:
+        stats["max_err_over_tol"] = worst
     return flips
 
 
@@ -244,6 +249,28 @@ def test_golden_trajectory_gpu(api, golden):
 def test_decode_trajectory(api, port, dt, B, H, s, steps):
     flips = run_trajectory(api, port, dt, B, H, s, steps, 0.2, seed=sum(map(ord, dt)) * 100 + H)
     assert flips <= max(1, steps * B // 10)
+
+
+def test_decode_trajectory_config4_full_length(api, port):
+    """BASELINE config 4 at its KV length: INT8 KV (fp16 q), OPT-30B heads
+    (H = 56), n = 4096..4098, against the oracle's fake-quantised fp64
+    AttentionState. The INT8 logit runs on FHFMA over codes biased by 1024
+    (skv_device.cuh); the +1024 bias is folded back per token, cancelling
+    about 10 bits of the fp32 dot -- the worst error stays well inside the
+    1e-3 bound."""
+    stats = {}
+    run_trajectory(api, port, "u8", 1, 56, 4095, 3, 0.2, seed=4096, stats=stats)
+    print(f"config4 n=4096 INT8: max err / tol = {stats['max_err_over_tol']:.3f}")
+    assert stats["max_err_over_tol"] < 0.5, stats
+
+
+def test_decode_trajectory_bf16_outputs(api, port):
+    """Config 3 as benchmarked: bf16 cache, bf16 OUTPUTS (no out_f32). bf16
+    rounding of the output (2^-9 of the element) fits the north_star bound
+    |g - r| <= 1e-3 (|r| + max|r|) since max|r| >= |r|."""
+    stats = {}
+    run_trajectory(api, port, "bf16", 2, 40, 1024, 4, 0.2, seed=1313, out_f32=False, stats=stats)
+    assert stats["max_err_over_tol"] < 1.0, stats
 
 
 def test_decode_trajectory_u8_f32_query(api, port):
@@ -518,13 +545,58 @@ def test_long_selection_global_scratch(api, port):
 
 
 @pytest.mark.parametrize("causal", [True, False])
-def test_dense_attention(api, port, causal):
-    """dense_attention (attention.hpp:91-117) through the C ABI vs the oracle:
-    outputs and the full weight matrix within the fp32 tolerance."""
-    rng = np.random.default_rng(17)
-    s, D = 90, 128
-    q, k, v = (rng.standard_normal((s, D)) * sc for sc in (0.5, 1.0, 1.0))
+@pytest.mark.parametrize("sq,sk", [(90, 90), (1, 70), (17, 70), (70, 70), (1, 128), (17, 128), (70, 128)])
+def test_dense_attention(api, port, causal, sq, sk):
+    """dense_attention (attention.hpp:91-117) through the C ABI vs the oracle,
+    square and non-square: the causal mask is bottom-right aligned (:98-103),
+    so one query over a 100-token cache sees every key. Outputs and the full
+    weight matrix within the fp32 tolerance."""
+    rng = np.random.default_rng(17 + sq + sk)
+    D = 128
+    q = rng.standard_normal((sq, D)) * 0.5
+    k, v = rng.standard_normal((sk, D)), rng.standard_normal((sk, D))
     attn, aw = api.dense_attention(cuda(q), cuda(k), cuda(v), causal)
     r_attn, r_aw = port.dense_attention(q, k, v, causal)
     assert_close(attn.cpu().numpy(), r_attn, TOL["f32"], "dense_attention attn")
     np.testing.assert_allclose(aw.cpu().numpy(), r_aw, rtol=1e-5, atol=1e-7)
+
+
+def test_dense_attention_contract(api):
+    """Empty inputs and a causal row without a visible key raise the
+    reference's ContractViolation (attention.hpp:95, matrix.hpp:145)."""
+    z = torch.zeros((0, 128), device="cuda")
+    a = torch.zeros((5, 128), device="cuda")
+    b = torch.zeros((9, 128), device="cuda")
+    for q, k in ((z, a), (a, z), (b, a)):
+        with pytest.raises(api.ContractViolation):
+            api.dense_attention(q, k, k, True)
+
+
+@pytest.mark.parametrize("dt", ["f32", "f16"])
+def test_attend_over_indices_unsorted_repeated(api, port, dt):
+    """attend_over_indices (attention.hpp:183-231) takes any index order and
+    repeats: each occurrence is one softmax term and adds its own weight to
+    the accumulator (acc[idx] += w per occurrence, :219-227). Outputs, weights
+    and the importance fold against the oracle, plus the step's sparsity."""
+    rng = np.random.default_rng(41)
+    B, H, D, n, m = 2, 8, 128, 257, 120
+    kv = round_to(rng.standard_normal((B, n, 2, H, D)), dt)
+    q = round_to(rng.standard_normal((B, H, D)), dt)
+    cache = api.SwaCache(1, B, H, D, n + 4, kv_dtype=dt)
+    cache.append_tokens(0, 0, 0, cuda(kv[:, :, 0], TD[dt]), cuda(kv[:, :, 1], TD[dt]))
+    base = rng.random((B, n))
+    cache.set_importance(0, cuda(base))
+    idx = rng.integers(0, n, size=(B, m)).astype(np.int32)
+    idx[:, 5] = idx[:, 0]  # guaranteed repeats
+    idx[:, 9] = n - 1
+    out, w = cache.attend_over_indices(0, n, cuda(idx), cuda(q, TD[dt]), return_weights=True)
+    imp = cache.importance(0, n).cpu().numpy()
+    sp = cache.sparsity(0).cpu().numpy()
+    for b in range(B):
+        seq = OracleSeq(port, H, D, n)
+        seq.keys[:] = kv[b, :, 0].transpose(1, 0, 2)
+        seq.vals[:] = kv[b, :, 1].transpose(1, 0, 2)
+        attn, aw = port.attend_over_indices(seq.keys, seq.vals, seq.acc, n, q[b], idx[b], n)
+        assert_close(out[b].float().cpu().numpy(), attn, TOL[dt], f"attn b={b}")
+        np.testing.assert_allclose(imp[b] - base[b], aw, rtol=1e-4, atol=1e-7)
+        assert abs(sp[b] - port.attention_sparsity(aw[None])) <= 1.0 / n
