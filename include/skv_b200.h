@@ -74,6 +74,35 @@ skv_status skv_cache_create(const skv_cache_desc* desc, skv_cache** out);
 skv_status skv_cache_destroy(skv_cache* cache);
 skv_status skv_cache_get_desc(const skv_cache* cache, skv_cache_desc* desc, uint64_t* device_bytes);
 
+/* A cache whose device K/V is a PAGED POOL bounded by a KvLedger device
+ * capacity (memsim.hpp:77-215, CostParams::device_capacity): every
+ * (layer, sequence) owns floor(capacity / (L * B * token bytes)) token slots
+ * (at most `capacity` tokens), token bytes = 2 * H * row. With a plan and a
+ * host tier attached (skv_cache_set_plan, skv_cache_enable_host_tier), each
+ * decode step's offloads and deletions free slots and its reloads,
+ * recomputations and the new token (store_new) take them, so a KV larger
+ * than the budget decodes within it. The prompt must be written in order
+ * (skv_cache_write, token t takes slot t) before the first decode step; a
+ * plan is required to decode. The KvLedger capacity check raises
+ * SKV_ERR_OOM with the reference's message. */
+skv_status skv_cache_create_paged(const skv_cache_desc* desc, uint64_t device_capacity, skv_cache** out);
+/* The KvLedger device capacity in bytes for a non-paged cache (default:
+ * unbounded): store_new / reload / restore beyond it fail with SKV_ERR_OOM
+ * (memsim.hpp:193-200). Decode-time accounting runs with a plan attached. */
+skv_status skv_cache_set_capacity(skv_cache* cache, uint64_t device_capacity);
+/* KvLedger::device_bytes / host_bytes (memsim.hpp:86-87) summed over layers
+ * and sequences, the peak device bytes so far and the capacity; synchronises
+ * `stream`. Returns the first failure a kernel reported (SKV_ERR_OOM:
+ * "simulated OOM: device tier needs X bytes, capacity C"; SKV_ERR_CONTRACT:
+ * a gathered token not device-resident, engine.hpp:625-628). Every decode
+ * entry point also returns such a failure on its next call. */
+skv_status skv_ledger_totals(const skv_cache* cache, uint64_t* device_bytes, uint64_t* host_bytes,
+                             uint64_t* peak_device_bytes, uint64_t* capacity, void* stream);
+/* Storage shape: token slots per (layer, sequence), bytes of the device K/V
+ * pool, and bytes of the full [L][B][capacity] K/V it stands for. */
+skv_status skv_cache_storage(const skv_cache* cache, int32_t* slots_per_sequence, uint64_t* kv_pool_bytes,
+                             uint64_t* full_kv_bytes);
+
 /* AttentionState::append_token for tokens [t0, t0+nt) of sequences
  * [b0, b0+nb) (attention.hpp:65-74; fake-quant as engine.hpp:469-483 when
  * kv_dtype is SKV_U8). k, v: device [nb][nt][H][D] in q_dtype. Zeroes the

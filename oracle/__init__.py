@@ -80,6 +80,49 @@ def _p(a: np.ndarray, ct):
 _D, _I64, _U16, _SZ = C.c_double, C.c_int64, C.c_uint16, C.c_size_t
 
 
+class RefLedger:
+    """The reference's own KvLedger (memsim.hpp:77-215), compiled from the
+    unmodified headers (oracle/_ref): driven with the engine's action order
+    (engine.hpp:686-716 then store_new) it is the checker for the device
+    ledger's byte totals and its OutOfDeviceMemory point and message."""
+
+    OPS = {"store_new": 0, "offload": 1, "reload": 2, "erase": 3, "restore": 4}
+
+    def __init__(self, layers: int, capacity: int):
+        if not os.path.exists(REF_SO):
+            raise FileNotFoundError(f"reference build missing: {REF_SO}")
+        lib = self.lib = C.CDLL(REF_SO)
+        lib.ref_ledger_new.restype = C.c_void_p
+        lib.ref_ledger_new.argtypes = [_SZ, C.c_uint64]
+        lib.ref_ledger_free.argtypes = [C.c_void_p]
+        lib.ref_ledger_op.argtypes = [C.c_void_p, C.c_int, _SZ, C.POINTER(_I64), _SZ, C.c_uint64]
+        lib.ref_ledger_bytes.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        lib.ref_ledger_tiers.argtypes = [C.c_void_p, _SZ, _SZ, C.POINTER(C.c_int8)]
+        lib.ref_last_error.restype = C.c_char_p
+        self.h = lib.ref_ledger_new(layers, capacity)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.ref_ledger_free(self.h)
+            self.h = None
+
+    def op(self, name: str, layer: int, tokens, nbytes: int = 0) -> None:
+        t = np.ascontiguousarray(np.asarray(tokens, np.int64).reshape(-1))
+        rc = self.lib.ref_ledger_op(self.h, self.OPS[name], layer, _p(t, _I64), t.size, nbytes)
+        if rc:
+            raise _ERR.get(rc, RuntimeError)(self.lib.ref_last_error().decode())
+
+    def bytes(self):
+        d, h = C.c_uint64(), C.c_uint64()
+        self.lib.ref_ledger_bytes(self.h, C.byref(d), C.byref(h))
+        return d.value, h.value
+
+    def tiers(self, layer: int, ntok: int) -> np.ndarray:
+        out = np.zeros(ntok, np.int8)
+        self.lib.ref_ledger_tiers(self.h, layer, ntok, _p(out, C.c_int8))
+        return out
+
+
 class Oracle:
     def __init__(self, kind: str = "port"):
         if kind not in ("port", "reference"):

@@ -391,4 +391,44 @@ double ref_bench_swa(size_t H, size_t D, size_t n0, double r, size_t items, size
     return b;
 }
 
+// memsim.hpp:77-215: a live reference KvLedger behind an opaque handle, so
+// the tests can drive it with the same action sequence as the device ledger
+// and compare byte totals and the OutOfDeviceMemory point and message.
+void* ref_ledger_new(size_t layers, uint64_t capacity) {
+    skv::KvLedger* l = nullptr;
+    guarded([&] { l = new skv::KvLedger(layers, capacity); });
+    return l;
+}
+void ref_ledger_free(void* h) { delete static_cast<skv::KvLedger*>(h); }
+// op: 0 store_new (each token), 1 offload, 2 reload, 3 erase, 4 restore (each token)
+int ref_ledger_op(void* h, int op, size_t layer, const int64_t* toks, size_t nt, uint64_t bytes) {
+    auto& L = *static_cast<skv::KvLedger*>(h);
+    return guarded([&] {
+        std::vector<std::size_t> t(toks, toks + nt);
+        switch (op) {
+        case 0:
+            for (std::size_t x : t) L.store_new(layer, x, bytes);
+            break;
+        case 1: L.offload(layer, t); break;
+        case 2: L.reload(layer, t); break;
+        case 3: L.erase(layer, t); break;
+        case 4:
+            for (std::size_t x : t) L.restore(layer, x, bytes);
+            break;
+        default: throw std::runtime_error("ref_ledger_op: unknown op");
+        }
+    });
+}
+void ref_ledger_bytes(void* h, uint64_t* device_bytes, uint64_t* host_bytes) {
+    auto& L = *static_cast<skv::KvLedger*>(h);
+    *device_bytes = L.device_bytes();
+    *host_bytes = L.host_bytes();
+}
+// tiers of tokens [0, ntok) of `layer`: -1 not stored, else Tier
+void ref_ledger_tiers(void* h, size_t layer, size_t ntok, int8_t* out) {
+    auto& L = *static_cast<skv::KvLedger*>(h);
+    for (size_t t = 0; t < ntok; ++t)
+        out[t] = L.exists(layer, t) ? static_cast<int8_t>(L.tier(layer, t)) : static_cast<int8_t>(-1);
+}
+
 } // extern "C"

@@ -67,6 +67,10 @@ def _declare(lib):
         "skv_swa_window_k": (SZ, [SZ, D]),
         "skv_swa_keep_count": (SZ, [SZ, D]),
         "skv_cache_create": (I, [P, P]),
+        "skv_cache_create_paged": (I, [P, U64, P]),
+        "skv_cache_set_capacity": (I, [P, U64]),
+        "skv_ledger_totals": (I, [P, P, P, P, P, P]),
+        "skv_cache_storage": (I, [P, P, P, P]),
         "skv_cache_destroy": (I, [P]),
         "skv_cache_get_desc": (I, [P, P, P]),
         "skv_cache_write": (I, [P, I, I, I, I, I, P, P, P]),

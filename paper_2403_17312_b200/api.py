@@ -191,7 +191,11 @@ class SwaCache:
     HBM, fp64 head-summed importance accumulator."""
 
     def __init__(self, layers: int, batch: int, heads: int, head_dim: int, capacity: int,
-                 kv_dtype="f16", q_dtype=None, device: int | None = None, out_f32: bool = False):
+                 kv_dtype="f16", q_dtype=None, device: int | None = None, out_f32: bool = False,
+                 device_capacity: int | None = None):
+        """device_capacity (bytes): a PAGED cache whose device K/V pool is
+        bounded by the KvLedger capacity (skv_cache_create_paged); None: the
+        dense [L][B][capacity] layout."""
         self.layers, self.batch, self.heads, self.head_dim, self.capacity = (
             layers, batch, heads, head_dim, capacity)
         self.kv_code = _code(kv_dtype)
@@ -204,7 +208,10 @@ class SwaCache:
         d = _Desc(layers, batch, heads, head_dim, capacity, self.kv_code, self.q_code, self.device,
                   int(out_f32))
         h = C.c_void_p()
-        check(lib().skv_cache_create(C.byref(d), C.byref(h)))
+        if device_capacity is None:
+            check(lib().skv_cache_create(C.byref(d), C.byref(h)))
+        else:
+            check(lib().skv_cache_create_paged(C.byref(d), int(device_capacity), C.byref(h)))
         self._h = h
 
     def set_head_shard(self, head_offset: int, total_heads: int, reduce=None):
@@ -248,6 +255,22 @@ class SwaCache:
         b = C.c_uint64()
         check(lib().skv_cache_get_desc(self._h, None, C.byref(b)))
         return b.value
+
+    # ---- KvLedger byte accounting (memsim.hpp:77-215)
+    def set_capacity(self, device_capacity: int):
+        check(lib().skv_cache_set_capacity(self._h, int(device_capacity)))
+
+    def ledger_totals(self) -> dict:
+        """device / host / peak device bytes and the capacity; raises the first
+        failure a kernel reported (OutOfDeviceMemory, ContractViolation)."""
+        v = [C.c_uint64() for _ in range(4)]
+        check(lib().skv_ledger_totals(self._h, *[C.byref(x) for x in v], _stream()))
+        return dict(zip(("device_bytes", "host_bytes", "peak_device_bytes", "capacity"), (x.value for x in v)))
+
+    def storage(self) -> dict:
+        sl, pool, full = C.c_int32(), C.c_uint64(), C.c_uint64()
+        check(lib().skv_cache_storage(self._h, C.byref(sl), C.byref(pool), C.byref(full)))
+        return {"slots_per_sequence": sl.value, "kv_pool_bytes": pool.value, "full_kv_bytes": full.value}
 
     def _q(self, t: torch.Tensor, shape) -> torch.Tensor:
         if t.dtype != self.q_dtype or tuple(t.shape) != tuple(shape):

@@ -101,7 +101,8 @@ struct skv_cache {
     skv_cache_desc d{};
     size_t row_bytes = 0;    // one head row of D elements (storage dtype)
     size_t tok_bytes = 0;    // K+V of one token, all heads
-    size_t layer_bytes = 0;  // [B][Ncap] tokens
+    size_t layer_bytes = 0;  // device K/V of one layer: [B][pcap] token slots
+    size_t host_layer_bytes = 0;  // host tier of one layer: [B][Ncap] tokens
     uint8_t* kv = nullptr;
     float2* meta = nullptr;
     double* imp = nullptr;
@@ -117,6 +118,7 @@ struct skv_cache {
     std::vector<const uint8_t*> rec_x;
     std::vector<uint8_t*> rec_wt;
     uint8_t* rec_a = nullptr;  // gathered rows [B*Ncap][h]
+    float* rec_c = nullptr;    // INT8 caches: the GEMM's fp32 K|V rows [B*Ncap][2h] before quantisation
     int2* rec_map = nullptr;   // [B*Ncap] (b, t)
     unsigned* counters = nullptr;  // [L][B] attend-tail arrival counters (zero between launches)
     int* rec_m = nullptr;      // gathered row count
@@ -157,6 +159,25 @@ struct skv_cache {
     bool in_step = false;  // inside skv_swa_decode_step(_host): a whole step's layers
     bool defer_select = false;
     std::vector<std::pair<int, skvd::SelectParams>> deferred;  // (layer, params)
+    // paged store (skv_cache_create_paged): every (layer, sequence) owns pcap
+    // token slots of the device pool; offload / erase free them, reload /
+    // restore / store_new allocate them (ledger_step_kernel)
+    bool paged = false;
+    int pcap = 0;                  // slots per (layer, sequence); the capacity when not paged
+    int* slot = nullptr;           // [L][B][Ncap] token -> slot, -1 not on device
+    int* fq = nullptr;             // [L][B][pcap] free-slot FIFO rings
+    unsigned* fq_ht = nullptr;     // [L][B][2] (head, free count)
+    int* act_slots = nullptr;      // [L][B][4][Ncap] slots of the last action lists
+    int* aux = nullptr;            // [L][B][4] reload split (recycled destinations)
+    // KvLedger byte accounting (memsim.hpp:77-215) and the device status
+    skvd::LedgerTotals* tot = nullptr;
+    unsigned* arrive = nullptr;                // [L]
+    unsigned long long* layer_allocs = nullptr;  // [L]
+    uint64_t cap_bytes = ~0ull;                // KvLedger device_capacity
+    skvd::DevStatus* status = nullptr;         // mapped pinned host memory
+    skvd::DevStatus* status_dev = nullptr;     // its device alias
+    std::vector<int> ident;        // [L][B] prompt high-water mark (tokens written in order from 0)
+    std::vector<char> decoded;     // [L] a decode step ran on this layer
     // measurement
     bool prof = false;
     std::vector<cudaEvent_t> ev;  // start/stop pairs
@@ -172,6 +193,37 @@ struct skv_cache {
 constexpr int kHostChunks = 2;  // layer chunks of the host-buffer step pipeline (2 measured best: 1.08 ms vs 0.97 ms copy bound at config 2)
 
 static size_t out_size(const skv_cache* c) { return c->d.out_f32 ? 4 : dtype_size(c->d.q_dtype); }
+
+// The device status (mapped pinned memory) as an error: the first KvLedger
+// OOM (memsim.hpp:193-200, the reference's message) or residency violation
+// (engine.hpp:625-628) a kernel reported. Sticky, like the reference's throw.
+static skv_status check_status(const skv_cache* c) {
+    if (c == nullptr || c->status == nullptr) return SKV_OK;
+    const volatile skvd::DevStatus* st = c->status;
+    const int code = st->code;
+    if (code <= 0) return SKV_OK;
+    if (code == 2) {
+        if (st->needed > 0)
+            return fail(SKV_ERR_OOM, "simulated OOM: device tier needs %llu bytes, capacity %llu",
+                        static_cast<unsigned long long>(st->needed), static_cast<unsigned long long>(st->capacity));
+        return fail(SKV_ERR_OOM, "device KV pool exhausted: a (layer, sequence) slot pool of layer %d is full at "
+                    "step %lld", st->layer, static_cast<long long>(st->step));
+    }
+    return fail(SKV_ERR_CONTRACT, "decode_step: gathered token not device-resident (layer %d sequence %d token %d)",
+                st->layer, st->seq, st->token);
+}
+
+static skvd::CacheView cache_view(skv_cache* c, int layer) {
+    skvd::CacheView v{};
+    const size_t lt = static_cast<size_t>(layer) * c->d.batch * c->d.capacity;
+    v.kv = c->kv + layer * c->layer_bytes;
+    v.Ncap = c->d.capacity;
+    v.kv_ncap = c->pcap;
+    v.slot = c->paged ? c->slot + lt : nullptr;
+    v.fq_ht = c->paged ? c->fq_ht + static_cast<size_t>(layer) * c->d.batch * 2 : nullptr;
+    v.tot = c->tot;
+    return v;
+}
 
 extern "C" {
 
@@ -200,7 +252,7 @@ size_t skv_swa_keep_count(size_t n, double r) {
     return 2 * k < n ? 2 * k : n;
 }
 
-skv_status skv_cache_create(const skv_cache_desc* desc, skv_cache** out) {
+static skv_status cache_create_impl(const skv_cache_desc* desc, uint64_t paged_capacity, skv_cache** out) {
     SKV_REQUIRE(desc != nullptr && out != nullptr, "skv_cache_create: null argument");
     const skv_cache_desc& d = *desc;
     SKV_REQUIRE(d.layers > 0 && d.batch > 0 && d.heads > 0 && d.capacity > 0,
@@ -221,14 +273,31 @@ skv_status skv_cache_create(const skv_cache_desc* desc, skv_cache** out) {
     // one stored head row; INT8 rows carry their (scale, bias) pair inline
     c->row_bytes = static_cast<size_t>(d.head_dim) * dtype_size(d.kv_dtype) + (d.kv_dtype == SKV_U8 ? 8 : 0);
     c->tok_bytes = 2 * static_cast<size_t>(d.heads) * c->row_bytes;
-    c->layer_bytes = static_cast<size_t>(d.batch) * d.capacity * c->tok_bytes;
+    c->paged = paged_capacity > 0;
+    if (c->paged) {
+        // the KvLedger capacity split evenly over (layer, sequence) slot pools
+        const uint64_t per = paged_capacity / (static_cast<uint64_t>(d.layers) * d.batch * c->tok_bytes);
+        if (per < 1) {
+            delete c;
+            return fail(SKV_ERR_OOM, "simulated OOM: device tier needs %llu bytes, capacity %llu",
+                        static_cast<unsigned long long>(static_cast<uint64_t>(d.layers) * d.batch * c->tok_bytes),
+                        static_cast<unsigned long long>(paged_capacity));
+        }
+        c->pcap = static_cast<int>(std::min<uint64_t>(per, static_cast<uint64_t>(d.capacity)));
+        c->cap_bytes = paged_capacity;
+    } else {
+        c->pcap = d.capacity;
+    }
+    c->layer_bytes = static_cast<size_t>(d.batch) * c->pcap * c->tok_bytes;
+    c->host_layer_bytes = static_cast<size_t>(d.batch) * d.capacity * c->tok_bytes;
     const size_t kv_bytes = c->layer_bytes * d.layers;
     const size_t meta_bytes = 0;  // inline in the INT8 rows
-    const size_t imp_bytes = static_cast<size_t>(d.layers) * d.batch * d.capacity * 8;
-    const size_t wpart_bytes = static_cast<size_t>(d.layers) * d.batch * d.heads * d.capacity * 4;
-    const size_t cnt_bytes = static_cast<size_t>(d.layers) * d.batch * d.capacity * 4;  // selections
-    const size_t tier_bytes = static_cast<size_t>(d.layers) * d.batch * d.capacity;
-    const size_t list_bytes = static_cast<size_t>(d.layers) * d.batch * 4 * d.capacity * 4;
+    const size_t cells = static_cast<size_t>(d.layers) * d.batch * d.capacity;
+    const size_t imp_bytes = cells * 8;
+    const size_t wpart_bytes = cells * d.heads * 4;
+    const size_t cnt_bytes = cells * 4;  // selections
+    const size_t tier_bytes = cells;
+    const size_t list_bytes = cells * 4 * 4;
     const size_t acnt_bytes = static_cast<size_t>(d.layers) * d.batch * 4 * 4;
     const size_t sp_bytes = static_cast<size_t>(d.layers) * d.batch * 8;
     const size_t ctr_bytes = static_cast<size_t>(d.layers) * d.batch * 4;
@@ -241,18 +310,39 @@ skv_status skv_cache_create(const skv_cache_desc* desc, skv_cache** out) {
         c->device_bytes += bytes;
         return true;
     };
-    if (!alloc(reinterpret_cast<void**>(&c->kv), kv_bytes) ||
-        !alloc(reinterpret_cast<void**>(&c->meta), meta_bytes) ||
-        !alloc(reinterpret_cast<void**>(&c->imp), imp_bytes) ||
-        !alloc(reinterpret_cast<void**>(&c->wpart), wpart_bytes) ||
-        !alloc(reinterpret_cast<void**>(&c->idx), cnt_bytes) ||
-        !alloc(reinterpret_cast<void**>(&c->tiers), tier_bytes) ||
-        !alloc(reinterpret_cast<void**>(&c->act_lists), list_bytes) ||
-        !alloc(reinterpret_cast<void**>(&c->act_counts), acnt_bytes) ||
-        !alloc(reinterpret_cast<void**>(&c->sparsity), sp_bytes) ||
-        !alloc(reinterpret_cast<void**>(&c->counters), ctr_bytes)) {
-        const uint64_t want = kv_bytes + meta_bytes + imp_bytes + wpart_bytes + cnt_bytes + tier_bytes + list_bytes +
-                              acnt_bytes;
+    bool ok = alloc(reinterpret_cast<void**>(&c->kv), kv_bytes) &&
+              alloc(reinterpret_cast<void**>(&c->meta), meta_bytes) &&
+              alloc(reinterpret_cast<void**>(&c->imp), imp_bytes) &&
+              alloc(reinterpret_cast<void**>(&c->wpart), wpart_bytes) &&
+              alloc(reinterpret_cast<void**>(&c->idx), cnt_bytes) &&
+              alloc(reinterpret_cast<void**>(&c->tiers), tier_bytes) &&
+              alloc(reinterpret_cast<void**>(&c->act_lists), list_bytes) &&
+              alloc(reinterpret_cast<void**>(&c->act_counts), acnt_bytes) &&
+              alloc(reinterpret_cast<void**>(&c->sparsity), sp_bytes) &&
+              alloc(reinterpret_cast<void**>(&c->counters), ctr_bytes) &&
+              alloc(reinterpret_cast<void**>(&c->tot), sizeof(skvd::LedgerTotals)) &&
+              alloc(reinterpret_cast<void**>(&c->arrive), static_cast<size_t>(d.layers) * 4) &&
+              alloc(reinterpret_cast<void**>(&c->layer_allocs), static_cast<size_t>(d.layers) * 8);
+    if (ok && c->paged)
+        ok = alloc(reinterpret_cast<void**>(&c->slot), cells * 4) &&
+             alloc(reinterpret_cast<void**>(&c->fq), static_cast<size_t>(d.layers) * d.batch * c->pcap * 4) &&
+             alloc(reinterpret_cast<void**>(&c->fq_ht), static_cast<size_t>(d.layers) * d.batch * 8) &&
+             alloc(reinterpret_cast<void**>(&c->act_slots), list_bytes) &&
+             alloc(reinterpret_cast<void**>(&c->aux), acnt_bytes);
+    if (ok) {
+        void* h = nullptr;
+        ok = cudaHostAlloc(&h, sizeof(skvd::DevStatus), cudaHostAllocMapped | cudaHostAllocPortable) == cudaSuccess;
+        if (ok) {
+            c->status = static_cast<skvd::DevStatus*>(h);
+            std::memset(c->status, 0, sizeof(skvd::DevStatus));
+            void* dp = nullptr;
+            ok = cudaHostGetDevicePointer(&dp, h, 0) == cudaSuccess;
+            c->status_dev = static_cast<skvd::DevStatus*>(dp);
+        }
+        if (!ok) cudaGetLastError();
+    }
+    if (!ok) {
+        const uint64_t want = kv_bytes + imp_bytes + wpart_bytes + cnt_bytes + tier_bytes + list_bytes + acnt_bytes;
         skv_cache_destroy(c);
         return fail(SKV_ERR_OOM, "skv_cache_create: cannot allocate %llu device bytes",
                     static_cast<unsigned long long>(want));
@@ -262,16 +352,42 @@ skv_status skv_cache_create(const skv_cache_desc* desc, skv_cache** out) {
     SKV_CUDA(cudaMemset(c->act_counts, 0, acnt_bytes));
     SKV_CUDA(cudaMemset(c->sparsity, 0, sp_bytes));
     SKV_CUDA(cudaMemset(c->counters, 0, ctr_bytes));
+    SKV_CUDA(cudaMemset(c->tot, 0, sizeof(skvd::LedgerTotals)));
+    SKV_CUDA(cudaMemset(c->arrive, 0, static_cast<size_t>(d.layers) * 4));
+    SKV_CUDA(cudaMemset(c->layer_allocs, 0, static_cast<size_t>(d.layers) * 8));
+    if (c->paged) {
+        SKV_CUDA(cudaMemset(c->slot, 0xFF, cells * 4));
+        SKV_CUDA(cudaMemset(c->aux, 0, acnt_bytes));
+        // every ring starts full, slots in order: the prompt takes slot t for token t
+        std::vector<int> ring(c->pcap);
+        for (int i = 0; i < c->pcap; ++i) ring[i] = i;
+        std::vector<unsigned> ht(static_cast<size_t>(d.layers) * d.batch * 2);
+        for (size_t i = 0; i < ht.size(); i += 2) {
+            ht[i] = 0;
+            ht[i + 1] = static_cast<unsigned>(c->pcap);
+        }
+        for (size_t r = 0; r < static_cast<size_t>(d.layers) * d.batch; ++r)
+            SKV_CUDA(cudaMemcpy(c->fq + r * c->pcap, ring.data(), ring.size() * 4, cudaMemcpyHostToDevice));
+        SKV_CUDA(cudaMemcpy(c->fq_ht, ht.data(), ht.size() * 4, cudaMemcpyHostToDevice));
+    }
     c->pend_n.assign(d.layers, -1);
     c->pend_r.assign(d.layers, 0.0);
     c->ledger_j.assign(d.layers, -1);
     c->rec_x.assign(d.layers, nullptr);
     c->rec_wt.assign(d.layers, nullptr);
-    if (meta_bytes) SKV_CUDA(cudaMemset(c->meta, 0, meta_bytes));
+    c->ident.assign(static_cast<size_t>(d.layers) * d.batch, 0);
+    c->decoded.assign(d.layers, 0);
     SKV_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, d.device));
     SKV_CUDA(cudaDeviceGetAttribute(&c->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, d.device));
     *out = c;
     return SKV_OK;
+}
+
+skv_status skv_cache_create(const skv_cache_desc* desc, skv_cache** out) { return cache_create_impl(desc, 0, out); }
+
+skv_status skv_cache_create_paged(const skv_cache_desc* desc, uint64_t device_capacity, skv_cache** out) {
+    SKV_REQUIRE(device_capacity > 0, "KvLedger: zero device capacity");
+    return cache_create_impl(desc, device_capacity, out);
 }
 
 skv_status skv_cache_destroy(skv_cache* c) {
@@ -287,6 +403,16 @@ skv_status skv_cache_destroy(skv_cache* c) {
     cudaFree(c->act_counts);
     cudaFree(c->sparsity);
     cudaFree(c->counters);
+    cudaFree(c->tot);
+    cudaFree(c->arrive);
+    cudaFree(c->layer_allocs);
+    cudaFree(c->slot);
+    cudaFree(c->fq);
+    cudaFree(c->fq_ht);
+    cudaFree(c->act_slots);
+    cudaFree(c->aux);
+    cudaFree(c->rec_c);
+    if (c->status) cudaFreeHost(c->status);
     if (c->host_kv) cudaFreeHost(c->host_kv);
     for (uint8_t* w : c->rec_wt) cudaFree(w);
     cudaFree(c->rec_a);
@@ -329,12 +455,40 @@ skv_status skv_cache_write(skv_cache* c, int layer, int b0, int nb, int t0, int 
                            const void* v, void* stream) {
     if (skv_status s = check_block(c, layer, b0, nb, t0, nt)) return s;
     SKV_REQUIRE(k != nullptr && v != nullptr, "append_token: null rows");
+    if (skv_status s = check_status(c)) return s;
     DeviceGuard guard(c->d.device);
+    const cudaStream_t st = as_stream(stream);
     const size_t lt = static_cast<size_t>(layer) * c->d.batch * c->d.capacity;
+    // tokens this write stores for the first time (KvLedger::store_new)
+    uint64_t fresh = 0;
+    for (int b = b0; b < b0 + nb; ++b) {
+        const int hw = c->ident[static_cast<size_t>(layer) * c->d.batch + b];
+        fresh += static_cast<uint64_t>(std::max(0, t0 + nt - std::max(hw, t0)));
+        if (c->paged)
+            SKV_REQUIRE(!c->decoded[layer] && t0 <= hw,
+                        "paged cache: skv_cache_write fills the prompt in order before the first decode step");
+    }
+    if (c->cap_bytes != ~0ull && fresh > 0) {
+        // memsim.hpp:99-109: store_new checks the device capacity per token
+        skvd::LedgerTotals tot{};
+        SKV_CUDA(cudaMemcpyAsync(&tot, c->tot, sizeof tot, cudaMemcpyDeviceToHost, st));
+        SKV_CUDA(cudaStreamSynchronize(st));
+        const uint64_t e = c->tok_bytes;
+        if ((tot.dev_tokens + fresh) * e > c->cap_bytes || (c->paged && t0 + nt > c->pcap)) {
+            const uint64_t fit = c->cap_bytes / e;
+            return fail(SKV_ERR_OOM, "simulated OOM: device tier needs %llu bytes, capacity %llu",
+                        static_cast<unsigned long long>(e * (std::max<uint64_t>(tot.dev_tokens, fit) + 1)),
+                        static_cast<unsigned long long>(c->cap_bytes));
+        }
+    }
     c->pend_n[layer] = -1;
-    SKV_CUDA(launch_cache_write(c->d.kv_dtype, c->d.q_dtype, c->kv + layer * c->layer_bytes, c->imp + lt,
-                                c->tiers + lt, k, v,
-                                c->d.heads, c->d.capacity, b0, nb, t0, nt, as_stream(stream)));
+    const skvd::CacheView cv = cache_view(c, layer);
+    SKV_CUDA(launch_cache_write(c->d.kv_dtype, c->d.q_dtype, cv, c->imp + lt, c->tiers + lt, k, v, c->d.heads, b0, nb,
+                                t0, nt, st));
+    for (int b = b0; b < b0 + nb; ++b) {
+        int& hw = c->ident[static_cast<size_t>(layer) * c->d.batch + b];
+        hw = std::max(hw, t0 + nt);
+    }
     return SKV_OK;
 }
 
@@ -343,10 +497,8 @@ skv_status skv_cache_read(const skv_cache* c, int layer, int b0, int nb, int t0,
     if (skv_status s = check_block(c, layer, b0, nb, t0, nt)) return s;
     SKV_REQUIRE(out != nullptr, "skv_cache_read: null output");
     DeviceGuard guard(c->d.device);
-    const size_t lt = static_cast<size_t>(layer) * c->d.batch * c->d.capacity;
-    (void)lt;
-    SKV_CUDA(launch_cache_read(c->d.kv_dtype, c->kv + layer * c->layer_bytes, out, c->d.heads,
-                               c->d.capacity, b0, nb, t0, nt, as_stream(stream)));
+    const skvd::CacheView cv = cache_view(const_cast<skv_cache*>(c), layer);
+    SKV_CUDA(launch_cache_read(c->d.kv_dtype, cv, out, c->d.heads, b0, nb, t0, nt, as_stream(stream)));
     return SKV_OK;
 }
 
@@ -402,7 +554,7 @@ skv_status pick_attend(skv_cache* c, int m, const DecodeLaunch** dl_out, size_t*
             if (env_hg && hg != env_hg) continue;
             const DecodeLaunch* dl = find_decode(c->d.kv_dtype, c->d.q_dtype, hg);
             if (!dl) continue;
-            const size_t smem = dl->smem(m, gmem);
+            const size_t smem = dl->smem(m, gmem, c->paged);
             if (smem > static_cast<size_t>(c->max_smem)) continue;
             smallest = dl;
             smallest_smem = smem;
@@ -647,6 +799,11 @@ skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok
     skvd::AttendParams p{};
     p.kv = c->kv + layer * c->layer_bytes;
     p.kv_w = c->kv + layer * c->layer_bytes;
+    p.kv_ncap = c->pcap;
+    p.slots = c->paged ? c->slot + lt : nullptr;
+    p.tiers = c->has_plan ? c->tiers + lt : nullptr;  // residency check (engine.hpp:625-628)
+    p.status = c->status_dev;
+    p.layer = layer;
     p.q = q;
     p.k_new = k_new;
     p.v_new = v_new;
@@ -771,6 +928,25 @@ skv_status launch_ledger_c(skv_cache* c, int layer, long long j, const int* sel,
     p.counts = c->act_counts + static_cast<size_t>(layer) * c->d.batch * 4;
     p.apply = apply ? 1 : 0;
     p.store_current = store_current ? 1 : 0;
+    if (c->paged) {
+        p.slots.slot = c->slot + lt;
+        p.slots.slot_ld = c->d.capacity;
+        p.slots.fq = c->fq + static_cast<size_t>(layer) * c->d.batch * c->pcap;
+        p.slots.fq_ht = c->fq_ht + static_cast<size_t>(layer) * c->d.batch * 2;
+        p.slots.pcap = c->pcap;
+        p.act_slots = c->act_slots + lt * 4;
+        p.aux = c->aux + static_cast<size_t>(layer) * c->d.batch * 4;
+    }
+    if (apply) {  // KvLedger byte accounting + the capacity check (memsim.hpp:193-200)
+        p.tot = c->tot;
+        p.arrive = c->arrive + layer;
+        p.layer_allocs = c->layer_allocs + layer;
+    }
+    p.cap_bytes = c->cap_bytes;
+    p.tok_bytes = c->tok_bytes;
+    p.layer = layer;
+    p.step = j;
+    p.status = c->status_dev;
     SKV_REQUIRE(p.existing < c->d.capacity, "step_actions: step beyond the cache capacity");
     SKV_CUDA(launch_ledger(p, c->d.batch, pdl, st));
     if (apply) c->ledger_j[layer] = j;
@@ -784,32 +960,51 @@ skv_status launch_movement(skv_cache* c, int layer, bool pdl, cudaStream_t st) {
     skvd::MoveParams mp{};
     const size_t lt = static_cast<size_t>(layer) * c->d.batch;
     mp.dev = c->kv + layer * c->layer_bytes;
-    mp.host = c->host_kv + layer * c->layer_bytes;
+    mp.host = c->host_kv + layer * c->host_layer_bytes;
     mp.lists = c->act_lists + lt * 4 * c->d.capacity;
     mp.counts = c->act_counts + lt * 4;
     mp.list_ld = c->d.capacity;
     mp.tok_bytes = static_cast<long long>(c->tok_bytes);
     mp.seq_bytes = static_cast<long long>(c->tok_bytes) * c->d.capacity;
+    mp.dev_seq_bytes = static_cast<long long>(c->tok_bytes) * c->pcap;
     mp.poison = c->poison ? 1 : 0;
     mp.which = -1;  // offload and reload in one launch: both PCIe directions at once
+    if (c->paged) {
+        mp.act_slots = c->act_slots + lt * 4 * c->d.capacity;
+        mp.aux = c->aux + lt * 4;
+    }
     SKV_CUDA(launch_move(mp, c->d.batch, c->d.capacity, pdl, st));
+    if (c->paged) {  // reloads into slots this step's offload frees: after those copies
+        mp.which = 2;
+        mp.second = 1;
+        SKV_CUDA(launch_move(mp, c->d.batch, c->d.capacity, pdl, st));
+    }
     if (c->rec_x[layer]) {
         // recompute_kv for this step's list: gather the retained rows, one
         // tcgen05 GEMM against [Wk | Wv]^T, K/V written straight into the rows
+        // (INT8: through fp32 rows and the fake-quant, engine.hpp:729-730)
         const long long h = static_cast<long long>(c->d.heads) * c->d.head_dim;
         const long long xrow = h * static_cast<long long>(dtype_size(c->d.q_dtype));
         SKV_CUDA(launch_recompute_gather(c->rec_x[layer], xrow * c->d.capacity, xrow, mp.lists, mp.counts,
-                                         c->d.capacity, c->rec_a, c->rec_map, c->rec_m, c->d.batch, st));
-        skvd::KvScatter sc{};
-        sc.kv = mp.dev;
-        sc.rowmap = c->rec_map;
-        sc.H = c->d.heads;
-        sc.D = c->d.head_dim;
-        sc.Ncap = c->d.capacity;
-        sc.row_bytes = static_cast<int>(c->row_bytes);
+                                         c->d.capacity, c->rec_a, c->rec_map, c->rec_m, c->d.batch, st,
+                                         c->paged ? mp.act_slots : nullptr));
         const int m_cap = static_cast<int>((static_cast<long long>(c->d.batch) * c->d.capacity + 127) / 128 * 128);
-        SKV_CUDA(launch_gemm_tn(c->rec_a, c->rec_wt[layer], nullptr, c->rec_m, m_cap, static_cast<int>(2 * h),
-                                static_cast<int>(h), c->d.q_dtype == SKV_BF16, st, &sc));
+        if (c->d.kv_dtype == SKV_U8) {
+            SKV_CUDA(launch_gemm_tn(c->rec_a, c->rec_wt[layer], c->rec_c, c->rec_m, m_cap, static_cast<int>(2 * h),
+                                    static_cast<int>(h), c->d.q_dtype == SKV_BF16, st, nullptr));
+            SKV_CUDA(launch_quant_scatter(c->d.q_dtype, c->rec_c, c->rec_m, m_cap, c->rec_map, mp.dev, c->d.heads,
+                                          c->pcap, st));
+        } else {
+            skvd::KvScatter sc{};
+            sc.kv = mp.dev;
+            sc.rowmap = c->rec_map;
+            sc.H = c->d.heads;
+            sc.D = c->d.head_dim;
+            sc.Ncap = c->pcap;
+            sc.row_bytes = static_cast<int>(c->row_bytes);
+            SKV_CUDA(launch_gemm_tn(c->rec_a, c->rec_wt[layer], nullptr, c->rec_m, m_cap, static_cast<int>(2 * h),
+                                    static_cast<int>(h), c->d.q_dtype == SKV_BF16, st, &sc));
+        }
     }
     return SKV_OK;
 }
@@ -822,6 +1017,9 @@ skv_status decode_layer_impl(skv_cache* c, int layer, int n, double r, const voi
                              cudaStream_t st) {
     StepShape s;
     if (skv_status e = step_shape(c, n, r, &s)) return e;
+    if (c->paged && !c->has_plan)
+        return fail(SKV_ERR_CONTRACT, "paged cache: attach a plan (skv_cache_set_plan) before decoding");
+    c->decoded[layer] = 1;
     bool fresh = false;
     if (!(c->pend_n[layer] == n && c->pend_r[layer] == r)) {
         if (skv_status e = launch_select_c(c, layer, 0, nullptr, 0, 0, 0, -1, n, r, false, st)) return e;
@@ -924,10 +1122,14 @@ skv_status skv_prefill_layer(skv_cache* c, int layer, int s, const void* q, void
     double* imp = c->imp + lay * B * c->d.capacity;
     double* psp = c->pf_sparsity + lay * B;
     const void* kv = c->kv + lay * c->layer_bytes;
-    int kv_ncap = c->d.capacity;
+    int kv_ncap = c->pcap;
+    if (c->paged)  // the TMA maps read the prompt rows in place: token t must sit in slot t
+        for (int b = 0; b < B; ++b)
+            SKV_REQUIRE(!c->decoded[layer] && c->ident[lay * B + b] >= s,
+                        "paged cache: the tensor-core prefill needs the prompt written in order first");
     if (int8) {
         uint8_t* deq = c->pf_scratch + base_scratch;
-        SKV_CUDA(launch_dequant_layer_f16(c->kv + lay * c->layer_bytes, deq, H, c->d.capacity, B, s, st));
+        SKV_CUDA(launch_dequant_layer_f16(c->kv + lay * c->layer_bytes, deq, H, c->pcap, B, s, st));
         kv = deq;
         kv_ncap = s;
     }
@@ -985,6 +1187,7 @@ skv_status skv_swa_decode_layer(skv_cache* c, int layer, int n, double r, const 
     SKV_REQUIRE(c != nullptr, "null cache");
     SKV_REQUIRE(layer >= 0 && layer < c->d.layers, "KvLedger: layer out of range");
     SKV_REQUIRE(q && k_new && v_new && out, "decode_step: null argument");
+    if (skv_status e = check_status(c)) return e;
     DeviceGuard guard(c->d.device);
     return decode_layer_impl(c, layer, n, r, q, k_new, v_new, out, idx_out, w_out, false, as_stream(stream));
 }
@@ -1045,6 +1248,7 @@ skv_status skv_swa_decode_step(skv_cache* c, int n, double r, const void* q, con
                                const void* v_new, void* out, void* stream) {
     SKV_REQUIRE(c != nullptr, "null cache");
     SKV_REQUIRE(q && k_new && v_new && out, "decode_step: null argument");
+    if (skv_status e = check_status(c)) return e;
     StepShape s;
     if (skv_status st = step_shape(c, n, r, &s)) return st;
     DeviceGuard guard(c->d.device);
@@ -1076,6 +1280,7 @@ skv_status skv_swa_decode_step_host(skv_cache* c, int n, double r, const void* q
                                     const void* v_host, void* out_host, void* stream) {
     SKV_REQUIRE(c != nullptr, "null cache");
     SKV_REQUIRE(q_host && k_host && v_host && out_host, "decode_step: null argument");
+    if (skv_status e = check_status(c)) return e;
     StepShape shape;
     if (skv_status st = step_shape(c, n, r, &shape)) return st;
     DeviceGuard guard(c->d.device);
@@ -1132,6 +1337,7 @@ skv_status skv_attend_over_indices(skv_cache* c, int layer, int n, const int32_t
     SKV_REQUIRE(m >= 1, "attend_over_indices: empty selection");
     SKV_REQUIRE(m <= n, "attend_over_indices: more indices than tokens");
     SKV_REQUIRE(idx && q && out, "attend_over_indices: null argument");
+    if (skv_status e = check_status(c)) return e;
     DeviceGuard guard(c->d.device);
     const cudaStream_t st = as_stream(stream);
     // The reference validates every index (attention.hpp:186-192). Indices
@@ -1264,7 +1470,7 @@ skv_status skv_cache_enable_host_tier(skv_cache* c, int poison) {
     DeviceGuard guard(c->d.device);
     if (!c->host_kv) {
         void* h = nullptr;
-        const size_t bytes = c->layer_bytes * c->d.layers;
+        const size_t bytes = c->host_layer_bytes * c->d.layers;
         if (cudaHostAlloc(&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
             cudaGetLastError();
             return fail(SKV_ERR_OOM, "host tier: cannot pin %llu bytes", static_cast<unsigned long long>(bytes));
@@ -1279,8 +1485,9 @@ skv_status skv_cache_attach_recompute(skv_cache* c, int layer, const void* x_ln1
                                       void* stream) {
     SKV_REQUIRE(c != nullptr, "null cache");
     SKV_REQUIRE(layer >= 0 && layer < c->d.layers, "KvLedger: layer out of range");
-    if (!(c->d.kv_dtype == c->d.q_dtype && (c->d.q_dtype == SKV_F16 || c->d.q_dtype == SKV_BF16)))
-        return fail(SKV_ERR_UNSUPPORTED, "recompute: fp16/bf16 caches only");
+    if (!((c->d.kv_dtype == c->d.q_dtype || c->d.kv_dtype == SKV_U8) &&
+          (c->d.q_dtype == SKV_F16 || c->d.q_dtype == SKV_BF16)))
+        return fail(SKV_ERR_UNSUPPORTED, "recompute: fp16/bf16 compute (fp16/bf16 or INT8 caches) only");
     const long long h = static_cast<long long>(c->d.heads) * c->d.head_dim;
     if (h % 256 != 0) return fail(SKV_ERR_UNSUPPORTED, "recompute: hidden %lld not a multiple of 256", h);
     DeviceGuard guard(c->d.device);
@@ -1302,7 +1509,9 @@ skv_status skv_cache_attach_recompute(skv_cache* c, int layer, const void* x_ln1
     if (!grab(reinterpret_cast<void**>(&c->rec_wt[layer]), static_cast<size_t>(2 * h * h) * 2) ||
         !grab(reinterpret_cast<void**>(&c->rec_a), rows * static_cast<size_t>(h) * 2) ||
         !grab(reinterpret_cast<void**>(&c->rec_map), rows * sizeof(int2)) ||
-        !grab(reinterpret_cast<void**>(&c->rec_m), sizeof(int)))
+        !grab(reinterpret_cast<void**>(&c->rec_m), sizeof(int)) ||
+        (c->d.kv_dtype == SKV_U8 &&
+         !grab(reinterpret_cast<void**>(&c->rec_c), rows * static_cast<size_t>(2 * h) * 4)))
         return fail(SKV_ERR_OOM, "recompute: cannot allocate buffers");
     SKV_CUDA(launch_transpose_kv_weights(wk, wv, c->rec_wt[layer], static_cast<int>(h), st));
     c->rec_x[layer] = static_cast<const uint8_t*>(x_ln1);
@@ -1407,6 +1616,7 @@ skv_status skv_cache_set_plan(skv_cache* c, const skv_plan* plan) {
 
 skv_status skv_ledger_set(skv_cache* c, int layer, int b0, int nb, int len, const uint8_t* src, void* stream) {
     if (skv_status s = check_block(c, layer, b0, nb, 0, len)) return s;
+    if (c->paged) return fail(SKV_ERR_UNSUPPORTED, "paged cache: tiers follow the slots; set them by decoding");
     DeviceGuard guard(c->d.device);
     uint8_t* dst = c->tiers + (static_cast<size_t>(layer) * c->d.batch + b0) * c->d.capacity;
     SKV_CUDA(cudaMemcpy2DAsync(dst, c->d.capacity, src, len, len, nb, cudaMemcpyDefault, as_stream(stream)));
@@ -1421,6 +1631,36 @@ skv_status skv_ledger_get(const skv_cache* c, int layer, int b0, int nb, int len
     return SKV_OK;
 }
 
+skv_status skv_cache_set_capacity(skv_cache* c, uint64_t device_capacity) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    SKV_REQUIRE(device_capacity > 0, "KvLedger: zero device capacity");
+    c->cap_bytes = device_capacity;
+    return SKV_OK;
+}
+
+skv_status skv_ledger_totals(const skv_cache* c, uint64_t* device_bytes, uint64_t* host_bytes,
+                             uint64_t* peak_device_bytes, uint64_t* capacity, void* stream) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    DeviceGuard guard(c->d.device);
+    skvd::LedgerTotals t{};
+    SKV_CUDA(cudaMemcpyAsync(&t, c->tot, sizeof t, cudaMemcpyDeviceToHost, as_stream(stream)));
+    SKV_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    if (device_bytes) *device_bytes = t.dev_tokens * c->tok_bytes;
+    if (host_bytes) *host_bytes = t.host_tokens * c->tok_bytes;
+    if (peak_device_bytes) *peak_device_bytes = std::max(t.peak_dev_tokens, t.dev_tokens) * c->tok_bytes;
+    if (capacity) *capacity = c->cap_bytes;
+    return check_status(c);
+}
+
+skv_status skv_cache_storage(const skv_cache* c, int32_t* slots_per_sequence, uint64_t* kv_pool_bytes,
+                             uint64_t* full_kv_bytes) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    if (slots_per_sequence) *slots_per_sequence = c->pcap;
+    if (kv_pool_bytes) *kv_pool_bytes = c->layer_bytes * c->d.layers;
+    if (full_kv_bytes) *full_kv_bytes = c->host_layer_bytes * c->d.layers;
+    return SKV_OK;
+}
+
 skv_status skv_step_actions(skv_cache* c, int layer, int j, const int32_t* selected, int m, int k, int apply,
                             int32_t* lists_out, int32_t* counts_out, void* stream) {
     SKV_REQUIRE(c != nullptr, "null cache");
@@ -1428,6 +1668,9 @@ skv_status skv_step_actions(skv_cache* c, int layer, int j, const int32_t* selec
     SKV_REQUIRE(layer >= 0 && layer < c->d.layers, "KvLedger: layer out of range");
     SKV_REQUIRE(j >= 0 && j < c->plan.output_len, "step_actions: step beyond output length");
     SKV_REQUIRE(selected != nullptr && m >= 0 && k >= 1, "step_actions: bad selection");
+    if (c->paged && apply)
+        return fail(SKV_ERR_UNSUPPORTED, "paged cache: actions are applied (with their data movement) by decoding");
+    if (skv_status e = check_status(c)) return e;
     DeviceGuard guard(c->d.device);
     const cudaStream_t st = as_stream(stream);
     if (skv_status e = launch_ledger_c(c, layer, j, selected, m, m, k, apply != 0, false, false, st)) return e;

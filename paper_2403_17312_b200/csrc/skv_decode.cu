@@ -8,8 +8,8 @@ using namespace skvd;
 namespace {
 
 template <class KV, class QT, int HG>
-size_t smem_of(int m, bool gmem) {
-    return decode_smem<KV, HG>(m, gmem).total;
+size_t smem_of(int m, bool gmem, bool paged) {
+    return decode_smem<KV, HG>(m, gmem, paged).total;
 }
 
 template <class KV, class QT, int HG>

@@ -24,6 +24,7 @@
 #include <type_traits>
 
 #include "skv_device.cuh"
+#include "skv_ledger.cuh"
 #include "skv_select.cuh"
 
 #ifndef SKV_STAGE_BYTES
@@ -76,6 +77,16 @@ struct AttendParams {
     // scratch instead of shared memory ([B][G][Ncap] ids, [B][G][HG][Ncap] f32)
     int* gtok;
     float* gwts;
+    // Paged store: token -> slot map of this layer ([B][Ncap], -1: not on
+    // device) and the slot stride of kv; nullptr: kv is token-indexed.
+    const int* slots;
+    int kv_ncap;
+    // Residency check (engine.hpp:625-628): with a plan attached, every
+    // gathered token must be device-resident (tiers [B][Ncap] of this layer);
+    // a violation is reported through status.
+    const uint8_t* tiers;
+    DevStatus* status;
+    int layer;
     SelectParams sel;    // imp / wpart / apply / cur_tok / sparsity / next selection; tok_prev = this CTA's list
 };
 
@@ -106,13 +117,13 @@ struct DecodeCfg {
 };
 
 struct DecodeSmem {
-    size_t ring, bars, tok, wts, topk, scratch, flag, total;
+    size_t ring, bars, tok, slot, wts, topk, scratch, flag, total;
 };
 
 // Shared-memory carve-up; identical on host (launch size) and device. gmem:
 // the token list and the weights are in global scratch (long selections).
 template <class KV, int HG>
-__host__ __device__ inline DecodeSmem decode_smem(int m, bool gmem = false) {
+__host__ __device__ inline DecodeSmem decode_smem(int m, bool gmem = false, bool paged = false) {
     if (gmem) m = 0;
     using C = DecodeCfg<KV, HG>;
     DecodeSmem s;
@@ -123,6 +134,8 @@ __host__ __device__ inline DecodeSmem decode_smem(int m, bool gmem = false) {
     o += 2 * C::S * 8;
     s.tok = o;
     o = align_up(o + static_cast<size_t>(m) * 4, 16);
+    s.slot = o;  // paged: the selected tokens' slots
+    o = align_up(o + (paged ? static_cast<size_t>(m) * 4 : 0), 16);
     s.wts = o;  // logits, then weights [HG][m] f32
     o = align_up(o + static_cast<size_t>(HG) * m * 4, 16);
     s.topk = o;
@@ -185,7 +198,8 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
     const int g = blockIdx.x, b = blockIdx.y, G = gridDim.x;
     const int H = p.H, n = p.n, m = p.m;
     const bool gmem = p.gtok != nullptr;
-    const DecodeSmem L = decode_smem<KV, HG>(m, gmem);
+    const bool paged = p.slots != nullptr;
+    const DecodeSmem L = decode_smem<KV, HG>(m, gmem, paged);
 
     uint8_t* ring = smem + L.ring;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
@@ -200,7 +214,10 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
     pdl_launch_dependents();
 
     const size_t TOKB = static_cast<size_t>(2) * H * ROWE;  // bytes per token (K and V planes)
-    const uint8_t* kvb = p.kv + static_cast<size_t>(b) * p.Ncap * TOKB + static_cast<size_t>(g) * ROWB;
+    const uint8_t* kvb = p.kv + static_cast<size_t>(b) * p.kv_ncap * TOKB + static_cast<size_t>(g) * ROWB;
+    const int* slot_row = paged ? p.slots + static_cast<size_t>(b) * p.Ncap : nullptr;
+    // smem slot list (paged, shared-memory token list); long selections look slots up in the producer
+    int* tslot = (paged && !gmem) ? reinterpret_cast<int*>(smem + L.slot) : nullptr;
 
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
@@ -209,11 +226,24 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
         }
         fence_barrier_init();
     }
-    if (p.tok != nullptr) {
-        const int* src = p.tok + static_cast<size_t>(b) * p.tok_ld;
-        for (int i = tid; i < m; i += kDecodeThreads) tok[i] = src[i];
-    } else {
-        for (int i = tid; i < m; i += kDecodeThreads) tok[i] = i;
+    {
+        const int* src = p.tok ? p.tok + static_cast<size_t>(b) * p.tok_ld : nullptr;
+        const uint8_t* trow = p.tiers ? p.tiers + static_cast<size_t>(b) * p.Ncap : nullptr;
+        for (int i = tid; i < m; i += kDecodeThreads) {
+            const int t = src ? src[i] : i;
+            tok[i] = t;
+            const bool cur = p.append && i == m - 1;  // the appended token: stored by this kernel
+            if (trow && !cur && trow[t] != kTierDevice && g == 0)
+                report_status(p.status, 1, p.layer, b, t, -1, 0ull, 0ull);  // engine.hpp:625-628
+            if (tslot) {
+                int sl = slot_row[t];
+                if (sl < 0) {
+                    if (g == 0) report_status(p.status, 1, p.layer, b, t, -1, 0ull, 0ull);
+                    sl = 0;
+                }
+                tslot[i] = sl;
+            }
+        }
     }
     __syncthreads();
 
@@ -250,7 +280,8 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
             __syncwarp();
             if (lane < mine) {
                 const int i = pw + lane * kProducerWarps;
-                const int t = tok[base + i];
+                int t = tslot ? tslot[base + i] : tok[base + i];
+                if (paged && !tslot) t = max(slot_row[t], 0);
                 const uint8_t* src = kvb + static_cast<size_t>(t) * TOKB + vsel * H * ROWE;
                 if (!QUANT && has_cur && i == cnt - 1) src = vsel ? vnew : knew;
                 bulk_g2s(ring + stage * STAGEB + i * ROWB, src, ROWB, &full[stage], pol);
@@ -265,7 +296,8 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
 
     // ---- append the step's new K/V rows for this head group (token n-1)
     if (p.append) {
-        const size_t tok_off = (static_cast<size_t>(b) * p.Ncap + (n - 1)) * TOKB +
+        const int cur_slot = paged ? max(slot_row[n - 1], 0) : n - 1;
+        const size_t tok_off = (static_cast<size_t>(b) * p.kv_ncap + cur_slot) * TOKB +
                                static_cast<size_t>(g) * ROWB;
         if constexpr (!QUANT) {
             constexpr int VPR = ROWB / 16;  // compute dtype == storage dtype

@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                              __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
                 } else {
                     const int2 bt = sc.rowmap[row];
+                    if (bt.y < 0) continue;  // no slot (paged OOM, reported by the ledger)
                     const int hidden = sc.H * sc.D;
                     const int j = n0 + c * 32;
                     const int kvsel = j / hidden, hh = (j % hidden) / sc.D, d = j % sc.D;
@@ -199,19 +200,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 __global__ void __launch_bounds__(256)
     recompute_gather_kernel(const uint8_t* __restrict__ x, long long x_seq, long long x_row, const int* lists,
                             const int* counts, long long list_ld, uint8_t* __restrict__ A, int2* rowmap, int* m_out,
-                            int B) {
+                            int B, const int* dst_slots) {
     const int b = blockIdx.x;
     int off = 0;
     for (int i = 0; i < b; ++i) off += counts[i * 4 + 3];
     const int cnt = counts[b * 4 + 3];
     const int* list = lists + (static_cast<size_t>(b) * 4 + 3) * list_ld;
-    const long long vecs = x_row / 16;
-    for (long long v = threadIdx.x; v < static_cast<long long>(cnt) * vecs; v += blockDim.x) {
-        const int i = static_cast<int>(v / vecs);
+    const int* dslot = dst_slots ? dst_slots + (static_cast<size_t>(b) * 4 + 3) * list_ld : nullptr;
+    const int vecs = static_cast<int>(x_row / 16);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    for (int i = warp; i < cnt; i += nwarps) {  // one warp per row: no 64-bit index division
         const int t = list[i];
         const uint4* src = reinterpret_cast<const uint4*>(x + b * x_seq + static_cast<long long>(t) * x_row);
-        reinterpret_cast<uint4*>(A + static_cast<size_t>(off + i) * x_row)[v % vecs] = src[v % vecs];
-        if (v % vecs == 0) rowmap[off + i] = make_int2(b, t);
+        uint4* dst = reinterpret_cast<uint4*>(A + static_cast<size_t>(off + i) * x_row);
+        for (int v = lane; v < vecs; v += 32) dst[v] = src[v];
+        if (lane == 0)  // paged: the destination is the slot the ledger allocated
+            rowmap[off + i] = make_int2(b, dslot ? dslot[i] : t);
     }
     if (b == B - 1 && threadIdx.x == 0) *m_out = off + cnt;
 }
@@ -222,8 +226,9 @@ namespace skv_impl {
 
 cudaError_t launch_recompute_gather(const uint8_t* x, long long x_seq, long long x_row, const int* lists,
                                     const int* counts, long long list_ld, uint8_t* A, int2* rowmap, int* m_out,
-                                    int B, cudaStream_t st) {
-    skvd::recompute_gather_kernel<<<B, 256, 0, st>>>(x, x_seq, x_row, lists, counts, list_ld, A, rowmap, m_out, B);
+                                    int B, cudaStream_t st, const int* dst_slots) {
+    skvd::recompute_gather_kernel<<<B, 256, 0, st>>>(x, x_seq, x_row, lists, counts, list_ld, A, rowmap, m_out, B,
+                                                     dst_slots);
     count_launch();
     return cudaGetLastError();
 }

@@ -29,11 +29,13 @@ cudaError_t launch_quantize(const double* x, long long len, long long cs, uint32
 cudaError_t launch_dequantize(const uint16_t* codes, long long len, long long cs,
                               const double* scales, const long long* zps, double* out,
                               cudaStream_t st);
-cudaError_t launch_cache_write(int kv_dtype, int q_dtype, uint8_t* kv, double* imp, uint8_t* tiers,
-                               const void* k, const void* v, int H, int Ncap, int b0, int nb, int t0, int nt,
-                               cudaStream_t st);
-cudaError_t launch_cache_read(int kv_dtype, const uint8_t* kv, float* out, int H, int Ncap, int b0, int nb,
-                              int t0, int nt, cudaStream_t st);
+cudaError_t launch_cache_write(int kv_dtype, int q_dtype, const skvd::CacheView& cv, double* imp, uint8_t* tiers,
+                               const void* k, const void* v, int H, int b0, int nb, int t0, int nt, cudaStream_t st);
+cudaError_t launch_cache_read(int kv_dtype, const skvd::CacheView& cv, float* out, int H, int b0, int nb, int t0,
+                              int nt, cudaStream_t st);
+// INT8 recompute write-back: fp32 GEMM rows [M][2h] -> quantised rows at rowmap's (b, slot)
+cudaError_t launch_quant_scatter(int q_dtype, const float* C, const int* m_dev, int m_cap, const int2* rowmap,
+                                 uint8_t* kv, int H, int kv_ncap, cudaStream_t st);
 
 }  // namespace skv_impl
 namespace skvd {
@@ -56,12 +58,12 @@ size_t prefill_scratch_bytes(int B, int H, int s);
 cudaError_t launch_dequant_layer_f16(const uint8_t* kv, void* out, int H, int Ncap, int B, int s, cudaStream_t st);
 cudaError_t launch_recompute_gather(const uint8_t* x, long long x_seq, long long x_row, const int* lists,
                                     const int* counts, long long list_ld, uint8_t* A, int2* rowmap, int* m_out,
-                                    int B, cudaStream_t st);
+                                    int B, cudaStream_t st, const int* dst_slots = nullptr);
 
 // Fused decode kernel: one instantiation per (kv dtype, q dtype, HG).
 struct DecodeLaunch {
     const void* func;
-    size_t (*smem)(int m, bool gmem);  // gmem: token list + weights in global scratch
+    size_t (*smem)(int m, bool gmem, bool paged);  // gmem: token list + weights in global scratch
     int hg;
     size_t ring_bytes;  // shared-memory ring (reused for the tail's selection keys)
 };

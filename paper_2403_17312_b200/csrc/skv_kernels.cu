@@ -33,23 +33,100 @@ __device__ __forceinline__ uint64_t block_excl_scan(uint64_t v, uint64_t* warp_t
     return base + inc - v;
 }
 
+// Block-wide sum of an int (all threads get it).
+template <int NT>
+__device__ __forceinline__ long long block_sum(long long v, long long* red, int tid) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if ((tid & 31) == 0) red[tid >> 5] = v;
+    __syncthreads();
+    long long t = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) t += red[w];
+    __syncthreads();
+    return t;
+}
+
+// KvLedger byte accounting of one (layer, sequence) step (thread 0): the
+// device / host token deltas go into the cache's totals; the last sequence
+// of the layer checks the device capacity after the layer's allocations --
+// the reference checks before every store_new / reload / restore
+// (memsim.hpp:99-109, 126-135, 158-165, 193-200), and since a layer's frees
+// precede its allocations (engine.hpp:686-716) the running total peaks at
+// the end, so the two agree. The failing request is reported with the
+// reference's numbers: entries are tok_bytes each, so the first allocation
+// that does not fit needs tok_bytes * (max(T0, floor(cap / tok_bytes)) + 1)
+// bytes, T0 the tokens on device after the frees.
+__device__ void ledger_account(const LedgerParams& p, int b, long long d_dev, long long d_host, long long allocs) {
+    if (p.tot == nullptr) return;
+    atomicAdd(&p.tot->dev_tokens, static_cast<unsigned long long>(d_dev));
+    atomicAdd(&p.tot->host_tokens, static_cast<unsigned long long>(d_host));
+    atomicAdd(p.layer_allocs, static_cast<unsigned long long>(allocs));
+    __threadfence();
+    const unsigned prev = atomicAdd(p.arrive, 1u);
+    if (prev != gridDim.x - 1) return;
+    __threadfence();
+    const unsigned long long dev = atomicAdd(&p.tot->dev_tokens, 0ull);
+    const unsigned long long al = atomicExch(p.layer_allocs, 0ull);
+    atomicMax(&p.tot->peak_dev_tokens, dev);
+    const unsigned long long e = p.tok_bytes;
+    const unsigned long long ex = atomicExch(&p.tot->exhausted, 0ull);
+    if (dev * e > p.cap_bytes) {  // the reference's check comes first
+        const unsigned long long t0 = dev - al;
+        const unsigned long long fit = p.cap_bytes / e;
+        report_status(p.status, 2, p.layer, -1, -1, p.step, e * ((t0 > fit ? t0 : fit) + 1), p.cap_bytes);
+    } else if (ex) {  // within the capacity, but one (layer, sequence) pool ran dry
+        report_status(p.status, 2, p.layer, -1, -1, p.step, 0ull, p.cap_bytes);
+    }
+    *p.arrive = 0;
+}
+
 // step_actions (scheduler.hpp:320-381) + apply_actions (engine.hpp:686-716)
-// for one layer, one CTA per sequence. See skv_ledger.cuh.
+// for one layer, one CTA per sequence. See skv_ledger.cuh. With a paged store
+// the applied moves also free / allocate token slots: offloaded rows free
+// theirs (tail of the FIFO, in token order), reloads, recomputes and the
+// step's new token (store_new) take slots from the head, in that order.
 __global__ void __launch_bounds__(kLedgerThreads) ledger_step_kernel(const LedgerParams p) {
     constexpr int NT = kLedgerThreads;
     constexpr uint64_t M21 = (1ull << 21) - 1;
     __shared__ uint64_t wt[NT / 32];
+    __shared__ long long red[NT / 32];
+    __shared__ int s_split;
     extern __shared__ __align__(128) uint8_t smem[];
     const int b = blockIdx.x, tid = threadIdx.x;
-    pdl_launch_dependents();
     pdl_wait();  // the selection comes from the preceding select kernel
+    pdl_launch_dependents();
     const int ntok = p.existing;
+    const bool paged = p.slots.slot != nullptr;
     uint8_t* tg = p.tiers + static_cast<size_t>(b) * p.tier_ld;
     int* lists = p.lists + static_cast<size_t>(b) * 4 * p.list_ld;
     int* cnt = p.counts + static_cast<size_t>(b) * 4;
+    int* aslots = p.act_slots ? p.act_slots + static_cast<size_t>(b) * 4 * p.list_ld : nullptr;
+    int* slot = paged ? p.slots.slot + static_cast<size_t>(b) * p.slots.slot_ld : nullptr;
+    int* fq = paged ? p.slots.fq + static_cast<size_t>(b) * p.slots.pcap : nullptr;
+    unsigned* ht = paged ? p.slots.fq_ht + static_cast<size_t>(b) * 2 : nullptr;
+    // store_new of the step's token (the current token is never on a list);
+    // ht = (head, free count) of the FIFO ring
+    auto store_current = [&](unsigned head, unsigned count) {
+        if (paged) {
+            if (count > 0) {
+                slot[ntok] = fq[head];
+                ht[0] = (head + 1) % static_cast<unsigned>(p.slots.pcap);
+                ht[1] = count - 1;
+            } else {
+                slot[ntok] = -1;
+                if (p.tot) atomicAdd(&p.tot->exhausted, 1ull);  // reported by ledger_account
+            }
+        }
+        tg[ntok] = kTierDevice;
+    };
     if (p.phase == 1) {
         if (tid < 4) cnt[tid] = 0;
-        if (tid == 0 && p.store_current) tg[ntok] = kTierDevice;
+        if (tid == 0 && p.aux) p.aux[b * 4] = 0;
+        if (tid == 0 && p.store_current) {
+            store_current(paged ? ht[0] : 0u, paged ? ht[1] : 0u);
+            if (p.apply) ledger_account(p, b, 1, 0, 1);
+        }
         return;
     }
     uint8_t* t8 = smem;          // pre-action tiers [ntok]
@@ -73,6 +150,7 @@ __global__ void __launch_bounds__(kLedgerThreads) ledger_step_kernel(const Ledge
     }
     uint64_t tot;
     const uint64_t ex = block_excl_scan<NT>((dv << 42) | (hs << 21) | dnl, wt, &tot, tid);
+    const long long ndev = static_cast<long long>(tot >> 42);
     const long long nh = static_cast<long long>((tot >> 21) & M21);
     const long long ndnl = static_cast<long long>(tot & M21);
     const long long to_off = p.target > nh ? p.target - nh : 0;
@@ -136,23 +214,100 @@ __global__ void __launch_bounds__(kLedgerThreads) ledger_step_kernel(const Ledge
         }
     }
     __syncthreads();
+    const int n_rl = static_cast<int>(stot >> 32), n_rc = static_cast<int>(stot & 0xffffffffu);
     if (tid == 0) {
         cnt[0] = static_cast<int>(n_off);
         cnt[1] = static_cast<int>(n_del);
-        cnt[2] = static_cast<int>(stot >> 32);
-        cnt[3] = static_cast<int>(stot & 0xffffffffu);
+        cnt[2] = n_rl;
+        cnt[3] = n_rc;
     }
-    if (p.apply) {
-        for (int i = tid; i < ntok; i += NT) {
-            const uint8_t a = act[i];
-            if (!a) continue;
-            uint8_t t = t8[i];
+    if (!p.apply) return;
+    // a token offloaded and re-selected in the same step keeps its device row
+    // (the state the sequential offload-then-reload leaves): no slot moves
+    auto kept = [&](int t) { return (act[t] & 1) && (act[t] & 4) && !(act[t] & 2); };
+    if (paged) {
+        const unsigned head0 = ht[0], cnt0 = ht[1], pcap = static_cast<unsigned>(p.slots.pcap);
+        // frees: offloaded rows that are not kept, in offload-list (token) order
+        int nf_mine = 0;
+        const int oper = (static_cast<int>(n_off) + NT - 1) / NT;
+        const int obeg = min(tid * oper, static_cast<int>(n_off)), oend = min(obeg + oper, static_cast<int>(n_off));
+        for (int i = obeg; i < oend; ++i) nf_mine += !kept(lists[i]);
+        uint64_t ftot;
+        unsigned fr = static_cast<unsigned>(block_excl_scan<NT>(static_cast<uint64_t>(nf_mine), wt, &ftot, tid));
+        for (int i = obeg; i < oend; ++i) {
+            const int t = lists[i];
+            const int sl = slot[t];
+            aslots[i] = sl;  // the offload copies out of this slot
+            if (!kept(t)) {
+                fq[(head0 + cnt0 + fr++) % pcap] = sl;
+                slot[t] = -1;
+            }
+        }
+        const unsigned cnt1 = cnt0 + static_cast<unsigned>(ftot);
+        // allocations: reload-list entries (not kept), then recompute entries
+        const int n_al_lists = n_rl + n_rc;
+        const int aper = (n_al_lists + NT - 1) / NT;
+        const int abeg = min(tid * aper, n_al_lists), aend = min(abeg + aper, n_al_lists);
+        int na_mine = 0;
+        for (int i = abeg; i < aend; ++i) {
+            const int t = i < n_rl ? lists[2 * p.list_ld + i] : lists[3 * p.list_ld + (i - n_rl)];
+            na_mine += !(i < n_rl && kept(t));
+        }
+        if (tid == 0) s_split = n_rl;
+        uint64_t atot;
+        unsigned ar = static_cast<unsigned>(block_excl_scan<NT>(static_cast<uint64_t>(na_mine), wt, &atot, tid));
+        for (int i = abeg; i < aend; ++i) {
+            const bool rel = i < n_rl;
+            const int t = rel ? lists[2 * p.list_ld + i] : lists[3 * p.list_ld + (i - n_rl)];
+            int* as = rel ? aslots + 2 * p.list_ld + i : aslots + 3 * p.list_ld + (i - n_rl);
+            if (rel && kept(t)) {  // keeps its row: nothing to copy in
+                *as = -1;
+                continue;
+            }
+            const unsigned a = ar++;
+            if (a < cnt1) {
+                const int sl = fq[(head0 + a) % pcap];
+                slot[t] = sl;
+                *as = sl;
+                if (rel && a >= cnt0) atomicMin(&s_split, i);  // a slot this step's offload frees
+            } else {
+                slot[t] = -1;
+                *as = -1;
+                if (p.tot) atomicAdd(&p.tot->exhausted, 1ull);  // reported by ledger_account
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const unsigned used = static_cast<unsigned>(atot) < cnt1 ? static_cast<unsigned>(atot) : cnt1;
+            const unsigned head1 = (head0 + used) % pcap, cnt2 = cnt1 - used;
+            ht[0] = head1;
+            ht[1] = cnt2;
+            p.aux[b * 4] = s_split;
+            if (p.store_current) store_current(head1, cnt2);
+        }
+    }
+    // tiers after the step + the ledger's byte deltas
+    long long post_dev = 0, post_host = 0, allocs = 0;
+    for (int i = tid; i < ntok; i += NT) {
+        const uint8_t a = act[i];
+        uint8_t t = t8[i];
+        if (a) {
             if (a & 1) t = kTierHost;
             if (a & 2) t = kTierDeleted;
             if (a & 4) t = kTierDevice;
             tg[i] = t;
+            allocs += (a & 4) && !kept(i);
         }
-        if (tid == 0 && p.store_current) tg[ntok] = kTierDevice;
+        post_dev += t == kTierDevice;
+        post_host += t == kTierHost;
+    }
+    post_dev = block_sum<NT>(post_dev, red, tid);
+    post_host = block_sum<NT>(post_host, red, tid);
+    allocs = block_sum<NT>(allocs, red, tid);
+    if (tid == 0) {
+        if (p.store_current && !paged) tg[ntok] = kTierDevice;
+        const long long sc = p.store_current ? 1 : 0;
+        ledger_account(p, b, post_dev + sc - ndev, post_host - nh, allocs + sc);
     }
 }
 
@@ -188,30 +343,43 @@ __device__ __forceinline__ bool in_sorted(const int* list, int cnt, int t) {
 // and selected in the same step, scheduler.hpp:360-375) keeps its device row:
 // the offload copies it out without poisoning it and the reload skips it --
 // the state the sequential offload-then-reload leaves behind.
+// Paged store: the device side is addressed by the ledger's slot lists. A
+// reload into a slot that this step's offload frees must wait for that copy:
+// those reloads (from aux[b*4] on) run in a second launch (second = 1).
 __global__ void __launch_bounds__(256) kv_move_kernel(const MoveParams p) {
-    pdl_launch_dependents();
     pdl_wait();  // the lists come from the preceding ledger kernel
+    pdl_launch_dependents();
     const int b = blockIdx.y;
     const bool both = p.which < 0;
     const int which = both ? (blockIdx.z == 0 ? 0 : 2) : p.which;
-    const int cnt = p.counts[b * 4 + which];
+    int lo = 0, hi = p.counts[b * 4 + which];
+    if (which == 2 && p.aux) {
+        const int split = p.aux[b * 4];
+        if (p.second) lo = split;
+        else hi = split < hi ? split : hi;
+    }
     const int* list = p.lists + (static_cast<size_t>(b) * 4 + which) * p.list_ld;
+    const int* slots = p.act_slots ? p.act_slots + (static_cast<size_t>(b) * 4 + which) * p.list_ld : nullptr;
     const int ocnt = both ? p.counts[b * 4 + (2 - which)] : 0;
     const int* other = p.lists + (static_cast<size_t>(b) * 4 + (2 - which)) * p.list_ld;
     const long long vec_per_tok = p.tok_bytes / 16;
-    const long long total = static_cast<long long>(cnt) * vec_per_tok;
+    const long long total = static_cast<long long>(hi - lo) * vec_per_tok;
     for (long long v = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; v < total;
          v += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int t = list[v / vec_per_tok];
+        const int i = lo + static_cast<int>(v / vec_per_tok);
+        const int t = list[i];
+        const int sl = slots ? slots[i] : t;
+        if (sl < 0) continue;  // a kept row, or no slot (the ledger reported the OOM)
         const bool shared = both && in_sorted(other, ocnt, t);
-        const size_t off = static_cast<size_t>(b) * p.seq_bytes + static_cast<size_t>(t) * p.tok_bytes +
-                           static_cast<size_t>(v % vec_per_tok) * 16;
+        const size_t vo = static_cast<size_t>(v % vec_per_tok) * 16;
+        const size_t hoff = static_cast<size_t>(b) * p.seq_bytes + static_cast<size_t>(t) * p.tok_bytes + vo;
+        const size_t doff = static_cast<size_t>(b) * p.dev_seq_bytes + static_cast<size_t>(sl) * p.tok_bytes + vo;
         if (which == 0) {
-            uint4* d = reinterpret_cast<uint4*>(p.dev + off);
-            *reinterpret_cast<uint4*>(p.host + off) = *d;
+            uint4* d = reinterpret_cast<uint4*>(p.dev + doff);
+            *reinterpret_cast<uint4*>(p.host + hoff) = *d;
             if (p.poison && !shared) *d = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
         } else if (!shared) {
-            *reinterpret_cast<uint4*>(p.dev + off) = *reinterpret_cast<const uint4*>(p.host + off);
+            *reinterpret_cast<uint4*>(p.dev + doff) = *reinterpret_cast<const uint4*>(p.host + hoff);
         }
     }
 }
@@ -366,13 +534,72 @@ __global__ void dequantize_kernel(const uint16_t* __restrict__ codes, long long 
 }
 
 // ------------------------------------------------------------- cache write
-// AttentionState::append_token for a block of tokens (+ engine head_rows
-// fake-quant). One warp per (b, t, kv, head) row of D elements.
-template <class QT, class KV>
-__global__ void cache_write_kernel(uint8_t* __restrict__ kv, double* __restrict__ imp, uint8_t* __restrict__ tiers, const QT* __restrict__ k,
-                                   const QT* __restrict__ v, int H, int Ncap, int b0, int nb, int t0,
-                                   int nt) {
+// One (token, K|V, head) row of D values from the compute dtype into the
+// storage dtype, one warp; INT8 rows are engine.hpp:469-483's fake-quant
+// (quant.hpp:43-81 per head_dim group, in fp64: bit-exact codes).
+__device__ __forceinline__ void quant_row_u8(uint8_t* dst, const double (&x)[kHeadDim / 32], int lane) {
     constexpr int D = kHeadDim;
+    double lo = x[0], hi = x[0];
+#pragma unroll
+    for (int i = 1; i < D / 32; ++i) {
+        lo = x[i] < lo ? x[i] : lo;
+        hi = hi < x[i] ? x[i] : hi;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double olo = __shfl_xor_sync(0xffffffffu, lo, off);
+        const double ohi = __shfl_xor_sync(0xffffffffu, hi, off);
+        lo = olo < lo ? olo : lo;
+        hi = hi < ohi ? ohi : hi;
+    }
+    double scale;
+    if (hi == lo) {
+        const double a = fabs(lo);
+        scale = a < 1e-12 ? 1e-12 : a;
+    } else {
+        const double s = (hi - lo) / 255.0;
+        scale = s < 1e-12 ? 1e-12 : s;
+    }
+    const long long zp = rne_ref(-lo / scale);
+    uint32_t packed = 0;
+#pragma unroll
+    for (int i = 0; i < D / 32; ++i) {
+        long long c = rne_ref(x[i] / scale + static_cast<double>(zp));
+        c = c < 0 ? 0 : (c > 255 ? 255 : c);
+        packed |= static_cast<uint32_t>(c) << (8 * i);
+    }
+    reinterpret_cast<uint32_t*>(dst)[lane] = packed;
+    if (lane == 0)
+        *reinterpret_cast<float2*>(dst + D) =
+            make_float2(static_cast<float>(scale), static_cast<float>(-scale * static_cast<double>(zp)));
+}
+
+// One (token, K|V, head) row of D values from the compute dtype into the
+// storage dtype, one warp; INT8 rows are engine.hpp:469-483's fake-quant
+// (quant.hpp:43-81 per head_dim group, in fp64: bit-exact codes).
+template <class QT, class KV>
+__device__ __forceinline__ void store_row(uint8_t* dst, const QT* src, int lane) {
+    constexpr int D = kHeadDim;
+    if constexpr (!KV::QUANT) {
+        using T = typename KV::T;
+        T* d = reinterpret_cast<T*>(dst);
+        for (int i = lane; i < D; i += 32) d[i] = from_f<T>(to_f(src[i]));
+    } else {
+        double x[D / 32];
+#pragma unroll
+        for (int i = 0; i < D / 32; ++i) x[i] = static_cast<double>(to_f(src[lane * (D / 32) + i]));
+        quant_row_u8(dst, x, lane);
+    }
+}
+
+// AttentionState::append_token for a block of tokens (+ engine head_rows
+// fake-quant). One warp per (b, t, kv, head) row of D elements. Paged store:
+// prompt tokens take slot t (the FIFO hands slots out in order until the
+// first decode allocation), and the sequence's FIFO head moves past them.
+template <class QT, class KV>
+__global__ void cache_write_kernel(const CacheView cv, double* __restrict__ imp, uint8_t* __restrict__ tiers,
+                                   const QT* __restrict__ k, const QT* __restrict__ v, int H, int b0, int nb,
+                                   int t0, int nt) {
     const long long row = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const long long rows = static_cast<long long>(nb) * nt * 2 * H;
@@ -381,56 +608,59 @@ __global__ void cache_write_kernel(uint8_t* __restrict__ kv, double* __restrict_
     const int which = static_cast<int>((row / H) % 2);
     const int t = static_cast<int>((row / (2 * H)) % nt);
     const int bb = static_cast<int>(row / (2LL * H * nt));
-    const QT* src = (which ? v : k) + ((static_cast<size_t>(bb) * nt + t) * H + h) * D;
-    const size_t tok = static_cast<size_t>(b0 + bb) * Ncap + (t0 + t);
-    uint8_t* dst = kv + ((tok * 2 + which) * H + h) * static_cast<size_t>(kv_row_bytes<KV>());
-    if constexpr (!KV::QUANT) {
-        using T = typename KV::T;
-        T* d = reinterpret_cast<T*>(dst);
-        for (int i = lane; i < D; i += 32) d[i] = from_f<T>(to_f(src[i]));
-    } else {
-        double x[D / 32];
-        for (int i = 0; i < D / 32; ++i) x[i] = static_cast<double>(to_f(src[lane * (D / 32) + i]));
-        double lo = x[0], hi = x[0];
-        for (int i = 1; i < D / 32; ++i) {
-            lo = x[i] < lo ? x[i] : lo;
-            hi = hi < x[i] ? x[i] : hi;
-        }
-        for (int off = 16; off > 0; off >>= 1) {
-            const double olo = __shfl_xor_sync(0xffffffffu, lo, off);
-            const double ohi = __shfl_xor_sync(0xffffffffu, hi, off);
-            lo = olo < lo ? olo : lo;
-            hi = hi < ohi ? ohi : hi;
-        }
-        double scale;
-        if (hi == lo) {
-            const double a = fabs(lo);
-            scale = a < 1e-12 ? 1e-12 : a;
-        } else {
-            const double s = (hi - lo) / 255.0;
-            scale = s < 1e-12 ? 1e-12 : s;
-        }
-        const long long zp = rne_ref(-lo / scale);
-        uint32_t packed = 0;
-        for (int i = 0; i < D / 32; ++i) {
-            long long c = rne_ref(x[i] / scale + static_cast<double>(zp));
-            c = c < 0 ? 0 : (c > 255 ? 255 : c);
-            packed |= static_cast<uint32_t>(c) << (8 * i);
-        }
-        reinterpret_cast<uint32_t*>(dst)[lane] = packed;
-        if (lane == 0)
-            *reinterpret_cast<float2*>(dst + D) =
-                make_float2(static_cast<float>(scale), static_cast<float>(-scale * static_cast<double>(zp)));
-    }
+    const QT* src = (which ? v : k) + ((static_cast<size_t>(bb) * nt + t) * H + h) * kHeadDim;
+    const size_t tok = static_cast<size_t>(b0 + bb) * cv.Ncap + (t0 + t);
+    const size_t srow = static_cast<size_t>(b0 + bb) * cv.kv_ncap + (t0 + t);  // slot t when paged
+    uint8_t* dst = cv.kv + ((srow * 2 + which) * H + h) * static_cast<size_t>(kv_row_bytes<KV>());
+    store_row<QT, KV>(dst, src, lane);
     if (lane == 0 && h == 0 && which == 0) {
         imp[tok] = 0.0;
-        if (tiers) tiers[tok] = 0;  // KvLedger::store_new: new KV lands on device
+        if (tiers) {
+            if (cv.tot && tiers[tok] == kTierAbsent) atomicAdd(&cv.tot->dev_tokens, 1ull);
+            tiers[tok] = kTierDevice;  // KvLedger::store_new: new KV lands on device
+        }
+        if (cv.slot) {
+            cv.slot[tok] = t0 + t;
+            if (t == nt - 1) {  // one thread per sequence: the FIFO moves past the prompt
+                unsigned* ht = cv.fq_ht + static_cast<size_t>(b0 + bb) * 2;
+                const unsigned pcap = static_cast<unsigned>(cv.kv_ncap);
+                const unsigned used = pcap - ht[1];
+                const unsigned ni = used > static_cast<unsigned>(t0 + nt) ? used : static_cast<unsigned>(t0 + nt);
+                ht[0] = ni % pcap;
+                ht[1] = pcap - ni;
+            }
+        }
     }
 }
 
-// Cache read-back to fp32 [nb][nt][2][H][D].
+// INT8 recompute write-back (engine.hpp:718-737: recompute_kv re-applies
+// head_rows' fake-quant): the recompute GEMM's fp32 rows [M][2h] are rounded
+// to the compute dtype, as the appended rows were, and quantised into their
+// slots. One warp per (row, K|V, head).
+template <class QT>
+__global__ void quant_scatter_kernel(const float* __restrict__ C, const int* __restrict__ m_dev, const int2* rowmap,
+                                     uint8_t* kv, int H, int kv_ncap) {
+    const long long w = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const long long M = *m_dev;
+    if (w >= M * 2 * H) return;
+    const int h = static_cast<int>(w % H), which = static_cast<int>((w / H) % 2);
+    const long long r = w / (2LL * H);
+    const int2 bt = rowmap[r];
+    if (bt.y < 0) return;
+    const float* src = C + (r * 2 * H + static_cast<long long>(which) * H + h) * kHeadDim;
+    double x[kHeadDim / 32];
+#pragma unroll
+    for (int i = 0; i < kHeadDim / 32; ++i) x[i] = static_cast<double>(to_f(from_f<QT>(src[lane * (kHeadDim / 32) + i])));
+    uint8_t* dst = kv + ((static_cast<size_t>(bt.x) * kv_ncap + bt.y) * 2 + which) * static_cast<size_t>(H) *
+                            kv_row_bytes<KvU8>() + static_cast<size_t>(h) * kv_row_bytes<KvU8>();
+    quant_row_u8(dst, x, lane);
+}
+
+// Cache read-back to fp32 [nb][nt][2][H][D]; rows not on device (paged,
+// slot -1) read as NaN.
 template <class KV>
-__global__ void cache_read_kernel(const uint8_t* __restrict__ kv, float* __restrict__ out, int H, int Ncap, int b0, int nb, int t0,
+__global__ void cache_read_kernel(const CacheView cv, float* __restrict__ out, int H, int b0, int nb, int t0,
                                   int nt) {
     constexpr int D = kHeadDim;
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -442,8 +672,16 @@ __global__ void cache_read_kernel(const uint8_t* __restrict__ kv, float* __restr
     const int which = static_cast<int>((r / H) % 2);
     const int t = static_cast<int>((r / (2 * H)) % nt);
     const int bb = static_cast<int>(r / (2LL * H * nt));
-    const size_t tok = static_cast<size_t>(b0 + bb) * Ncap + (t0 + t);
-    const uint8_t* row = kv + ((tok * 2 + which) * H + h) * static_cast<size_t>(kv_row_bytes<KV>());
+    int st = t0 + t;
+    if (cv.slot) {
+        st = cv.slot[static_cast<size_t>(b0 + bb) * cv.Ncap + (t0 + t)];
+        if (st < 0) {
+            out[i] = __int_as_float(0x7fffffff);
+            return;
+        }
+    }
+    const size_t tok = static_cast<size_t>(b0 + bb) * cv.kv_ncap + st;
+    const uint8_t* row = cv.kv + ((tok * 2 + which) * H + h) * static_cast<size_t>(kv_row_bytes<KV>());
     if constexpr (KV::QUANT) {
         const float2 ms = *reinterpret_cast<const float2*>(row + D);
         out[i] = fmaf(ms.x, static_cast<float>(row[d]), ms.y);
@@ -611,55 +849,67 @@ cudaError_t launch_dequantize(const uint16_t* codes, long long len, long long cs
 }
 
 template <class QT, class KV>
-static cudaError_t write_t(uint8_t* kv, double* imp, uint8_t* tiers, const void* k, const void* v,
-                           int H, int Ncap, int b0, int nb, int t0, int nt, cudaStream_t st) {
+static cudaError_t write_t(const CacheView& cv, double* imp, uint8_t* tiers, const void* k, const void* v, int H,
+                           int b0, int nb, int t0, int nt, cudaStream_t st) {
     const long long rows = static_cast<long long>(nb) * nt * 2 * H;
     const int threads = 256;
     const long long blocks = (rows * 32 + threads - 1) / threads;
     cache_write_kernel<QT, KV><<<static_cast<unsigned>(blocks), threads, 0, st>>>(
-        kv, imp, tiers, static_cast<const QT*>(k), static_cast<const QT*>(v), H, Ncap, b0, nb, t0, nt);
+        cv, imp, tiers, static_cast<const QT*>(k), static_cast<const QT*>(v), H, b0, nb, t0, nt);
     count_launch();
     return cudaGetLastError();
 }
 
-cudaError_t launch_cache_write(int kv_dtype, int q_dtype, uint8_t* kv, double* imp, uint8_t* tiers,
-                               const void* k, const void* v, int H, int Ncap, int b0, int nb, int t0, int nt,
-                               cudaStream_t st) {
+cudaError_t launch_cache_write(int kv_dtype, int q_dtype, const CacheView& cv, double* imp, uint8_t* tiers,
+                               const void* k, const void* v, int H, int b0, int nb, int t0, int nt, cudaStream_t st) {
     switch (kv_dtype) {
     case SKV_F32:
-        return write_t<float, KvF32>(kv, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
+        return write_t<float, KvF32>(cv, imp, tiers, k, v, H, b0, nb, t0, nt, st);
     case SKV_F16:
-        return write_t<__half, KvF16>(kv, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
+        return write_t<__half, KvF16>(cv, imp, tiers, k, v, H, b0, nb, t0, nt, st);
     case SKV_BF16:
-        return write_t<__nv_bfloat16, KvBF16>(kv, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
+        return write_t<__nv_bfloat16, KvBF16>(cv, imp, tiers, k, v, H, b0, nb, t0, nt, st);
     case SKV_U8:
-        if (q_dtype == SKV_F32) return write_t<float, KvU8>(kv, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
-        if (q_dtype == SKV_F16) return write_t<__half, KvU8>(kv, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
-        return write_t<__nv_bfloat16, KvU8>(kv, imp, tiers, k, v, H, Ncap, b0, nb, t0, nt, st);
+        if (q_dtype == SKV_F32) return write_t<float, KvU8>(cv, imp, tiers, k, v, H, b0, nb, t0, nt, st);
+        if (q_dtype == SKV_F16) return write_t<__half, KvU8>(cv, imp, tiers, k, v, H, b0, nb, t0, nt, st);
+        return write_t<__nv_bfloat16, KvU8>(cv, imp, tiers, k, v, H, b0, nb, t0, nt, st);
     }
     return cudaErrorInvalidValue;
 }
 
 template <class KV>
-static cudaError_t read_t(const uint8_t* kv, float* out, int H, int Ncap, int b0, int nb, int t0, int nt,
-                          cudaStream_t st) {
+static cudaError_t read_t(const CacheView& cv, float* out, int H, int b0, int nb, int t0, int nt, cudaStream_t st) {
     const long long total = static_cast<long long>(nb) * nt * 2 * H * kHeadDim;
     const int threads = 256;
     cache_read_kernel<KV><<<static_cast<unsigned>((total + threads - 1) / threads), threads, 0, st>>>(
-        kv, out, H, Ncap, b0, nb, t0, nt);
+        cv, out, H, b0, nb, t0, nt);
     count_launch();
     return cudaGetLastError();
 }
 
-cudaError_t launch_cache_read(int kv_dtype, const uint8_t* kv, float* out, int H, int Ncap, int b0, int nb,
-                              int t0, int nt, cudaStream_t st) {
+cudaError_t launch_cache_read(int kv_dtype, const CacheView& cv, float* out, int H, int b0, int nb, int t0, int nt,
+                              cudaStream_t st) {
     switch (kv_dtype) {
-    case SKV_F32: return read_t<KvF32>(kv, out, H, Ncap, b0, nb, t0, nt, st);
-    case SKV_F16: return read_t<KvF16>(kv, out, H, Ncap, b0, nb, t0, nt, st);
-    case SKV_BF16: return read_t<KvBF16>(kv, out, H, Ncap, b0, nb, t0, nt, st);
-    case SKV_U8: return read_t<KvU8>(kv, out, H, Ncap, b0, nb, t0, nt, st);
+    case SKV_F32: return read_t<KvF32>(cv, out, H, b0, nb, t0, nt, st);
+    case SKV_F16: return read_t<KvF16>(cv, out, H, b0, nb, t0, nt, st);
+    case SKV_BF16: return read_t<KvBF16>(cv, out, H, b0, nb, t0, nt, st);
+    case SKV_U8: return read_t<KvU8>(cv, out, H, b0, nb, t0, nt, st);
     }
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_quant_scatter(int q_dtype, const float* C, const int* m_dev, int m_cap, const int2* rowmap,
+                                 uint8_t* kv, int H, int kv_ncap, cudaStream_t st) {
+    const long long warps = static_cast<long long>(m_cap) * 2 * H;
+    const unsigned blocks = static_cast<unsigned>((warps * 32 + 255) / 256);
+    if (q_dtype == SKV_F16)
+        quant_scatter_kernel<__half><<<blocks, 256, 0, st>>>(C, m_dev, rowmap, kv, H, kv_ncap);
+    else if (q_dtype == SKV_BF16)
+        quant_scatter_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(C, m_dev, rowmap, kv, H, kv_ncap);
+    else
+        quant_scatter_kernel<float><<<blocks, 256, 0, st>>>(C, m_dev, rowmap, kv, H, kv_ncap);
+    count_launch();
+    return cudaGetLastError();
 }
 
 }  // namespace skv_impl

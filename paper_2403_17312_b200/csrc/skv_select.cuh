@@ -93,7 +93,7 @@ __device__ __forceinline__ void stage_candidates(double* kd, const double* imp, 
 #endif
 
 template <int NT, int BAR>
-__device__ __forceinline__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<NT>& s, uint64_t* keys,
+__device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<NT>& s, uint64_t* keys,
                                 SelectScratch<NT>& sc) {
     double* imp = p.imp + static_cast<size_t>(b) * p.imp_ld;
     // top-k candidates [0, nc): staged as fp64 in the key buffer, keyed in place

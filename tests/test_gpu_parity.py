@@ -264,13 +264,28 @@ def test_decode_trajectory_config4_full_length(api, port):
     assert stats["max_err_over_tol"] < 0.5, stats
 
 
-def test_decode_trajectory_bf16_outputs(api, port):
-    """Config 3 as benchmarked: bf16 cache, bf16 OUTPUTS (no out_f32). bf16
-    rounding of the output (2^-9 of the element) fits the north_star bound
-    |g - r| <= 1e-3 (|r| + max|r|) since max|r| >= |r|."""
-    stats = {}
-    run_trajectory(api, port, "bf16", 2, 40, 1024, 4, 0.2, seed=1313, out_f32=False, stats=stats)
-    assert stats["max_err_over_tol"] < 1.0, stats
+def test_decode_bf16_outputs_are_rounded_f32_outputs(api):
+    """bf16 outputs differ from the fp32-output path only by the final
+    rounding (bit-exact): bf16 keeps 8 significant bits, so a bf16 output
+    alone can sit 2^-9..2^-8 of the element off -- beyond the north_star's
+    1e-3 -- which is why bench.py's config 3 (bf16) reports fp32 outputs
+    (out_f32, checked against the oracle in test_decode_trajectory)."""
+    g = torch.Generator(device="cuda").manual_seed(33)
+    B, H, D, s, steps = 4, 40, 128, 300, 4
+    caches = [api.SwaCache(1, B, H, D, s + steps, kv_dtype="bf16", out_f32=f) for f in (True, False)]
+    kv = torch.randn((B, s + steps, 2, H, D), generator=g, device="cuda").bfloat16()
+    q0 = torch.randn((B, H, D), generator=g, device="cuda").bfloat16()
+    for c in caches:
+        c.append_tokens(0, 0, 0, kv[:, :s, 0].contiguous(), kv[:, :s, 1].contiguous())
+        c.prefill_seed(0, s, q0)
+    for j in range(steps):
+        n = s + j + 1
+        q = torch.randn((B, H, D), generator=g, device="cuda").bfloat16()
+        kn, vn = kv[:, n - 1, 0].contiguous(), kv[:, n - 1, 1].contiguous()
+        o32 = caches[0].swa_decode_layer(0, n, 0.2, q, kn, vn)[0]
+        o16 = caches[1].swa_decode_layer(0, n, 0.2, q, kn, vn)[0]
+        assert o32.dtype == torch.float32 and o16.dtype == torch.bfloat16
+        assert torch.equal(o32.bfloat16(), o16)
 
 
 def test_decode_trajectory_u8_f32_query(api, port):
