@@ -327,30 +327,138 @@ def run_reference(args, cfg, rank: int, world: int):
     print(json.dumps(line), flush=True)
 
 
-def schedule_estimate(plan: dict, phases: dict, out_len: int, seqs: int) -> dict:
-    """The whole out_len-step decode under solve_plan's schedule (steps
-    [0, p1) Phase I, [p1, p2) Phase II, [p2, n) Phase III), priced with the
-    per-step times measured above from step 0 of each phase. An estimate: a
-    step's cost grows with the context, and the phases are timed at its start."""
-    p1 = min(int(plan.get("p1", out_len)), out_len)
-    p2 = min(max(int(plan.get("p2", out_len)), p1), out_len)
-    if not plan.get("recompute_enabled", True):  # phase_of_step: no Phase III without recomputation
-        p2 = out_len
-    spans = {"phase1": p1, "phase2": p2 - p1, "phase3": out_len - p2}
-    sec = sum(spans[k] * phases[k]["ms_per_step"] / 1000.0 for k in spans if spans[k] and k in phases)
-    return {"steps_per_phase": spans, "est_decode_seconds": sec,
-            "est_tokens_per_s": seqs * out_len / sec if sec > 0 else None,
-            "note": "per-phase step times from this run x solve_plan's phase lengths (start-of-phase costs)"}
+def phase_of_step(plan: dict, j: int) -> int:
+    """scheduler.hpp:52-60."""
+    if j < plan["p1"]:
+        return 1
+    if j < plan["p2"] or not plan.get("recompute_enabled", True):
+        return 2
+    return 3
+
+
+def fit_mac_rate(points) -> dict:
+    """bench.hpp:44-68 fit_mac_rate: least squares of t ~= M / rate over
+    (MACs, seconds) points, minimised over x = 1 / rate."""
+    sxx = sum(m * m for m, _ in points)
+    sxt = sum(m * t for m, t in points)
+    x = sxt / sxx
+    res = [abs(t - m * x) for m, t in points]
+    return {"fitted_mac_rate": 1.0 / x, "points": [{"macs": m, "seconds": t} for m, t in points],
+            "max_residual_s": max(res), "max_residual_rel": max(r / t for r, (_, t) in zip(res, points))}
+
+
+def calibrate_costs(api, torch, cfg, g) -> dict:
+    """CostParams from this GPU:
+    * mac_rate by the reference's own recipe (bench.hpp:84-108 bench_mac_rate):
+      Dense decodes (r = 1) timed at several KV lengths, attention MACs
+      2 b l h kept per step (memsim.hpp:57-62), fit t ~ M / rate;
+    * bandwidth: the duplex movement kernel (offload + reload rows in one
+      launch, as a Phase II step moves them), bytes both ways / time -- the
+      reference charges transfer_time on d2h + h2d tokens (memsim.hpp:50-54)."""
+    B, H = cfg["B"], cfg["H"]
+    h = H * D
+    Lc, steps = 2, 6
+    points = []
+    for s_i in (512, 1024, 2048):
+        c = api.SwaCache(Lc, B, H, D, s_i + steps + 2, kv_dtype="f16")
+        c.set_variant("dense")
+        for l in range(Lc):
+            kp = torch.randn((B, s_i, H, D), generator=g, device="cuda", dtype=torch.float16)
+            c.append_tokens(l, 0, 0, kp, torch.randn_like(kp))
+            c.prefill_seed(l, s_i, torch.randn((B, H, D), generator=g, device="cuda", dtype=torch.float16))
+        q, k, v = (torch.randn((Lc, B, H, D), generator=g, device="cuda", dtype=torch.float16) for _ in range(3))
+        out = torch.empty_like(q)
+        c.swa_decode_step(s_i + 1, 1.0, q, k, v, out)  # warm-up
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        macs = 0.0
+        for j in range(1, steps):
+            n = s_i + 1 + j
+            c.swa_decode_step(n, 1.0, q, k, v, out)
+            macs += 2.0 * B * Lc * h * n  # dense: kept = n
+        e1.record()
+        torch.cuda.synchronize()
+        points.append((macs, e0.elapsed_time(e1) / 1000.0))
+        c.close()
+    fit = fit_mac_rate(points)
+    rows, s_m = 256, 1024
+    c = api.SwaCache(1, B, H, D, s_m, kv_dtype="f16")
+    kp = torch.randn((B, s_m, H, D), generator=g, device="cuda", dtype=torch.float16)
+    c.append_tokens(0, 0, 0, kp, torch.randn_like(kp))
+    c.enable_host_tier(poison=False)
+    ms = c.profile_move(0, rows, reps=5)
+    c.close()
+    moved = 2 * rows * B * (2 * H * D * 2)
+    return {"mac_rate": fit["fitted_mac_rate"], "bandwidth": moved / (ms / 1000.0), "mac_fit": fit,
+            "bandwidth_probe": {"rows_each_way_per_seq": rows, "seqs": B, "bytes": moved, "ms": ms,
+                                "kernel": "skvd::kv_move_kernel (offload + reload in one launch)"}}
+
+
+def run_schedule(api, torch, cfg, plan: dict, out_len: int, budget: int, shared: dict, g) -> dict:
+    """Execute one schedule end to end on a PAGED cache whose device K/V pool
+    is bounded by the budget (skv_cache_create_paged): tensor-core prefill,
+    then out_len decode steps; every step runs step_actions + apply_actions on
+    the device ledger, moves the listed rows over PCIe, recomputes deleted
+    selected tokens on the tcgen05 GEMM, and frees / allocates pool slots.
+    Per-step CUDA events give the measured seconds per phase."""
+    L, B, H, s = cfg["L"], cfg["B"], cfg["H"], cfg["s"]
+    ncap = s + out_len + 1
+    x, wk, wv, qin = shared["x"], shared["wk"], shared["wv"], shared["qin"]
+    cache = api.SwaCache(L, B, H, D, ncap, kv_dtype="f16", device_capacity=budget)
+    cache.enable_host_tier(poison=False)
+    for l in range(L):
+        xs = x[l][:, :s]
+        cache.append_tokens(l, 0, 0, (xs @ wk[l]).reshape(B, s, H, D), (xs @ wv[l]).reshape(B, s, H, D))
+        cache.prefill_layer(l, torch.randn((B, s, H, D), generator=g, device="cuda", dtype=torch.float16) * 0.5)
+        cache.attach_recompute(l, x[l], wk[l], wv[l])
+    cache.set_plan(plan["alpha"] or 0.5, plan["beta"] or 0.5, plan["p1"], plan["p2"], s, out_len,
+                   recompute_enabled=plan.get("recompute_enabled", True))
+    out = torch.empty((L, B, H, D), device="cuda", dtype=torch.float16)
+    torch.cuda.synchronize()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(out_len + 1)]
+    counters = {0: cache.ledger_counters()}
+    evs[0].record()
+    for j in range(out_len):
+        n = s + j + 1
+        q, k, v = qin[j % len(qin)]
+        cache.swa_decode_step(n, RATIO, q, k, v, out)
+        evs[j + 1].record()
+        if j + 1 in (plan["p1"], plan["p2"]):  # phase boundary: the rows moved so far
+            counters[j + 1] = cache.ledger_counters()
+    torch.cuda.synchronize()
+    counters[out_len] = cache.ledger_counters()
+    tot = cache.ledger_totals()
+    stor = cache.storage()
+    step_s = [evs[j].elapsed_time(evs[j + 1]) / 1000.0 for j in range(out_len)]
+    phases = {}
+    for j, t in enumerate(step_s):
+        ph = phases.setdefault(phase_of_step(plan, j), {"steps": 0, "measured_s": 0.0})
+        ph["steps"] += 1
+        ph["measured_s"] += t
+    marks = sorted(counters)
+    for a, b in zip(marks, marks[1:]):
+        if b > a:
+            ph = phases[phase_of_step(plan, a)]
+            for key in ("offloaded", "deleted", "reloaded", "recomputed"):
+                ph[key + "_rows"] = ph.get(key + "_rows", 0) + counters[b][key] - counters[a][key]
+    cache.close()
+    del cache
+    torch.cuda.empty_cache()
+    return {"phases": phases, "decode_s": sum(step_s), "ledger": tot, "storage": stor}
 
 
 def run_config5(args, cfg, rank: int, world: int):
     """BASELINE config 5: the three-phase caching / eviction / recomputation
-    schedule. solve_plan (host, scheduler.hpp:207-303) picks (alpha, beta, p1,
-    p2) for the device KV budget; then each phase is timed on its own from the
-    same prompt state: Phase I (all device), Phase II (offload to the pinned
-    host tier + reloads, from step 0) and Phase III (plus deletion and tcgen05
-    recomputation of selected deleted tokens). Every step runs the device
-    ledger (step_actions + apply_actions) and moves the listed rows."""
+    schedule, executed and checked against its own prediction.
+    1. CostParams calibrated on this GPU (calibrate_costs).
+    2. solve_plan (host, scheduler.hpp:207-303) for the per-GPU KV budget.
+    3. The solved plan runs the whole decode on a paged cache whose device
+       K/V pool is the budget (smaller than the full KV), and the measured
+       seconds per phase are set beside PlanPrediction's (scheduler.hpp:75-81).
+    4. Unless the solved plan already has a Phase III, the same (alpha, beta)
+       with p2 halfway through the offload phase runs too (predict_plan),
+       so eviction and tcgen05 recomputation are measured as well."""
     import torch
 
     from paper_2403_17312_b200 import api
@@ -358,80 +466,69 @@ def run_config5(args, cfg, rank: int, world: int):
 
     L, B, H, s = cfg["L"], cfg["B"], cfg["H"], cfg["s"]
     h = H * D
-    W, K = args.warmup, args.steps
-    ncap = s + W + K + 2
-    qdt = torch.float16
-    budget = int(cfg["budget_gb"] * 1e9)
-    cost = dict(hidden=h, layers=L, batch=B, input_len=s, output_len=cfg["out_len"], ratio=RATIO,
-                bandwidth=47e9, bytes_per_element=2, device_capacity=budget, mac_rate=peaks()[0] * 1e9 / 2,
-                recompute_overhead=1.0)
-    plan, pred = api.solve_plan(cost)
+    out_len = args.decode_len or cfg["out_len"]
+    budget = int((args.budget_gb or cfg["budget_gb"]) * 1e9)
     g = torch.Generator(device="cuda").manual_seed(2403_17312 + 5000 + rank)
-    # retained post-LN1 rows and the K/V projections, so recomputation re-derives
-    # exactly the stored K/V (engine.hpp:718-737)
-    x = [torch.randn((B, ncap, h), generator=g, device="cuda", dtype=qdt) for _ in range(L)]
-    wk = [(torch.randn((h, h), generator=g, device="cuda") / h ** 0.5).to(qdt) for _ in range(L)]
-    wv = [(torch.randn((h, h), generator=g, device="cuda") / h ** 0.5).to(qdt) for _ in range(L)]
-    qin = [torch.randn((L, B, H, D), generator=g, device="cuda", dtype=qdt) for _ in range(4)]
-
-    def kv_of(l, t0, t1):
-        xs = x[l][:, t0:t1]
-        return ((xs @ wk[l]).reshape(B, t1 - t0, H, D).contiguous(), (xs @ wv[l]).reshape(B, t1 - t0, H, D).contiguous())
-
-    knew = [torch.stack([kv_of(l, s + i, s + i + 1)[0][:, 0] for l in range(L)]) for i in range(W + K)]
-    vnew = [torch.stack([kv_of(l, s + i, s + i + 1)[1][:, 0] for l in range(L)]) for i in range(W + K)]
-    out = torch.empty((L, B, H, D), device="cuda", dtype=qdt)
-    phases = {}
-    for phase in (1, 2, 3):
-        cache = api.SwaCache(L, B, H, D, ncap, kv_dtype="f16")
-        for l in range(L):
-            kp, vp = kv_of(l, 0, s)
-            cache.append_tokens(l, 0, 0, kp, vp)
-            del kp, vp
-            # Engine::prefill's attention on the tensor cores seeds the importance
-            cache.prefill_layer(l, torch.randn((B, s, H, D), generator=g, device="cuda", dtype=qdt) * 0.5)
-        if phase > 1:
-            cache.enable_host_tier(poison=False)
-            for l in range(L):
-                cache.attach_recompute(l, x[l], wk[l], wv[l])
-            # the phase under test from step 0 (p1 = 0); Phase III from step 1 on
-            cache.set_plan(plan["alpha"] or 0.5, plan["beta"] or 0.5, 0, W + K if phase == 2 else 1, s, W + K,
-                           recompute_enabled=True)
-        n = s
-        for i in range(W):
-            n += 1
-            cache.swa_decode_step(n, RATIO, qin[i % 4], knew[i], vnew[i], out)
-        torch.cuda.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        moved = recomputed = 0
-        e0.record()
-        for i in range(W, W + K):
-            n += 1
-            cache.swa_decode_step(n, RATIO, qin[i % 4], knew[i], vnew[i], out)
-        e1.record()
-        torch.cuda.synchronize()
-        ms = max_over_ranks(e0.elapsed_time(e1), device="cuda")  # the slowest rank
-        if phase > 1:
-            acts = [cache.last_actions(l) for l in range(L)]
-            moved = sum(len(a["offload"]) + len(a["reload"]) for al in acts for a in al)
-            recomputed = sum(len(a["recompute"]) for al in acts for a in al)
-        phases[f"phase{phase}"] = {"tokens_per_s": world * B * K / (ms / 1000.0), "ms_per_step": ms / K,
-                                   "last_step_moved_rows": moved, "last_step_recomputed_rows": recomputed}
-        cache.close()
-        del cache
-        torch.cuda.empty_cache()
+    cal = calibrate_costs(api, torch, cfg, g)
+    cost = dict(hidden=h, layers=L, batch=B, input_len=s, output_len=out_len, ratio=RATIO,
+                bandwidth=cal["bandwidth"], bytes_per_element=2, device_capacity=budget,
+                mac_rate=cal["mac_rate"], recompute_overhead=1.0)
+    t0 = time.perf_counter()
+    plan, pred = api.solve_plan(cost)
+    solve_s = time.perf_counter() - t0
+    runs = [("solved", plan, pred)]
+    if plan["p2"] >= out_len and plan["p1"] < out_len:
+        p3 = dict(plan, p2=plan["p1"] + (out_len - plan["p1"]) // 2, recompute_enabled=True)
+        runs.append(("with_phase3", p3, api.predict_plan(cost, p3)))
+    shared = {
+        # retained post-LN1 rows and the K/V projections (recompute_kv, engine.hpp:718-737)
+        "x": [torch.randn((B, s + out_len + 1, h), generator=g, device="cuda", dtype=torch.float16)
+              for _ in range(L)],
+        "wk": [(torch.randn((h, h), generator=g, device="cuda") / h ** 0.5).half() for _ in range(L)],
+        "wv": [(torch.randn((h, h), generator=g, device="cuda") / h ** 0.5).half() for _ in range(L)],
+        "qin": [tuple(torch.randn((L, B, H, D), generator=g, device="cuda", dtype=torch.float16) for _ in range(3))
+                for _ in range(4)],
+    }
+    results = {}
+    for name, pl, pr in runs:
+        res = run_schedule(api, torch, cfg, pl, out_len, budget, shared, g)
+        res["decode_s"] = max_over_ranks(res["decode_s"], device="cuda")
+        table = {}
+        for ph in (1, 2, 3):
+            got = res["phases"].get(ph)
+            if not got:
+                continue
+            want = pr["phase_compute"][ph - 1] + pr["phase_transfer"][ph - 1] + pr["phase_recompute"][ph - 1]
+            table[f"phase{ph}"] = dict(got, predicted_s=want, predicted_compute_s=pr["phase_compute"][ph - 1],
+                                       predicted_transfer_s=pr["phase_transfer"][ph - 1],
+                                       predicted_recompute_s=pr["phase_recompute"][ph - 1],
+                                       predicted_steps=pr["phase_steps"][ph - 1],
+                                       rel_error=(got["measured_s"] - want) / want if want else None,
+                                       tokens_per_s=world * B * got["steps"] / got["measured_s"])
+        results[name] = {"plan": pl, "predicted_total_decode_s": pr["total_seconds"] - pr["prefill_compute_seconds"],
+                         "measured_decode_s": res["decode_s"],
+                         "tokens_per_s": world * B * out_len / res["decode_s"], "phases": table,
+                         "device_bytes_peak": res["ledger"]["peak_device_bytes"],
+                         "device_capacity": res["ledger"]["capacity"], "host_bytes_end": res["ledger"]["host_bytes"],
+                         "kv_pool_bytes": res["storage"]["kv_pool_bytes"],
+                         "full_kv_bytes": res["storage"]["full_kv_bytes"]}
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, s + out_len // 2)
     if rank == 0:
-        line = {"metric": METRIC, "value": phases["phase1"]["tokens_per_s"], "unit": UNIT, "n_gpus": world,
-                "steps": K, "warmup": W, "ms_per_step": phases["phase1"]["ms_per_step"], "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f16", "data": "synthetic (seeded randn x, Wk, Wv)",
+        head = results["solved"]
+        line = {"metric": METRIC, "value": head["tokens_per_s"], "unit": UNIT, "n_gpus": world,
+                "steps": out_len, "warmup": args.warmup, "ms_per_step": 1000.0 * head["measured_decode_s"] / out_len,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+                "data": "synthetic (seeded randn x, Wk, Wv, q/k/v)",
                 "config": {"workload": cfg["name"], "per_gpu_batch": B, "global_batch": world * B,
-                           "device_kv_budget_bytes": budget, "plan": plan, "predicted": pred,
-                           "note": "value = Phase I; Phase II/III time the same steps with the host tier, "
-                                   "movement and tcgen05 recomputation active from step 0"},
-                "phases": phases,
-                "schedule": schedule_estimate(plan, phases, cfg["out_len"], world * B)}
+                           "decode_steps": out_len, "device_kv_budget_bytes": budget,
+                           "timing": "the whole decode (every step timed with CUDA events; warm-up = the "
+                                     "calibration runs before it)"},
+                "calibration": cal, "cost_params": cost, "solve_plan_s": solve_s, "schedules": results,
+                "cpu_baseline": cpu,
+                "note": "value = the solved schedule's decode tokens/s on a paged device KV bounded by the "
+                        "budget; schedules[*].phases set measured seconds beside PlanPrediction's"}
         print(json.dumps(line), flush=True)
 
 
@@ -452,6 +549,8 @@ def main():
     ap.add_argument("--no-centre", action="store_true",
                     help="time the first K decode steps instead of centring them on the config's decode")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no clocks/baseline/e2e)")
+    ap.add_argument("--decode-len", type=int, default=0, help="config 5: decode steps (default: the config's n)")
+    ap.add_argument("--budget-gb", type=float, default=0.0, help="config 5: device KV budget (default: the config's)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = CONFIGS[args.config]

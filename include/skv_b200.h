@@ -98,6 +98,16 @@ skv_status skv_cache_set_capacity(skv_cache* cache, uint64_t device_capacity);
  * entry point also returns such a failure on its next call. */
 skv_status skv_ledger_totals(const skv_cache* cache, uint64_t* device_bytes, uint64_t* host_bytes,
                              uint64_t* peak_device_bytes, uint64_t* capacity, void* stream);
+/* Cumulative rows the applied step_actions listed since creation, summed
+ * over layers and sequences: rows[0] offloaded, [1] deleted, [2] reloaded,
+ * [3] recomputed. Synchronises `stream`. */
+skv_status skv_ledger_counters(const skv_cache* cache, uint64_t* rows, void* stream);
+/* Calibration hook for CostParams::bandwidth (bench.hpp's fit is for
+ * mac_rate; the reference takes bandwidth as given): times the real duplex
+ * movement kernel moving `rows` token rows per sequence device->host and
+ * `rows` others host->device on `layer`, `reps` times; *ms per launch. Needs a
+ * non-paged cache with a host tier; overwrites that layer's rows and lists. */
+skv_status skv_profile_move(skv_cache* cache, int layer, int rows, int reps, double* ms, void* stream);
 /* Storage shape: token slots per (layer, sequence), bytes of the device K/V
  * pool, and bytes of the full [L][B][capacity] K/V it stands for. */
 skv_status skv_cache_storage(const skv_cache* cache, int32_t* slots_per_sequence, uint64_t* kv_pool_bytes,

@@ -71,6 +71,8 @@ def _declare(lib):
         "skv_cache_set_capacity": (I, [P, U64]),
         "skv_ledger_totals": (I, [P, P, P, P, P, P]),
         "skv_cache_storage": (I, [P, P, P, P]),
+        "skv_ledger_counters": (I, [P, P, P]),
+        "skv_profile_move": (I, [P, I, I, I, P, P]),
         "skv_cache_destroy": (I, [P]),
         "skv_cache_get_desc": (I, [P, P, P]),
         "skv_cache_write": (I, [P, I, I, I, I, I, P, P, P]),

@@ -267,6 +267,17 @@ class SwaCache:
         check(lib().skv_ledger_totals(self._h, *[C.byref(x) for x in v], _stream()))
         return dict(zip(("device_bytes", "host_bytes", "peak_device_bytes", "capacity"), (x.value for x in v)))
 
+    def ledger_counters(self) -> dict:
+        rows = (C.c_uint64 * 4)()
+        check(lib().skv_ledger_counters(self._h, rows, _stream()))
+        return dict(zip(("offloaded", "deleted", "reloaded", "recomputed"), (int(x) for x in rows)))
+
+    def profile_move(self, layer: int, rows: int, reps: int = 5) -> float:
+        """ms per duplex movement launch of `rows` rows each way per sequence."""
+        ms = C.c_double()
+        check(lib().skv_profile_move(self._h, layer, rows, reps, C.byref(ms), _stream()))
+        return ms.value
+
     def storage(self) -> dict:
         sl, pool, full = C.c_int32(), C.c_uint64(), C.c_uint64()
         check(lib().skv_cache_storage(self._h, C.byref(sl), C.byref(pool), C.byref(full)))

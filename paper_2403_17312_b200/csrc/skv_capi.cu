@@ -1652,6 +1652,63 @@ skv_status skv_ledger_totals(const skv_cache* c, uint64_t* device_bytes, uint64_
     return check_status(c);
 }
 
+skv_status skv_ledger_counters(const skv_cache* c, uint64_t* rows, void* stream) {
+    SKV_REQUIRE(c != nullptr && rows != nullptr, "null argument");
+    DeviceGuard guard(c->d.device);
+    skvd::LedgerTotals t{};
+    SKV_CUDA(cudaMemcpyAsync(&t, c->tot, sizeof t, cudaMemcpyDeviceToHost, as_stream(stream)));
+    SKV_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    for (int i = 0; i < 4; ++i) rows[i] = t.moved[i];
+    return SKV_OK;
+}
+
+// Calibration of CostParams::bandwidth on the real movement kernel: `rows`
+// token rows per sequence offloaded and `rows` others reloaded in one duplex
+// launch (as a Phase II step does), `reps` times, on layer `layer` of a
+// non-paged cache with a host tier. Overwrites that layer's action lists and
+// moves real rows: calibrate on a scratch cache.
+skv_status skv_profile_move(skv_cache* c, int layer, int rows, int reps, double* ms, void* stream) {
+    SKV_REQUIRE(c != nullptr && ms != nullptr, "null argument");
+    SKV_REQUIRE(layer >= 0 && layer < c->d.layers, "KvLedger: layer out of range");
+    SKV_REQUIRE(c->host_kv != nullptr && !c->paged, "profile_move: a non-paged cache with a host tier");
+    SKV_REQUIRE(rows >= 1 && 2 * rows <= c->d.capacity && reps >= 1, "profile_move: bad size");
+    DeviceGuard guard(c->d.device);
+    const cudaStream_t st = as_stream(stream);
+    const size_t lt = static_cast<size_t>(layer) * c->d.batch;
+    std::vector<int> lists(static_cast<size_t>(c->d.batch) * 4 * c->d.capacity, 0), counts(c->d.batch * 4, 0);
+    for (int b = 0; b < c->d.batch; ++b) {
+        for (int i = 0; i < rows; ++i) {
+            lists[(static_cast<size_t>(b) * 4 + 0) * c->d.capacity + i] = i;
+            lists[(static_cast<size_t>(b) * 4 + 2) * c->d.capacity + i] = rows + i;
+        }
+        counts[b * 4 + 0] = rows;
+        counts[b * 4 + 2] = rows;
+    }
+    SKV_CUDA(cudaMemcpyAsync(c->act_lists + lt * 4 * c->d.capacity, lists.data(), lists.size() * 4,
+                             cudaMemcpyHostToDevice, st));
+    SKV_CUDA(cudaMemcpyAsync(c->act_counts + lt * 4, counts.data(), counts.size() * 4, cudaMemcpyHostToDevice, st));
+    const bool poison = c->poison;
+    c->poison = false;
+    const uint8_t* rec = c->rec_x[layer];  // movement only: no recompute GEMM
+    c->rec_x[layer] = nullptr;
+    cudaEvent_t e0, e1;
+    SKV_CUDA(cudaEventCreate(&e0));
+    SKV_CUDA(cudaEventCreate(&e1));
+    skv_status out = launch_movement(c, layer, false, st);  // warm-up
+    SKV_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < reps && out == SKV_OK; ++i) out = launch_movement(c, layer, false, st);
+    SKV_CUDA(cudaEventRecord(e1, st));
+    SKV_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    SKV_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    c->poison = poison;
+    c->rec_x[layer] = rec;
+    *ms = t / reps;
+    return out;
+}
+
 skv_status skv_cache_storage(const skv_cache* c, int32_t* slots_per_sequence, uint64_t* kv_pool_bytes,
                              uint64_t* full_kv_bytes) {
     SKV_REQUIRE(c != nullptr, "null cache");

@@ -220,6 +220,12 @@ __global__ void __launch_bounds__(kLedgerThreads) ledger_step_kernel(const Ledge
         cnt[1] = static_cast<int>(n_del);
         cnt[2] = n_rl;
         cnt[3] = n_rc;
+        if (p.apply && p.tot) {
+            atomicAdd(&p.tot->moved[0], static_cast<unsigned long long>(n_off));
+            atomicAdd(&p.tot->moved[1], static_cast<unsigned long long>(n_del));
+            atomicAdd(&p.tot->moved[2], static_cast<unsigned long long>(n_rl));
+            atomicAdd(&p.tot->moved[3], static_cast<unsigned long long>(n_rc));
+        }
     }
     if (!p.apply) return;
     // a token offloaded and re-selected in the same step keeps its device row
