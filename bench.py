@@ -416,32 +416,36 @@ def run_schedule(api, torch, cfg, plan: dict, out_len: int, budget: int, shared:
                    recompute_enabled=plan.get("recompute_enabled", True))
     out = torch.empty((L, B, H, D), device="cuda", dtype=torch.float16)
     torch.cuda.synchronize()
+    # The device ledger runs one step ahead: call j attends step j and applies
+    # step j + 1's actions (its offload / reload / recompute traffic), so call j
+    # is booked to the phase of step j + 1 (the last call to the last step).
+    bucket = [phase_of_step(plan, min(j + 1, out_len - 1)) for j in range(out_len)]
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(out_len + 1)]
-    counters = {0: cache.ledger_counters()}
+    counters = {-1: cache.ledger_counters()}
     evs[0].record()
     for j in range(out_len):
         n = s + j + 1
         q, k, v = qin[j % len(qin)]
         cache.swa_decode_step(n, RATIO, q, k, v, out)
         evs[j + 1].record()
-        if j + 1 in (plan["p1"], plan["p2"]):  # phase boundary: the rows moved so far
-            counters[j + 1] = cache.ledger_counters()
+        if j + 1 < out_len and bucket[j + 1] != bucket[j]:  # phase boundary: the rows moved so far
+            counters[j] = cache.ledger_counters()
     torch.cuda.synchronize()
-    counters[out_len] = cache.ledger_counters()
+    counters[out_len - 1] = cache.ledger_counters()
     tot = cache.ledger_totals()
     stor = cache.storage()
     step_s = [evs[j].elapsed_time(evs[j + 1]) / 1000.0 for j in range(out_len)]
     phases = {}
     for j, t in enumerate(step_s):
-        ph = phases.setdefault(phase_of_step(plan, j), {"steps": 0, "measured_s": 0.0})
+        ph = phases.setdefault(bucket[j], {"steps": 0, "measured_s": 0.0, "kept_tokens": 0})
         ph["steps"] += 1
         ph["measured_s"] += t
+        ph["kept_tokens"] += api.swa_keep_count(s + j + 1, RATIO)
     marks = sorted(counters)
     for a, b in zip(marks, marks[1:]):
-        if b > a:
-            ph = phases[phase_of_step(plan, a)]
-            for key in ("offloaded", "deleted", "reloaded", "recomputed"):
-                ph[key + "_rows"] = ph.get(key + "_rows", 0) + counters[b][key] - counters[a][key]
+        ph = phases[bucket[b]]
+        for key in ("offloaded", "deleted", "reloaded", "recomputed"):
+            ph[key + "_rows"] = ph.get(key + "_rows", 0) + counters[b][key] - counters[a][key]
     cache.close()
     del cache
     torch.cuda.empty_cache()
@@ -494,16 +498,25 @@ def run_config5(args, cfg, rank: int, world: int):
         res = run_schedule(api, torch, cfg, pl, out_len, budget, shared, g)
         res["decode_s"] = max_over_ranks(res["decode_s"], device="cuda")
         table = {}
+        row_bytes = 2 * 2 * h  # one (layer, sequence) token entry: 2 e h (memsim.hpp:46-48 per sequence)
         for ph in (1, 2, 3):
             got = res["phases"].get(ph)
             if not got:
                 continue
             want = pr["phase_compute"][ph - 1] + pr["phase_transfer"][ph - 1] + pr["phase_recompute"][ph - 1]
+            # the same cost model (memsim.hpp:50-70) priced on the actions this run actually took
+            replay_c = 2.0 * B * L * h * got["kept_tokens"] / cost["mac_rate"]
+            replay_t = row_bytes * (got.get("offloaded_rows", 0) + got.get("reloaded_rows", 0)) / cost["bandwidth"]
+            replay_r = 2.0 * h * h * got.get("recomputed_rows", 0) / cost["mac_rate"]
+            replay = replay_c + replay_t + replay_r
             table[f"phase{ph}"] = dict(got, predicted_s=want, predicted_compute_s=pr["phase_compute"][ph - 1],
                                        predicted_transfer_s=pr["phase_transfer"][ph - 1],
                                        predicted_recompute_s=pr["phase_recompute"][ph - 1],
                                        predicted_steps=pr["phase_steps"][ph - 1],
                                        rel_error=(got["measured_s"] - want) / want if want else None,
+                                       replay_s=replay, replay_compute_s=replay_c, replay_transfer_s=replay_t,
+                                       replay_recompute_s=replay_r,
+                                       replay_rel_error=(got["measured_s"] - replay) / replay if replay else None,
                                        tokens_per_s=world * B * got["steps"] / got["measured_s"])
         results[name] = {"plan": pl, "predicted_total_decode_s": pr["total_seconds"] - pr["prefill_compute_seconds"],
                          "measured_decode_s": res["decode_s"],
@@ -528,7 +541,10 @@ def run_config5(args, cfg, rank: int, world: int):
                 "calibration": cal, "cost_params": cost, "solve_plan_s": solve_s, "schedules": results,
                 "cpu_baseline": cpu,
                 "note": "value = the solved schedule's decode tokens/s on a paged device KV bounded by the "
-                        "budget; schedules[*].phases set measured seconds beside PlanPrediction's"}
+                        "budget; schedules[*].phases set measured seconds beside PlanPrediction's (predicted_s: "
+                        "simulate_plan prices every global pick as a reload, scheduler.hpp:88-92) and beside the "
+                        "same cost model priced on the rows this run moved (replay_s); call j is booked to the "
+                        "phase of step j + 1, whose ledger actions and movement it runs"}
         print(json.dumps(line), flush=True)
 
 
