@@ -382,7 +382,7 @@ def calibrate_costs(api, torch, cfg, g) -> dict:
         points.append((macs, e0.elapsed_time(e1) / 1000.0))
         c.close()
     fit = fit_mac_rate(points)
-    rows, s_m = 256, 1024
+    rows, s_m = 512, 2048
     c = api.SwaCache(1, B, H, D, s_m, kv_dtype="f16")
     kp = torch.randn((B, s_m, H, D), generator=g, device="cuda", dtype=torch.float16)
     c.append_tokens(0, 0, 0, kp, torch.randn_like(kp))
@@ -444,7 +444,7 @@ def run_schedule(api, torch, cfg, plan: dict, out_len: int, budget: int, shared:
     marks = sorted(counters)
     for a, b in zip(marks, marks[1:]):
         ph = phases[bucket[b]]
-        for key in ("offloaded", "deleted", "reloaded", "recomputed"):
+        for key in ("offloaded", "deleted", "reloaded", "recomputed", "kept"):
             ph[key + "_rows"] = ph.get(key + "_rows", 0) + counters[b][key] - counters[a][key]
     cache.close()
     del cache
@@ -506,7 +506,8 @@ def run_config5(args, cfg, rank: int, world: int):
             want = pr["phase_compute"][ph - 1] + pr["phase_transfer"][ph - 1] + pr["phase_recompute"][ph - 1]
             # the same cost model (memsim.hpp:50-70) priced on the actions this run actually took
             replay_c = 2.0 * B * L * h * got["kept_tokens"] / cost["mac_rate"]
-            replay_t = row_bytes * (got.get("offloaded_rows", 0) + got.get("reloaded_rows", 0)) / cost["bandwidth"]
+            copies = got.get("offloaded_rows", 0) + got.get("reloaded_rows", 0) - got.get("kept_rows", 0)
+            replay_t = row_bytes * copies / cost["bandwidth"]
             replay_r = 2.0 * h * h * got.get("recomputed_rows", 0) / cost["mac_rate"]
             replay = replay_c + replay_t + replay_r
             table[f"phase{ph}"] = dict(got, predicted_s=want, predicted_compute_s=pr["phase_compute"][ph - 1],

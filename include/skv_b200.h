@@ -100,7 +100,9 @@ skv_status skv_ledger_totals(const skv_cache* cache, uint64_t* device_bytes, uin
                              uint64_t* peak_device_bytes, uint64_t* capacity, void* stream);
 /* Cumulative rows the applied step_actions listed since creation, summed
  * over layers and sequences: rows[0] offloaded, [1] deleted, [2] reloaded,
- * [3] recomputed. Synchronises `stream`. */
+ * [3] recomputed, [4] reloads of rows offloaded by the same step (they keep
+ * their device row: no host -> device copy). rows holds 5 values.
+ * Synchronises `stream`. */
 skv_status skv_ledger_counters(const skv_cache* cache, uint64_t* rows, void* stream);
 /* Calibration hook for CostParams::bandwidth (bench.hpp's fit is for
  * mac_rate; the reference takes bandwidth as given): times the real duplex

@@ -268,9 +268,9 @@ class SwaCache:
         return dict(zip(("device_bytes", "host_bytes", "peak_device_bytes", "capacity"), (x.value for x in v)))
 
     def ledger_counters(self) -> dict:
-        rows = (C.c_uint64 * 4)()
+        rows = (C.c_uint64 * 5)()
         check(lib().skv_ledger_counters(self._h, rows, _stream()))
-        return dict(zip(("offloaded", "deleted", "reloaded", "recomputed"), (int(x) for x in rows)))
+        return dict(zip(("offloaded", "deleted", "reloaded", "recomputed", "kept"), (int(x) for x in rows)))
 
     def profile_move(self, layer: int, rows: int, reps: int = 5) -> float:
         """ms per duplex movement launch of `rows` rows each way per sequence."""

@@ -265,8 +265,9 @@ static skv_status cache_create_impl(const skv_cache_desc* desc, uint64_t paged_c
     if (!ok_pair || dtype_size(d.kv_dtype) == 0)
         return fail(SKV_ERR_UNSUPPORTED, "skv_cache_create: kv_dtype %d with q_dtype %d", d.kv_dtype,
                     d.q_dtype);
-    if (d.kv_dtype == SKV_U8 && d.heads % 2 != 0)
-        return fail(SKV_ERR_UNSUPPORTED, "skv_cache_create: INT8 rows need an even head count (%d)", d.heads);
+    if (d.kv_dtype == SKV_U8 && d.heads % skvd::kU8Group != 0)
+        return fail(SKV_ERR_UNSUPPORTED, "skv_cache_create: INT8 storage groups heads by %d (heads %d)",
+                    skvd::kU8Group, d.heads);
     DeviceGuard guard(d.device);
     skv_cache* c = new skv_cache();
     c->d = d;
@@ -955,7 +956,9 @@ skv_status launch_ledger_c(skv_cache* c, int layer, long long j, const int* sel,
 
 // apply_actions data movement for one layer (engine.hpp:686-716): offload
 // then reload over the host tier, after the ledger kernel made the lists.
-skv_status launch_movement(skv_cache* c, int layer, bool pdl, cudaStream_t st) {
+// m_sel: the step's selection size, which bounds every list's length per
+// sequence (the recompute GEMM's row count is at most B * m_sel).
+skv_status launch_movement(skv_cache* c, int layer, bool pdl, cudaStream_t st, int m_sel = 0) {
     if (!c->host_kv) return SKV_OK;
     skvd::MoveParams mp{};
     const size_t lt = static_cast<size_t>(layer) * c->d.batch;
@@ -988,7 +991,8 @@ skv_status launch_movement(skv_cache* c, int layer, bool pdl, cudaStream_t st) {
         SKV_CUDA(launch_recompute_gather(c->rec_x[layer], xrow * c->d.capacity, xrow, mp.lists, mp.counts,
                                          c->d.capacity, c->rec_a, c->rec_map, c->rec_m, c->d.batch, st,
                                          c->paged ? mp.act_slots : nullptr));
-        const int m_cap = static_cast<int>((static_cast<long long>(c->d.batch) * c->d.capacity + 127) / 128 * 128);
+        const long long per = m_sel > 0 ? std::min(m_sel, c->d.capacity) : c->d.capacity;
+        const int m_cap = static_cast<int>((static_cast<long long>(c->d.batch) * per + 127) / 128 * 128);
         if (c->d.kv_dtype == SKV_U8) {
             SKV_CUDA(launch_gemm_tn(c->rec_a, c->rec_wt[layer], c->rec_c, c->rec_m, m_cap, static_cast<int>(2 * h),
                                     static_cast<int>(h), c->d.q_dtype == SKV_BF16, st, nullptr));
@@ -1030,7 +1034,8 @@ skv_status decode_layer_impl(skv_cache* c, int layer, int n, double r, const voi
                 if (skv_status e = launch_ledger_c(c, layer, j, layer_idx(c, layer), c->d.capacity, s.m, s.k, true,
                                                    true, false, st))
                     return e;
-                if (skv_status e = launch_movement(c, layer, true, st)) return e;
+                if (phase_of(c->plan, j) > 1)  // Phase I lists are empty: nothing to move
+                    if (skv_status e = launch_movement(c, layer, true, st, s.m)) return e;
             }
         }
     }
@@ -1054,7 +1059,8 @@ skv_status decode_layer_impl(skv_cache* c, int layer, int n, double r, const voi
             if (skv_status e = launch_ledger_c(c, layer, j_next, layer_idx(c, layer), c->d.capacity, sn.m, sn.k,
                                                true, true, !c->prof, st))
                 return e;
-            return launch_movement(c, layer, !c->prof, st);
+            if (phase_of(c->plan, j_next) == 1) return SKV_OK;  // Phase I lists are empty: nothing to move
+            return launch_movement(c, layer, !c->prof, st, sn.m);
         }
     }
     return SKV_OK;
@@ -1659,6 +1665,7 @@ skv_status skv_ledger_counters(const skv_cache* c, uint64_t* rows, void* stream)
     SKV_CUDA(cudaMemcpyAsync(&t, c->tot, sizeof t, cudaMemcpyDeviceToHost, as_stream(stream)));
     SKV_CUDA(cudaStreamSynchronize(as_stream(stream)));
     for (int i = 0; i < 4; ++i) rows[i] = t.moved[i];
+    rows[4] = t.kept;
     return SKV_OK;
 }
 

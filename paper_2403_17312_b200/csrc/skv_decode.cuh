@@ -112,7 +112,8 @@ struct DecodeCfg {
     static_assert(SLOTS % HG == 0, "head group must tile the consumer slots");
     static_assert(T * HG % SLOTS == 0 && RS >= 1 && RS <= LR, "stage rows must tile the slots");
     static_assert(T <= 32, "one producer lane per token row");
-    static_assert(!QUANT || HG % 2 == 0, "136-byte INT8 rows: an even head group keeps copies 16-byte sized");
+    static_assert(!QUANT || (HG % 2 == 0 && kU8Group % HG == 0),
+                  "INT8 head groups split the 8-head storage blocks into 16-byte sized copies");
     static_assert(SLOTS * D * 4 <= S * STAGEB, "reduction scratch aliases the ring");
 };
 
@@ -178,10 +179,11 @@ __device__ __forceinline__ float reduce_rows(float (&v)[RS], int c, int& row) {
 }
 
 // CTAs per SM the register budget must allow (ptxas otherwise picked
-// budgets that spilled): 3 for 16/32-bit rows, 2 for INT8 (wider stages).
+// budgets that spilled): 3 for 16-bit rows, 2 for fp32 and INT8 rows.
 template <class KV>
 constexpr int attend_min_blocks() {
-    return KV::QUANT ? 2 : 3;
+    // fp32 rows (config 1, the latency-bound parity case) need no third CTA per SM
+    return (KV::QUANT || KV::E == 4) ? 2 : 3;
 }
 
 template <class KV, class QT, int HG>
@@ -214,7 +216,9 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
     pdl_launch_dependents();
 
     const size_t TOKB = static_cast<size_t>(2) * H * ROWE;  // bytes per token (K and V planes)
-    const uint8_t* kvb = p.kv + static_cast<size_t>(b) * p.kv_ncap * TOKB + static_cast<size_t>(g) * ROWB;
+    // this sequence's token rows; a token holds K then V, H heads each
+    // (INT8: blocks of 8 heads, codes then (scale, bias), see u8_code_off)
+    const uint8_t* kvb = p.kv + static_cast<size_t>(b) * p.kv_ncap * TOKB;
     const int* slot_row = paged ? p.slots + static_cast<size_t>(b) * p.Ncap : nullptr;
     // smem slot list (paged, shared-memory token list); long selections look slots up in the producer
     int* tslot = (paged && !gmem) ? reinterpret_cast<int*>(smem + L.slot) : nullptr;
@@ -262,6 +266,13 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
                               (static_cast<size_t>(b) * H + g * HG) * ROWE;
         const uint8_t* vnew = static_cast<const uint8_t*>(p.v_new) +
                               (static_cast<size_t>(b) * H + g * HG) * ROWE;
+        // per-token offsets of this head group's K and V rows (INT8: codes, then (scale, bias))
+        const uint32_t off_k = QUANT ? static_cast<uint32_t>(u8_code_off(0, g * HG, H))
+                                     : static_cast<uint32_t>(g * HG * ROWE);
+        const uint32_t off_v = QUANT ? static_cast<uint32_t>(u8_code_off(1, g * HG, H))
+                                     : static_cast<uint32_t>((H + g * HG) * ROWE);
+        const uint32_t moff_k = QUANT ? static_cast<uint32_t>(u8_meta_off(0, g * HG, H)) : 0u;
+        const uint32_t moff_v = QUANT ? static_cast<uint32_t>(u8_meta_off(1, g * HG, H)) : 0u;
         bool synced = !p.append;
         for (int u = 0; u < 2 * nchunks; ++u) {
             const int vsel = u >= nchunks;
@@ -282,9 +293,20 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
                 const int i = pw + lane * kProducerWarps;
                 int t = tslot ? tslot[base + i] : tok[base + i];
                 if (paged && !tslot) t = max(slot_row[t], 0);
-                const uint8_t* src = kvb + static_cast<size_t>(t) * TOKB + vsel * H * ROWE;
-                if (!QUANT && has_cur && i == cnt - 1) src = vsel ? vnew : knew;
-                bulk_g2s(ring + stage * STAGEB + i * ROWB, src, ROWB, &full[stage], pol);
+                const uint8_t* tb = kvb + static_cast<size_t>(t) * TOKB;
+                uint8_t* dst = ring + stage * STAGEB + i * ROWB;
+                const uint8_t* src = tb + (vsel ? off_v : off_k);
+                if constexpr (QUANT) {
+                    if constexpr (HG == kU8Group) {  // codes + (scale, bias) of the block: one copy
+                        bulk_g2s(dst, src, ROWB, &full[stage], pol);
+                    } else {  // part of a block: codes, then their (scale, bias) pairs
+                        bulk_g2s(dst, src, HG * D, &full[stage], pol);
+                        bulk_g2s(dst + HG * D, tb + (vsel ? moff_v : moff_k), HG * 8, &full[stage], pol);
+                    }
+                } else {
+                    if (has_cur && i == cnt - 1) src = vsel ? vnew : knew;
+                    bulk_g2s(dst, src, ROWB, &full[stage], pol);
+                }
             }
         }
         return;
@@ -297,8 +319,8 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
     // ---- append the step's new K/V rows for this head group (token n-1)
     if (p.append) {
         const int cur_slot = paged ? max(slot_row[n - 1], 0) : n - 1;
-        const size_t tok_off = (static_cast<size_t>(b) * p.kv_ncap + cur_slot) * TOKB +
-                               static_cast<size_t>(g) * ROWB;
+        const size_t tok_base = (static_cast<size_t>(b) * p.kv_ncap + cur_slot) * TOKB;
+        const size_t tok_off = tok_base + static_cast<size_t>(g) * ROWB;  // non-quantized rows of the group
         if constexpr (!QUANT) {
             constexpr int VPR = ROWB / 16;  // compute dtype == storage dtype
             for (int i = ctid; i < 2 * VPR; i += kConsumerThreads) {
@@ -346,10 +368,10 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
                     c = c < 0 ? 0 : (c > 255 ? 255 : c);
                     packed |= static_cast<uint32_t>(c) << (8 * i);
                 }
-                uint8_t* row = p.kv_w + tok_off + kv * H * ROWE + h * ROWE;
+                uint8_t* row = p.kv_w + tok_base + u8_code_off(kv, g * HG + h, H);
                 reinterpret_cast<uint32_t*>(row)[lane] = packed;
                 if (lane == 0)
-                    *reinterpret_cast<float2*>(row + D) =
+                    *reinterpret_cast<float2*>(p.kv_w + tok_base + u8_meta_off(kv, g * HG + h, H)) =
                         make_float2(static_cast<float>(scale), static_cast<float>(-scale * static_cast<double>(zp)));
             }
             fence_global_to_async();
@@ -383,18 +405,16 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
 #pragma unroll
         for (int off = LR / 2; off > 0; off >>= 1) qsum += __shfl_xor_sync(0xffffffffu, qsum, off);
     }
-    const uint32_t lane_off = static_cast<uint32_t>(slot * ROWE + c * 16);
-    const float scale = p.scale;
-    // 16-byte vector at p; INT8 rows are 136 bytes, so only 8-byte aligned
-    auto ld16 = [](const uint8_t* q) -> uint4 {
-        if constexpr (QUANT) {
-            const uint2 a = *reinterpret_cast<const uint2*>(q);
-            const uint2 bb = *reinterpret_cast<const uint2*>(q + 8);
-            return make_uint4(a.x, a.y, bb.x, bb.y);
-        } else {
-            return *reinterpret_cast<const uint4*>(q);
-        }
+    // row r of a stage = (token r / HG, head r % HG); INT8 rows sit at 128-byte
+    // strides inside their token's block, the (scale, bias) pairs after them
+    const uint32_t lane_off = QUANT ? static_cast<uint32_t>((slot / HG) * ROWB + (slot % HG) * D + c * 16)
+                                    : static_cast<uint32_t>(slot * ROWE + c * 16);
+    auto meta_at = [&](const uint8_t* stage_base, int r) {
+        return *reinterpret_cast<const float2*>(stage_base + (r / HG) * ROWB + HG * D + (r % HG) * 8);
     };
+    const float scale = p.scale;
+    // 16-byte vector at q (16-byte aligned for every storage type)
+    auto ld16 = [](const uint8_t* q) -> uint4 { return *reinterpret_cast<const uint4*>(q); };
 
     // ---- pass 1: logits = (q . k) * scale  (attention.hpp:204-212)
     for (int u = 0; u < nchunks; ++u) {
@@ -433,7 +453,7 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
             const int t = r / HG;
             float logit;
             if constexpr (QUANT) {
-                const float2 ms = *reinterpret_cast<const float2*>(ring + stage * STAGEB + r * ROWE + D);
+                const float2 ms = meta_at(ring + stage * STAGEB, r);
                 // codes arrive as 1024 + c (cvt16x2, KvU8): dot = q.c + 1024 * sum(q)
                 logit = fmaf(ms.x, dot, fmaf(-kBiasU8, ms.x, ms.y) * qsum) * scale;
             } else {
@@ -505,7 +525,7 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
                 float2 vf[V2];
                 cvt16x2(raw[i], vf, KV{});
                 if constexpr (QUANT) {
-                    const float2 ms = *reinterpret_cast<const float2*>(ring + stage * STAGEB + r * ROWE + D);
+                    const float2 ms = meta_at(ring + stage * STAGEB, r);
                     const float a = w * ms.x;
                     const float2 a2 = make_float2(a, a);
 #pragma unroll
@@ -526,7 +546,7 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
                     float2 vf[V2];
                     cvt16x2(ld16(st + i * SLOTS * ROWE), vf, KV{});
                     if constexpr (QUANT) {
-                        const float2 ms = *reinterpret_cast<const float2*>(ring + stage * STAGEB + r * ROWE + D);
+                        const float2 ms = meta_at(ring + stage * STAGEB, r);
                         const float a = w * ms.x;
                         const float2 a2 = make_float2(a, a);
 #pragma unroll

@@ -122,6 +122,21 @@ struct KvU8 {  // affine 8-bit codes + per (token, head) fp32 (scale, bias)
     static constexpr bool QUANT = true;
 };
 
+// INT8 storage of one token: for K then V, the heads in blocks of 8, each
+// block [8 x 128 codes][8 x (scale, bias) fp32] = 1088 bytes, so every code
+// row is 16-byte aligned (one 128-bit shared-memory load per vector, no bank
+// conflicts) and a head group of 8 is still one contiguous bulk copy.
+constexpr int kU8Group = 8;
+constexpr int kU8Block = kU8Group * (128 + 8);
+__host__ __device__ inline size_t u8_code_off(int which, int h, int H) {
+    return static_cast<size_t>(which * (H / kU8Group) + h / kU8Group) * kU8Block +
+           static_cast<size_t>(h % kU8Group) * 128;
+}
+__host__ __device__ inline size_t u8_meta_off(int which, int h, int H) {
+    return static_cast<size_t>(which * (H / kU8Group) + h / kU8Group) * kU8Block + kU8Group * 128 +
+           static_cast<size_t>(h % kU8Group) * 8;
+}
+
 // 16 bytes -> 16/E floats.
 __device__ __forceinline__ void cvt16(const uint4& r, float (&f)[4], KvF32) {
     f[0] = __uint_as_float(r.x);

@@ -307,6 +307,12 @@ __global__ void __launch_bounds__(kLedgerThreads) ledger_step_kernel(const Ledge
         post_dev += t == kTierDevice;
         post_host += t == kTierHost;
     }
+    if (p.tot) {  // reloads that keep their device row: listed, but no host -> device copy
+        long long nk = 0;
+        for (int i = tid; i < n_rl; i += NT) nk += kept(lists[2 * p.list_ld + i]);
+        nk = block_sum<NT>(nk, red, tid);
+        if (tid == 0) atomicAdd(&p.tot->kept, static_cast<unsigned long long>(nk));
+    }
     post_dev = block_sum<NT>(post_dev, red, tid);
     post_host = block_sum<NT>(post_host, red, tid);
     allocs = block_sum<NT>(allocs, red, tid);
@@ -543,7 +549,7 @@ __global__ void dequantize_kernel(const uint16_t* __restrict__ codes, long long 
 // One (token, K|V, head) row of D values from the compute dtype into the
 // storage dtype, one warp; INT8 rows are engine.hpp:469-483's fake-quant
 // (quant.hpp:43-81 per head_dim group, in fp64: bit-exact codes).
-__device__ __forceinline__ void quant_row_u8(uint8_t* dst, const double (&x)[kHeadDim / 32], int lane) {
+__device__ __forceinline__ void quant_row_u8(uint8_t* dst, float2* meta, const double (&x)[kHeadDim / 32], int lane) {
     constexpr int D = kHeadDim;
     double lo = x[0], hi = x[0];
 #pragma unroll
@@ -575,26 +581,26 @@ __device__ __forceinline__ void quant_row_u8(uint8_t* dst, const double (&x)[kHe
         packed |= static_cast<uint32_t>(c) << (8 * i);
     }
     reinterpret_cast<uint32_t*>(dst)[lane] = packed;
-    if (lane == 0)
-        *reinterpret_cast<float2*>(dst + D) =
-            make_float2(static_cast<float>(scale), static_cast<float>(-scale * static_cast<double>(zp)));
+    if (lane == 0) *meta = make_float2(static_cast<float>(scale), static_cast<float>(-scale * static_cast<double>(zp)));
 }
 
 // One (token, K|V, head) row of D values from the compute dtype into the
 // storage dtype, one warp; INT8 rows are engine.hpp:469-483's fake-quant
 // (quant.hpp:43-81 per head_dim group, in fp64: bit-exact codes).
+// tok: the token's storage; row (which, h) of H heads.
 template <class QT, class KV>
-__device__ __forceinline__ void store_row(uint8_t* dst, const QT* src, int lane) {
+__device__ __forceinline__ void store_row(uint8_t* tok, int which, int h, int H, const QT* src, int lane) {
     constexpr int D = kHeadDim;
     if constexpr (!KV::QUANT) {
         using T = typename KV::T;
-        T* d = reinterpret_cast<T*>(dst);
+        T* d = reinterpret_cast<T*>(tok + static_cast<size_t>(which * H + h) * kv_row_bytes<KV>());
         for (int i = lane; i < D; i += 32) d[i] = from_f<T>(to_f(src[i]));
     } else {
         double x[D / 32];
 #pragma unroll
         for (int i = 0; i < D / 32; ++i) x[i] = static_cast<double>(to_f(src[lane * (D / 32) + i]));
-        quant_row_u8(dst, x, lane);
+        quant_row_u8(tok + u8_code_off(which, h, H), reinterpret_cast<float2*>(tok + u8_meta_off(which, h, H)), x,
+                     lane);
     }
 }
 
@@ -617,8 +623,8 @@ __global__ void cache_write_kernel(const CacheView cv, double* __restrict__ imp,
     const QT* src = (which ? v : k) + ((static_cast<size_t>(bb) * nt + t) * H + h) * kHeadDim;
     const size_t tok = static_cast<size_t>(b0 + bb) * cv.Ncap + (t0 + t);
     const size_t srow = static_cast<size_t>(b0 + bb) * cv.kv_ncap + (t0 + t);  // slot t when paged
-    uint8_t* dst = cv.kv + ((srow * 2 + which) * H + h) * static_cast<size_t>(kv_row_bytes<KV>());
-    store_row<QT, KV>(dst, src, lane);
+    uint8_t* tokp = cv.kv + srow * 2 * H * static_cast<size_t>(kv_row_bytes<KV>());
+    store_row<QT, KV>(tokp, which, h, H, src, lane);
     if (lane == 0 && h == 0 && which == 0) {
         imp[tok] = 0.0;
         if (tiers) {
@@ -658,9 +664,8 @@ __global__ void quant_scatter_kernel(const float* __restrict__ C, const int* __r
     double x[kHeadDim / 32];
 #pragma unroll
     for (int i = 0; i < kHeadDim / 32; ++i) x[i] = static_cast<double>(to_f(from_f<QT>(src[lane * (kHeadDim / 32) + i])));
-    uint8_t* dst = kv + ((static_cast<size_t>(bt.x) * kv_ncap + bt.y) * 2 + which) * static_cast<size_t>(H) *
-                            kv_row_bytes<KvU8>() + static_cast<size_t>(h) * kv_row_bytes<KvU8>();
-    quant_row_u8(dst, x, lane);
+    uint8_t* tokp = kv + (static_cast<size_t>(bt.x) * kv_ncap + bt.y) * 2 * H * kv_row_bytes<KvU8>();
+    quant_row_u8(tokp + u8_code_off(which, h, H), reinterpret_cast<float2*>(tokp + u8_meta_off(which, h, H)), x, lane);
 }
 
 // Cache read-back to fp32 [nb][nt][2][H][D]; rows not on device (paged,
@@ -687,11 +692,12 @@ __global__ void cache_read_kernel(const CacheView cv, float* __restrict__ out, i
         }
     }
     const size_t tok = static_cast<size_t>(b0 + bb) * cv.kv_ncap + st;
-    const uint8_t* row = cv.kv + ((tok * 2 + which) * H + h) * static_cast<size_t>(kv_row_bytes<KV>());
     if constexpr (KV::QUANT) {
-        const float2 ms = *reinterpret_cast<const float2*>(row + D);
-        out[i] = fmaf(ms.x, static_cast<float>(row[d]), ms.y);
+        const uint8_t* tokp = cv.kv + tok * 2 * H * kv_row_bytes<KV>();
+        const float2 ms = *reinterpret_cast<const float2*>(tokp + u8_meta_off(which, h, H));
+        out[i] = fmaf(ms.x, static_cast<float>(tokp[u8_code_off(which, h, H) + d]), ms.y);
     } else {
+        const uint8_t* row = cv.kv + ((tok * 2 + which) * H + h) * static_cast<size_t>(kv_row_bytes<KV>());
         using T = typename KV::T;
         out[i] = to_f(reinterpret_cast<const T*>(row)[d]);
     }
@@ -711,9 +717,9 @@ __global__ void dequant_layer_f16_kernel(const uint8_t* __restrict__ kv, __half*
     const int t = static_cast<int>((r / (2 * H)) % s);
     const int b = static_cast<int>(r / (2LL * H * s));
     const size_t tok = static_cast<size_t>(b) * Ncap + t;
-    const uint8_t* row = kv + ((tok * 2 + which) * H + h) * static_cast<size_t>(kv_row_bytes<KvU8>());
-    const float2 ms = *reinterpret_cast<const float2*>(row + D);
-    const uint2 codes = *reinterpret_cast<const uint2*>(row + c);  // rows are 8-byte aligned (136 B)
+    const uint8_t* tokp = kv + tok * 2 * H * static_cast<size_t>(kv_row_bytes<KvU8>());
+    const float2 ms = *reinterpret_cast<const float2*>(tokp + u8_meta_off(which, h, H));
+    const uint2 codes = *reinterpret_cast<const uint2*>(tokp + u8_code_off(which, h, H) + c);
     const uint8_t* cb = reinterpret_cast<const uint8_t*>(&codes);
     __half2 o[4];
 #pragma unroll

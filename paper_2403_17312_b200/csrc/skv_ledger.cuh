@@ -41,6 +41,7 @@ struct LedgerTotals {
     unsigned long long dev_tokens, host_tokens, peak_dev_tokens;
     unsigned long long exhausted;  // failed slot allocations of the running layer-step (paged)
     unsigned long long moved[4];   // cumulative rows offloaded, deleted, reloaded, recomputed
+    unsigned long long kept;       // cumulative reloads of rows offloaded in the same step (no copy in)
 };
 
 static __device__ __noinline__ void report_status(DevStatus* st, int code, int layer, int seq, int token, long long step,

@@ -118,9 +118,11 @@ def test_prefill_then_decode(api, port):
 
 
 def test_prefill_rejects_unsupported_and_bad_shapes(api):
-    c = api.SwaCache(1, 1, 2, 128, 64, kv_dtype="u8", q_dtype="f32")  # INT8 needs fp16 queries
+    with pytest.raises(api.Unsupported):  # INT8 storage groups heads by 8
+        api.SwaCache(1, 1, 2, 128, 64, kv_dtype="u8", q_dtype="f16")
+    c = api.SwaCache(1, 1, 8, 128, 64, kv_dtype="u8", q_dtype="f32")  # INT8 needs fp16 queries
     with pytest.raises(api.Unsupported):
-        c.prefill_layer(0, torch.zeros((1, 8, 2, 128), dtype=torch.float32, device="cuda"))
+        c.prefill_layer(0, torch.zeros((1, 8, 8, 128), dtype=torch.float32, device="cuda"))
     c = api.SwaCache(1, 1, 2, 128, 64, kv_dtype="f16")
     with pytest.raises(api.ContractViolation):
         c.prefill_layer(0, torch.zeros((1, 65, 2, 128), dtype=torch.float16, device="cuda"))
@@ -133,7 +135,7 @@ def test_prefill_int8(api, port):
     cores; the seed row and the last query's output are redone on the exact
     dequantisation. Reference: dense_attention on the fake-quantised K/V
     (engine.hpp:469-483 groups of D per (token, head))."""
-    B, H, s, D = 2, 4, 300, 128
+    B, H, s, D = 2, 8, 300, 128
     rng = np.random.default_rng(88)
     k = round_to(rng.standard_normal((B, s, H, D)), "f16")
     v = round_to(rng.standard_normal((B, s, H, D)), "f16")
