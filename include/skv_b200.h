@@ -162,6 +162,13 @@ skv_status skv_prefill_sparsity_get(const skv_cache* cache, int layer, double* d
 skv_status skv_swa_decode_layer(skv_cache* cache, int layer, int n, double r, const void* q,
                                 const void* k_new, const void* v_new, void* out,
                                 int32_t* idx_out, float* w_out, void* stream);
+/* The part of a decode step of `layer` at length n before its attend
+ * (engine.hpp:601-606): variant_selection for (n, r) when none is pending
+ * (the previous step normally made it) and, with a plan attached, that
+ * step's step_actions + apply_actions on the device ledger. A following
+ * skv_swa_decode_layer at (n, r) then only attends. Lets a host read the
+ * step's actions (skv_ledger_counters) before the attend runs. */
+skv_status skv_decode_prepare(skv_cache* cache, int layer, int n, double r, void* stream);
 /* All L layers of one decode step (q/k/v/out device [L][B][H][D]); L launches. */
 skv_status skv_swa_decode_step(skv_cache* cache, int n, double r, const void* q,
                                const void* k_new, const void* v_new, void* out, void* stream);
@@ -314,6 +321,31 @@ skv_status skv_last_actions(const skv_cache* cache, int layer, int32_t* lists_ou
  * row-major fp16 (bf16 != 0: bf16), C [M x N] fp32; M % 128, N % 256,
  * K % 64 == 0). Exposed for tests. */
 skv_status skv_gemm_tn(const void* A, const void* Bt, float* C, int M, int N, int K, int bf16, void* stream);
+
+/* ---- the reference toy transformer's dense operators on the GPU (fp64) ---
+ * For an engine step around the SWA attention (engine.hpp:571-684, the
+ * include/skv/b200_engine.hpp mirror of skv::Engine). All buffers device
+ * fp64 row-major, enqueued on `stream`.
+ * embed: out[t] = emb[ids[t]] + positional_term(pos0 + t) (engine.hpp:131-144,
+ *   360-381); ids device int64 [n].
+ * layernorm: layer_norm per row (engine.hpp:111-125), eps 1e-5.
+ * gemm: C (+)= A[M x K] . B[K x N] (matmul, matrix.hpp).
+ * gelu: tanh GELU in place (engine.hpp:127-129).
+ * convert / widen: fp64 -> fp32 and back (the attention cache dtype).
+ * causal_attention: dense_attention(q_h, k_h, v_h, true) for every head of
+ *   [s][heads*head_dim] q/k/v (attention.hpp:91-117, bottom-right aligned):
+ *   out [sq][heads*head_dim], aw [heads][sq][sk]. */
+skv_status skv_engine_embed(const double* emb, int h, const int64_t* ids, int n, int pos0, double* out,
+                            void* stream);
+skv_status skv_engine_layernorm(const double* x, int rows, int h, const double* gain, const double* bias,
+                                double* out, void* stream);
+skv_status skv_engine_gemm(const double* A, const double* B, double* C, int M, int N, int K, int accumulate,
+                           void* stream);
+skv_status skv_engine_gelu(double* x, size_t n, void* stream);
+skv_status skv_engine_convert(const double* in, float* out, size_t n, void* stream);
+skv_status skv_engine_widen(const float* in, double* out, size_t n, void* stream);
+skv_status skv_engine_causal_attention(const double* q, const double* k, const double* v, int sq, int sk, int heads,
+                                       int head_dim, double* out, double* aw, void* stream);
 
 /* ---- device memory helpers for hosts without the CUDA headers (the C++
  * mirror include/skv/b200.hpp uses these). skv_copy is cudaMemcpyDefault

@@ -141,6 +141,10 @@ struct skv_cache {
     uint8_t* stage = nullptr;
     size_t stage_bytes = 0;
     cudaStream_t h2d = nullptr, d2h = nullptr;
+    // whole-step decode: the batched select of the first layers runs on this
+    // side stream while the remaining layers' attends stream on the caller's
+    cudaStream_t sel_st = nullptr;
+    cudaEvent_t ev_sel_in = nullptr, ev_sel_out = nullptr;
     std::vector<cudaEvent_t> ev_in, ev_comp, ev_out;  // per chunk
     // head sharding: this cache holds heads [head_offset, head_offset + H) of
     // total_heads; the head-summed rows are summed across shards by `reduce`
@@ -428,6 +432,9 @@ skv_status skv_cache_destroy(skv_cache* c) {
     for (auto* v : {&c->ev_in, &c->ev_comp, &c->ev_out})
         for (cudaEvent_t e : *v) cudaEventDestroy(e);
     if (c->h2d) cudaStreamDestroy(c->h2d);
+    if (c->sel_st) cudaStreamDestroy(c->sel_st);
+    if (c->ev_sel_in) cudaEventDestroy(c->ev_sel_in);
+    if (c->ev_sel_out) cudaEventDestroy(c->ev_sel_out);
     if (c->d2h) cudaStreamDestroy(c->d2h);
     cudaFree(c->pf_scratch);
     cudaFree(c->pf_sparsity);
@@ -1013,6 +1020,28 @@ skv_status launch_movement(skv_cache* c, int layer, bool pdl, cudaStream_t st, i
     return SKV_OK;
 }
 
+// The part of a decode step before its attend (engine.hpp:601-606):
+// variant_selection when no selection for (n, r) is pending, and with a plan
+// that step's step_actions + apply_actions (normally done right after the
+// previous step). *fresh: a selection was made here.
+skv_status prepare_step(skv_cache* c, int layer, int n, double r, const StepShape& s, cudaStream_t st, bool* fresh) {
+    *fresh = false;
+    if (c->pend_n[layer] == n && c->pend_r[layer] == r) return SKV_OK;
+    if (skv_status e = launch_select_c(c, layer, 0, nullptr, 0, 0, 0, -1, n, r, false, st)) return e;
+    *fresh = true;
+    if (c->has_plan) {
+        const long long j = static_cast<long long>(n) - 1 - c->plan.input_len;
+        if (j >= 0 && j < c->plan.output_len && c->ledger_j[layer] != j) {
+            if (skv_status e = launch_ledger_c(c, layer, j, layer_idx(c, layer), c->d.capacity, s.m, s.k, true, true,
+                                               false, st))
+                return e;
+            if (phase_of(c->plan, j) > 1)  // Phase I lists are empty: nothing to move
+                if (skv_status e = launch_movement(c, layer, true, st, s.m)) return e;
+        }
+    }
+    return SKV_OK;
+}
+
 // One layer of one decode step: [select if no matching pending selection] ->
 // attend (append + gather + softmax + PV) -> select kernel (fold weights into
 // the importance, select for n+1 with the same ratio).
@@ -1025,20 +1054,7 @@ skv_status decode_layer_impl(skv_cache* c, int layer, int n, double r, const voi
         return fail(SKV_ERR_CONTRACT, "paged cache: attach a plan (skv_cache_set_plan) before decoding");
     c->decoded[layer] = 1;
     bool fresh = false;
-    if (!(c->pend_n[layer] == n && c->pend_r[layer] == r)) {
-        if (skv_status e = launch_select_c(c, layer, 0, nullptr, 0, 0, 0, -1, n, r, false, st)) return e;
-        fresh = true;
-        if (c->has_plan) {  // this step's bookkeeping (normally done right after the previous step)
-            const long long j = static_cast<long long>(n) - 1 - c->plan.input_len;
-            if (j >= 0 && j < c->plan.output_len && c->ledger_j[layer] != j) {
-                if (skv_status e = launch_ledger_c(c, layer, j, layer_idx(c, layer), c->d.capacity, s.m, s.k, true,
-                                                   true, false, st))
-                    return e;
-                if (phase_of(c->plan, j) > 1)  // Phase I lists are empty: nothing to move
-                    if (skv_status e = launch_movement(c, layer, true, st, s.m)) return e;
-            }
-        }
-    }
+    if (skv_status e = prepare_step(c, layer, n, r, s, st, &fresh)) return e;
     int G = 0;
     FoldSpec fold;
     fold.apply = 1;
@@ -1188,6 +1204,17 @@ skv_status skv_prefill_sparsity_get(const skv_cache* c, int layer, double* dst, 
     return SKV_OK;
 }
 
+skv_status skv_decode_prepare(skv_cache* c, int layer, int n, double r, void* stream) {
+    SKV_REQUIRE(c != nullptr, "null cache");
+    SKV_REQUIRE(layer >= 0 && layer < c->d.layers, "KvLedger: layer out of range");
+    if (skv_status e = check_status(c)) return e;
+    StepShape s;
+    if (skv_status e = step_shape(c, n, r, &s)) return e;
+    DeviceGuard guard(c->d.device);
+    bool fresh = false;
+    return prepare_step(c, layer, n, r, s, as_stream(stream), &fresh);
+}
+
 skv_status skv_swa_decode_layer(skv_cache* c, int layer, int n, double r, const void* q, const void* k_new,
                                 const void* v_new, void* out, int32_t* idx_out, float* w_out, void* stream) {
     SKV_REQUIRE(c != nullptr, "null cache");
@@ -1201,33 +1228,10 @@ skv_status skv_swa_decode_layer(skv_cache* c, int layer, int n, double r, const 
 // Layers [l0, l1) of one decode step; layer l > l0 launches with programmatic
 // dependent launch: its inputs were complete before the range's first launch,
 // so it can stream while the previous layer's kernels drain.
-static skv_status decode_layers(skv_cache* c, int l0, int l1, int n, double r, const void* q, const void* k_new,
-                                const void* v_new, void* out, cudaStream_t st) {
-    const size_t per_layer = static_cast<size_t>(c->d.batch) * c->d.heads * c->d.head_dim * dtype_size(c->d.q_dtype);
-    const size_t per_layer_out = static_cast<size_t>(c->d.batch) * c->d.heads * c->d.head_dim * out_size(c);
-    // Selects that cannot ride in the attend tail are batched after the
-    // layers (plans and head shards need them per layer: ledger / exchange).
-    c->in_step = l1 - l0 > 1;  // a single layer gains nothing from batching: keep its tail
-    c->defer_select = !c->has_plan && !c->reduce && !c->prof;
-    c->deferred.clear();
-    skv_status status = SKV_OK;
-    for (int l = l0; l < l1 && status == SKV_OK; ++l) {
-        const size_t o = per_layer * l;
-        status = decode_layer_impl(c, l, n, r, static_cast<const uint8_t*>(q) + o,
-                                   static_cast<const uint8_t*>(k_new) + o, static_cast<const uint8_t*>(v_new) + o,
-                                   static_cast<uint8_t*>(out) + per_layer_out * l, nullptr, nullptr, l > l0, st);
-    }
-    c->defer_select = false;
-    c->in_step = false;
-    if (status != SKV_OK || c->deferred.empty()) {
-        // a failed step leaves its deferred selections uncomputed: drop them
-        for (const auto& d : c->deferred) c->pend_n[d.first] = -1;
-        c->deferred.clear();
-        return status;
-    }
-    // One launch over the deferred layers (consecutive, same shape), in
-    // plain stream order: it needs every attend of the range complete, and
-    // the PDL-chained attends only order against their direct predecessor.
+// One batched select launch over the deferred layers (consecutive, same
+// shape) on stream st; clears the deferred list.
+static skv_status launch_deferred(skv_cache* c, cudaStream_t st) {
+    if (c->deferred.empty()) return SKV_OK;
     skvd::SelectParams p = c->deferred.front().second;
     const int first = c->deferred.front().first;
     const int cnt = static_cast<int>(c->deferred.size());
@@ -1248,6 +1252,65 @@ static skv_status decode_layers(skv_cache* c, int l0, int l1, int n, double r, c
         return fail(SKV_ERR_CUDA, "decode_step: batched select launch: %s", cudaGetErrorString(le));
     }
     return SKV_OK;
+}
+
+// Layers [l0, l1) of one decode step; layer l > l0 launches with programmatic
+// dependent launch: its inputs were complete before the range's first launch,
+// so it can stream while the previous layer's kernels drain. The selects of
+// a step only feed the next step: the first `split` layers' batched select
+// runs on a side stream behind an event, overlapping the remaining layers'
+// attends (HBM-bound) with its fold + top-k (latency-bound), and the rest run
+// batched after the last attend; the caller's stream then joins the side
+// stream. SKV_SELECT_SPLIT=0 keeps one batched select after all attends.
+static skv_status decode_layers(skv_cache* c, int l0, int l1, int n, double r, const void* q, const void* k_new,
+                                const void* v_new, void* out, cudaStream_t st) {
+    const size_t per_layer = static_cast<size_t>(c->d.batch) * c->d.heads * c->d.head_dim * dtype_size(c->d.q_dtype);
+    const size_t per_layer_out = static_cast<size_t>(c->d.batch) * c->d.heads * c->d.head_dim * out_size(c);
+    static const int env_split = [] {
+        const char* e = std::getenv("SKV_SELECT_SPLIT");  // tuning override: layers per side-stream batch
+        return e ? std::atoi(e) : -1;
+    }();
+    // Selects that cannot ride in the attend tail are batched after the
+    // layers (plans and head shards need them per layer: ledger / exchange).
+    c->in_step = l1 - l0 > 1;  // a single layer gains nothing from batching: keep its tail
+    c->defer_select = !c->has_plan && !c->reduce && !c->prof;
+    c->deferred.clear();
+    const int nl = l1 - l0;
+    const int split = !c->defer_select ? 0 : (env_split >= 0 ? std::min(env_split, nl - 1) : (nl >= 8 ? nl / 2 : 0));
+    bool side = false;
+    skv_status status = SKV_OK;
+    for (int l = l0; l < l1 && status == SKV_OK; ++l) {
+        const size_t o = per_layer * l;
+        status = decode_layer_impl(c, l, n, r, static_cast<const uint8_t*>(q) + o,
+                                   static_cast<const uint8_t*>(k_new) + o, static_cast<const uint8_t*>(v_new) + o,
+                                   static_cast<uint8_t*>(out) + per_layer_out * l, nullptr, nullptr, l > l0, st);
+        if (status == SKV_OK && split > 0 && l == l0 + split - 1 && !c->deferred.empty()) {
+            if (!c->sel_st) {
+                SKV_CUDA(cudaStreamCreateWithFlags(&c->sel_st, cudaStreamNonBlocking));
+                SKV_CUDA(cudaEventCreateWithFlags(&c->ev_sel_in, cudaEventDisableTiming));
+                SKV_CUDA(cudaEventCreateWithFlags(&c->ev_sel_out, cudaEventDisableTiming));
+            }
+            SKV_CUDA(cudaEventRecord(c->ev_sel_in, st));
+            SKV_CUDA(cudaStreamWaitEvent(c->sel_st, c->ev_sel_in, 0));
+            status = launch_deferred(c, c->sel_st);
+            SKV_CUDA(cudaEventRecord(c->ev_sel_out, c->sel_st));
+            side = true;
+        }
+    }
+    c->defer_select = false;
+    c->in_step = false;
+    if (status != SKV_OK) {
+        // a failed step leaves its deferred selections uncomputed: drop them
+        for (const auto& d : c->deferred) c->pend_n[d.first] = -1;
+        c->deferred.clear();
+        if (side) cudaStreamWaitEvent(st, c->ev_sel_out, 0);
+        return status;
+    }
+    // in plain stream order: it needs every attend of the range complete (the
+    // PDL-chained attends only order against their direct predecessor)
+    status = launch_deferred(c, st);
+    if (side) SKV_CUDA(cudaStreamWaitEvent(st, c->ev_sel_out, 0));
+    return status;
 }
 
 skv_status skv_swa_decode_step(skv_cache* c, int n, double r, const void* q, const void* k_new,

@@ -14,6 +14,7 @@
 namespace skv_impl {
 
 void count_launch();
+skv_status fail_msg(skv_status s, const char* msg);  // sets skv_last_error()
 
 cudaError_t launch_select(const skvd::SelectParams& p, int batch, bool pdl, cudaStream_t st, int layers = 1);
 cudaError_t launch_scatter_fold(double* imp, long long imp_ld, const float* wpart, int G, int m, const int* tok,

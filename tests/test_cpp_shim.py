@@ -41,3 +41,29 @@ def test_cpp_host_decode_loop():
     assert r.returncode == 0, r.stdout + r.stderr
     assert line["mismatched_steps"] == 0 and line["mismatched_layers"] == 0, line
     assert line["e2e_tokens_per_s"] > 0
+
+
+@pytest.mark.gpu
+def test_cpp_gpu_engine_matches_reference(tmp_path):
+    """the toy-transformer engine step on the GPU
+    (include/skv/b200_engine.hpp: embedding, LayerNorm, projections, the SWA
+    cache decode with the device ledger, FFN, logits) against the unmodified
+    reference skv::Engine::run on the same RunConfig -- dense / SWA / INT8 /
+    local / strided variants, dynamic / static / all-device schedules -- plus
+    the cached-vs-no-cache oracle (oracles.hpp:196-265) and the reference's
+    OutOfDeviceMemory. The GPU run's skvsim.steps.v1 CSV and
+    skvsim.metrics.v1 JSON come from the reference's own report.hpp."""
+    exe = os.path.join(HERE, "cpp", "build", "engine_parity")
+    if not os.path.exists(exe):
+        if os.path.isdir("/root/reference/proj/include"):
+            subprocess.run(["make", "-s", "-C", os.path.join(HERE, "cpp")], check=True)
+        else:
+            pytest.skip("reference headers absent and no prebuilt tests/cpp/build/engine_parity")
+    r = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "ALL OK" in r.stdout, r.stdout + r.stderr
+    steps = (tmp_path / "engine_dense_3phase_steps.csv").read_text().splitlines()
+    assert steps[0].startswith("skvsim.steps.v1,")
+    import json
+
+    m = json.loads((tmp_path / "engine_swa_dynamic_metrics.json").read_text())
+    assert m["schema"] == "skvsim.metrics.v1" and len(m["steps"]) > 0
