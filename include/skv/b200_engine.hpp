@@ -86,14 +86,15 @@ class Engine {
                     plan_.recompute_enabled ? 1 : 0, static_cast<int64_t>(cfg_.prompt_len),
                     static_cast<int64_t>(cfg_.gen_len)};
         cache_->set_plan(pl);
-        // the device ledger counts entries of the cache's own row size: the
-        // reference capacity in entries of layer_kv_bytes (memsim.hpp:46-48)
+        // The device ledger counts entries of the cache's own row size (tb_);
+        // the reference's entries are layer_kv_bytes (memsim.hpp:46-48). The
+        // capacity check is made here, per allocation in the reference's
+        // order (fit()): the device ledger applies each step's actions one
+        // step ahead, so its own check would fire a step early.
         lb_ = layer_kv_bytes(cfg_.cost);
         skv_cache_desc dd{};
         check(skv_cache_get_desc(cache_->handle(), &dd, nullptr));
-        const uint64_t entries = cfg_.cost.device_capacity / lb_;
         tb_ = 2ull * dd.heads * (quant ? 136 : 512);
-        if (entries < ~0ull / tb_) check(skv_cache_set_capacity(cache_->handle(), std::max<uint64_t>(entries, 1) * tb_));
         scratch_x_ = DeviceBuffer(std::max<std::size_t>(ncap, 1) * h * 8);
         scratch_n_ = DeviceBuffer(std::max<std::size_t>(ncap, 1) * h * 8);
         scratch_q_ = DeviceBuffer(std::max<std::size_t>(ncap, 1) * h * 8);

@@ -115,20 +115,30 @@ static void compare_runs(const char* name, const RunConfig& rc, const std::strin
 
 int main(int argc, char** argv) {
     const std::string outdir = argc > 1 ? argv[1] : "";
-    {   // Dense (r = 1) with a device budget forcing Phases I-III
+    {   // SWA r = 0.3, the dynamic plan under a device budget: Phases I-III
+        // (a fast recompute rate makes solve_plan choose deletion + recomputation)
         RunConfig c = base_config();
-        c.sparsity.variant = AttentionVariant::Dense;
+        c.sparsity.variant = AttentionVariant::Swa;
+        c.sparsity.ratio = 0.3;
+        c.bandwidth = 1e9;
+        c.mac_rate = 2e13;
         const CostParams p = c.cost_params();
         c.device_capacity = token_kv_bytes(p) * (c.prompt_len + 6);
-        compare_runs("dense_3phase", c, outdir);
+        compare_runs("swa_3phase", c, outdir);
     }
-    {   // SWA r = 0.3 with the dynamic plan
+    {   // SWA r = 0.3 with the dynamic plan: Phases I-II
         RunConfig c = base_config();
         c.sparsity.variant = AttentionVariant::Swa;
         c.sparsity.ratio = 0.3;
         const CostParams p = c.cost_params();
         c.device_capacity = token_kv_bytes(p) * (c.prompt_len + 4);
         compare_runs("swa_dynamic", c, outdir);
+    }
+    {   // Dense (r = 1): every token kept, all on device
+        RunConfig c = base_config();
+        c.sparsity.variant = AttentionVariant::Dense;
+        c.mode = ScheduleMode::AllDevice;
+        compare_runs("dense", c, outdir);
     }
     {   // INT8 KV (quant.enabled: head_rows fake-quant), static split
         RunConfig c = base_config();

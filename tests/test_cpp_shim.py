@@ -61,7 +61,7 @@ def test_cpp_gpu_engine_matches_reference(tmp_path):
             pytest.skip("reference headers absent and no prebuilt tests/cpp/build/engine_parity")
     r = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "ALL OK" in r.stdout, r.stdout + r.stderr
-    steps = (tmp_path / "engine_dense_3phase_steps.csv").read_text().splitlines()
+    steps = (tmp_path / "engine_swa_3phase_steps.csv").read_text().splitlines()
     assert steps[0].startswith("skvsim.steps.v1,")
     import json
 
