@@ -563,6 +563,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--head-shards", type=int, default=0,
                     help="batch x head mesh: head shards per batch group (0: all ranks when B < world, else 1)")
+    ap.add_argument("--shard-exchange", action="store_true",
+                    help="run the head-shard exchange (one NCCL all-reduce of the step rows per step) even with one "
+                         "head shard: measures its cost against the unsharded step (torchrun --nproc-per-node 1)")
     ap.add_argument("--no-centre", action="store_true",
                     help="time the first K decode steps instead of centring them on the config's decode")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no clocks/baseline/e2e)")
@@ -587,7 +590,7 @@ def main():
 
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or args.shard_exchange:
         import torch.distributed as dist
 
         if backend == "nccl":
@@ -632,6 +635,8 @@ def main():
     cache.set_variant(args.variant)
     if head_shard:
         cache.set_head_shard(h0, cfg["H"], dist_reducer(groups[bi]))
+    elif args.shard_exchange:  # the head-shard exchange path over all heads (overhead measurement)
+        cache.set_head_shard(0, cfg["H"], dist_reducer(None))
 
     sampler = ClockSampler(local) if not args.profile_only else None
     if sampler:
@@ -809,9 +814,11 @@ def main():
                                          "before the W warm-up steps are untimed state preparation")
                        if cfg.get("decode") and not args.no_centre else "steady state at the config's KV length",
                        "parallelism": (f"batch x{n_bgroups} x head x{head_shards} ({B} sequences, {H} of {cfg['H']} "
-                                       "heads per GPU; one fp64 all-reduce of the step row per layer-step within "
-                                       "each batch group)") if head_shard
-                       else f"batch-sharded x{world} (no collective)", "rank0_batch_offset": b0,
+                                       "heads per GPU; one fp64 all-reduce of every layer's step rows per step "
+                                       "within each batch group)") if head_shard
+                       else (f"batch-sharded x{world} + the head-shard exchange over one shard (--shard-exchange)"
+                             if args.shard_exchange else f"batch-sharded x{world} (no collective)"),
+                       "rank0_batch_offset": b0,
                        "l2": ("inputs larger than L2 (per-step KV gather >> 126 MB)" if args.config != 1 else
                               "config 1 is the latency-bound parity case: its 3.4 MB/step fit in L2")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -151,7 +151,7 @@ struct skv_cache {
     skv_reduce_fn reduce = nullptr;
     void* reduce_user = nullptr;
     int head_offset = 0, total_heads = 0;
-    double* xbuf = nullptr;  // [B][Ncap] step rows / prefill seed rows, then [B] prefill sparsity
+    double* xbuf = nullptr;  // head shards: [L][B][Ncap] step rows of a whole step / prefill seed rows + [B] sparsity
     uint64_t* gkeys = nullptr;  // [L][B][Ncap] top-k keys of long contexts (lazily)
     int* gtok = nullptr;        // [B][H][Ncap] attend token lists of long selections (lazily)
     float* gwts = nullptr;      // [B][H][Ncap] their logits / weights
@@ -876,7 +876,7 @@ skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok
     if (fold.apply) {
         if (fused) {
             note_pending(c, layer, sel, fold.r_next);
-        } else if (c->reduce) {
+        } else if (c->reduce && !c->defer_select) {
             // head shards: this shard's head-summed row -> all-reduce across
             // the shards (the caller's collective, ordered on st) -> fold it
             // and select; every shard then holds the same importance and
@@ -1246,7 +1246,31 @@ static skv_status launch_deferred(skv_cache* c, cudaStream_t st) {
     p.pdl_wait = 0;
     const std::vector<std::pair<int, skvd::SelectParams>> pending = std::move(c->deferred);
     c->deferred.clear();
-    const cudaError_t le = launch_select(p, c->d.batch, false, st, cnt);
+    cudaError_t le = cudaSuccess;
+    if (c->reduce) {
+        // head shards: every layer's head-summed step row of this shard in one
+        // pass, ONE all-reduce of the whole step's rows across the shards (the
+        // caller's collective on st), then every layer's fold + selection
+        // from the summed rows -- off the per-layer critical path
+        skvd::SelectParams pp = p;
+        pp.wsum_out = c->xbuf;
+        pp.ls_wsum = static_cast<long long>(c->d.batch) * p.m_prev;
+        pp.select = 0;
+        le = launch_select(pp, c->d.batch, false, st, cnt);
+        if (le == cudaSuccess) {
+            const skv_status e =
+                c->reduce(c->xbuf, static_cast<size_t>(cnt) * c->d.batch * p.m_prev, st, c->reduce_user);
+            if (e != SKV_OK) {
+                for (const auto& d : pending) c->pend_n[d.first] = -1;
+                return fail(e, "head-shard reduce failed (%d)", static_cast<int>(e));
+            }
+            p.wsum = c->xbuf;
+            p.ls_wsum = pp.ls_wsum;
+            le = launch_select(p, c->d.batch, false, st, cnt);
+        }
+    } else {
+        le = launch_select(p, c->d.batch, false, st, cnt);
+    }
     if (le != cudaSuccess) {
         for (const auto& d : pending) c->pend_n[d.first] = -1;
         return fail(SKV_ERR_CUDA, "decode_step: batched select launch: %s", cudaGetErrorString(le));
@@ -1273,10 +1297,12 @@ static skv_status decode_layers(skv_cache* c, int l0, int l1, int n, double r, c
     // Selects that cannot ride in the attend tail are batched after the
     // layers (plans and head shards need them per layer: ledger / exchange).
     c->in_step = l1 - l0 > 1;  // a single layer gains nothing from batching: keep its tail
-    c->defer_select = !c->has_plan && !c->reduce && !c->prof;
+    c->defer_select = !c->has_plan && !c->prof;  // head shards exchange the whole step's rows at once
     c->deferred.clear();
     const int nl = l1 - l0;
-    const int split = !c->defer_select ? 0 : (env_split >= 0 ? std::min(env_split, nl - 1) : (nl >= 8 ? nl / 2 : 0));
+    const int split = (!c->defer_select || c->reduce)
+                          ? 0
+                          : (env_split >= 0 ? std::min(env_split, nl - 1) : (nl >= 8 ? nl / 2 : 0));
     bool side = false;
     skv_status status = SKV_OK;
     for (int l = l0; l < l1 && status == SKV_OK; ++l) {
@@ -1603,7 +1629,11 @@ skv_status skv_cache_set_head_shard(skv_cache* c, int head_offset, int total_hea
                 "head shard: heads [offset, offset + H) must lie inside total_heads");
     DeviceGuard guard(c->d.device);
     if (c->xbuf == nullptr) {
-        const size_t bytes = static_cast<size_t>(c->d.batch) * (c->d.capacity + 1) * 8;
+        // the prefill's seed rows + sparsity ([B][Ncap + 1]) or a whole
+        // step's step rows ([L][B][m], m <= Ncap)
+        const size_t cells = std::max(static_cast<size_t>(c->d.batch) * (c->d.capacity + 1),
+                                      static_cast<size_t>(c->d.layers) * c->d.batch * c->d.capacity);
+        const size_t bytes = cells * 8;
         if (cudaMalloc(reinterpret_cast<void**>(&c->xbuf), bytes) != cudaSuccess) {
             cudaGetLastError();
             return fail(SKV_ERR_OOM, "head shard: cannot allocate the exchange row");

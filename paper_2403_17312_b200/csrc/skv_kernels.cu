@@ -416,6 +416,8 @@ __global__ void __launch_bounds__(kSelectThreads) swa_select_kernel(const Select
     q.idx += y * p.ls_idx;
     if (q.tok_prev) q.tok_prev += y * p.ls_idx;
     q.sparsity += y * p.ls_sp;
+    if (q.wsum) q.wsum += y * p.ls_wsum;
+    if (q.wsum_out) q.wsum_out += y * p.ls_wsum;
     fold_and_select<kSelectThreads, 1>(q, blockIdx.x, threadIdx.x, s, keys, scratch);
 }
 

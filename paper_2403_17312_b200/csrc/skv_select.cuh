@@ -51,6 +51,7 @@ struct SelectParams {
     // several layers in one launch (blockIdx.y = layer offset): element
     // strides of imp, wpart, idx/tok_prev and sparsity per layer (0: one layer)
     long long ls_imp, ls_wpart, ls_idx, ls_sp;
+    long long ls_wsum;  // per-layer stride of wsum / wsum_out (head-shard rows of a whole step)
     // long contexts: the candidates' keys live in global scratch laid out like
     // imp ([layers][B][imp_ld], same strides) instead of shared memory
     uint64_t* gkeys;

@@ -28,7 +28,10 @@ def _inputs():
     return kv, qp, qs
 
 
-def _run(h0, nh, reducer=None):
+def _run(h0, nh, reducer=None, whole_step=False):
+    """whole_step: skv_swa_decode_step over all layers (the head shards
+    exchange every layer's step rows in ONE all-reduce per step); else one
+    skv_swa_decode_layer per layer (one exchange per layer-step)."""
     from paper_2403_17312_b200 import api
 
     kv, qp, qs = _inputs()
@@ -43,6 +46,14 @@ def _run(h0, nh, reducer=None):
         res["sp"].append(cache.prefill_sparsity(l).cpu())
     for j in range(STEPS):
         n = S + j + 1
+        if whole_step:
+            for l in range(L):
+                res["idx"].append(cache.pending_selection(l, n, R).cpu() if j > 0 else torch.zeros(0))
+            out = torch.empty((L, B, nh, D), dtype=torch.float16, device="cuda")
+            cache.swa_decode_step(n, R, qs[j, :, :, hs].contiguous().cuda(), kv[:, :, n - 1, 0, hs].contiguous().cuda(),
+                                  kv[:, :, n - 1, 1, hs].contiguous().cuda(), out)
+            res["out"].extend(out.cpu().unbind(0))
+            continue
         for l in range(L):
             out, idx, _ = cache.swa_decode_layer(l, n, R, qs[j, l, :, hs].contiguous().cuda(),
                                                  kv[l, :, n - 1, 0, hs].contiguous().cuda(),
@@ -62,7 +73,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, backend, path):
+def _worker(rank, world, port, backend, path, whole_step=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
@@ -72,7 +83,7 @@ def _worker(rank, world, port, backend, path):
         from paper_2403_17312_b200.shard import dist_reducer, head_shard_range
 
         h0, nh = head_shard_range(H, world, rank)
-        torch.save((h0, nh, _run(h0, nh, dist_reducer())), os.path.join(path, f"rank{rank}.pt"))
+        torch.save((h0, nh, _run(h0, nh, dist_reducer(), whole_step)), os.path.join(path, f"rank{rank}.pt"))
     finally:
         dist.destroy_process_group()
 
@@ -92,10 +103,11 @@ def _check(want, parts):
             torch.testing.assert_close(b, a, rtol=0, atol=1e-12)
 
 
+@pytest.mark.parametrize("whole_step", [False, True])
 @pytest.mark.parametrize("world,backend", [(2, "gloo"), (1, "nccl")])
-def test_head_sharded_equals_unsharded(tmp_path, world, backend):
-    want = _run(0, H)
-    mp.start_processes(_worker, args=(world, _free_port(), backend, str(tmp_path)), nprocs=world,
+def test_head_sharded_equals_unsharded(tmp_path, world, backend, whole_step):
+    want = _run(0, H, whole_step=whole_step)
+    mp.start_processes(_worker, args=(world, _free_port(), backend, str(tmp_path), whole_step), nprocs=world,
                        start_method="spawn")
     _check(want, [torch.load(os.path.join(tmp_path, f"rank{r}.pt")) for r in range(world)])
 
