@@ -390,7 +390,27 @@ def calibrate_costs(api, torch, cfg, g) -> dict:
     ms = c.profile_move(0, rows, reps=5)
     c.close()
     moved = 2 * rows * B * (2 * H * D * 2)
+    # the recompute GEMM's own MAC rate (the tcgen05 kernel recompute_kv runs:
+    # [rows x h] . [h x 2h]); the reference prices recompute at mac_rate, so
+    # this only feeds the second replay column
+    import ctypes as C
+
+    M = 4096
+    A = torch.randn((M, h), generator=g, device="cuda", dtype=torch.float16)
+    Bt = torch.randn((2 * h, h), generator=g, device="cuda", dtype=torch.float16)
+    Cm = torch.empty((M, 2 * h), device="cuda", dtype=torch.float32)
+    run = lambda: api.check(api.lib().skv_gemm_tn(C.c_void_p(A.data_ptr()), C.c_void_p(Bt.data_ptr()),  # noqa: E731
+                                                  C.c_void_p(Cm.data_ptr()), M, 2 * h, h, 0, None))
+    run()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    gemm_rate = 5.0 * M * 2 * h * h / (e0.elapsed_time(e1) / 1000.0)
     return {"mac_rate": fit["fitted_mac_rate"], "bandwidth": moved / (ms / 1000.0), "mac_fit": fit,
+            "recompute_gemm_mac_rate": gemm_rate,
             "bandwidth_probe": {"rows_each_way_per_seq": rows, "seqs": B, "bytes": moved, "ms": ms,
                                 "kernel": "skvd::kv_move_kernel (offload + reload in one launch)"}}
 
@@ -510,6 +530,7 @@ def run_config5(args, cfg, rank: int, world: int):
             replay_t = row_bytes * copies / cost["bandwidth"]
             replay_r = 2.0 * h * h * got.get("recomputed_rows", 0) / cost["mac_rate"]
             replay = replay_c + replay_t + replay_r
+            replay_rg = 2.0 * h * h * got.get("recomputed_rows", 0) / cal["recompute_gemm_mac_rate"]
             table[f"phase{ph}"] = dict(got, predicted_s=want, predicted_compute_s=pr["phase_compute"][ph - 1],
                                        predicted_transfer_s=pr["phase_transfer"][ph - 1],
                                        predicted_recompute_s=pr["phase_recompute"][ph - 1],
@@ -518,6 +539,9 @@ def run_config5(args, cfg, rank: int, world: int):
                                        replay_s=replay, replay_compute_s=replay_c, replay_transfer_s=replay_t,
                                        replay_recompute_s=replay_r,
                                        replay_rel_error=(got["measured_s"] - replay) / replay if replay else None,
+                                       replay_gemm_rate_s=replay_c + replay_t + replay_rg,
+                                       replay_gemm_rate_rel_error=(got["measured_s"] - (replay_c + replay_t + replay_rg))
+                                       / (replay_c + replay_t + replay_rg) if replay else None,
                                        tokens_per_s=world * B * got["steps"] / got["measured_s"])
         results[name] = {"plan": pl, "predicted_total_decode_s": pr["total_seconds"] - pr["prefill_compute_seconds"],
                          "measured_decode_s": res["decode_s"],
@@ -544,8 +568,10 @@ def run_config5(args, cfg, rank: int, world: int):
                 "note": "value = the solved schedule's decode tokens/s on a paged device KV bounded by the "
                         "budget; schedules[*].phases set measured seconds beside PlanPrediction's (predicted_s: "
                         "simulate_plan prices every global pick as a reload, scheduler.hpp:88-92) and beside the "
-                        "same cost model priced on the rows this run moved (replay_s); call j is booked to the "
-                        "phase of step j + 1, whose ledger actions and movement it runs"}
+                        "same cost model priced on the rows this run moved (replay_s: rows copied = offloaded + "
+                        "reloaded - kept; replay_gemm_rate_s: recompute priced at the tcgen05 GEMM's measured MAC "
+                        "rate instead of the attention-fitted mac_rate); call j is booked to the phase of step "
+                        "j + 1, whose ledger actions and movement it runs"}
         print(json.dumps(line), flush=True)
 
 

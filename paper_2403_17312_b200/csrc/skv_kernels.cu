@@ -94,7 +94,10 @@ __global__ void __launch_bounds__(kLedgerThreads) ledger_step_kernel(const Ledge
     __shared__ int s_split;
     extern __shared__ __align__(128) uint8_t smem[];
     const int b = blockIdx.x, tid = threadIdx.x;
-    pdl_wait();  // the selection comes from the preceding select kernel
+    // Phase I only stores the step's new token: nothing of the preceding
+    // attend / select is read, so the next layer's attend may start at once.
+    // Every other phase reads the selection the preceding kernel made.
+    if (p.phase != 1) pdl_wait();
     pdl_launch_dependents();
     const int ntok = p.existing;
     const bool paged = p.slots.slot != nullptr;
