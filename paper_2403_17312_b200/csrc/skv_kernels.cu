@@ -71,12 +71,12 @@ __device__ void ledger_account(const LedgerParams& p, int b, long long d_dev, lo
     atomicMax(&p.tot->peak_dev_tokens, dev);
     const unsigned long long e = p.tok_bytes;
     const unsigned long long ex = atomicExch(&p.tot->exhausted, 0ull);
-    if (dev * e > p.cap_bytes) {  // the reference's check comes first
+    if (dev > p.cap_tokens) {  // dev * e > capacity: the reference's check comes first
         const unsigned long long t0 = dev - al;
-        const unsigned long long fit = p.cap_bytes / e;
-        report_status(p.status, 2, p.layer, -1, -1, p.step, e * ((t0 > fit ? t0 : fit) + 1), p.cap_bytes);
+        const unsigned long long fit = p.cap_tokens;
+        report_status_inl(p.status, 2, p.layer, -1, -1, p.step, e * ((t0 > fit ? t0 : fit) + 1), p.cap_bytes);
     } else if (ex) {  // within the capacity, but one (layer, sequence) pool ran dry
-        report_status(p.status, 2, p.layer, -1, -1, p.step, 0ull, p.cap_bytes);
+        report_status_inl(p.status, 2, p.layer, -1, -1, p.step, 0ull, p.cap_bytes);
     }
     *p.arrive = 0;
 }

@@ -44,7 +44,7 @@ struct LedgerTotals {
     unsigned long long kept;       // cumulative reloads of rows offloaded in the same step (no copy in)
 };
 
-static __device__ __noinline__ void report_status(DevStatus* st, int code, int layer, int seq, int token, long long step,
+__device__ __forceinline__ void report_status_inl(DevStatus* st, int code, int layer, int seq, int token, long long step,
                                               unsigned long long needed, unsigned long long cap) {
     if (st == nullptr) return;
     if (atomicCAS(&st->code, 0, -1) == 0) {  // first failure wins
@@ -57,6 +57,12 @@ static __device__ __noinline__ void report_status(DevStatus* st, int code, int l
         __threadfence_system();
         atomicExch(&st->code, code);
     }
+}
+// Out of line for the attend kernel (a cold path that must not cost it
+// registers); kernels with room call report_status_inl.
+static __device__ __noinline__ void report_status(DevStatus* st, int code, int layer, int seq, int token, long long step,
+                                              unsigned long long needed, unsigned long long cap) {
+    report_status_inl(st, code, layer, seq, token, step, needed, cap);
 }
 
 // Paged store: every (layer, sequence) owns `pcap` token slots of the pool;
@@ -106,6 +112,7 @@ struct LedgerParams {
     unsigned* arrive;  // this layer's arrival counter (0 between launches)
     unsigned long long* layer_allocs;  // this layer's allocation count accumulator (0 between launches)
     unsigned long long cap_bytes, tok_bytes;
+    unsigned long long cap_tokens;  // floor(cap_bytes / tok_bytes), host-computed (no 64-bit division on device)
     int layer;
     long long step;
     DevStatus* status;
