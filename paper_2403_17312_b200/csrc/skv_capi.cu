@@ -952,7 +952,7 @@ skv_status launch_ledger_c(skv_cache* c, int layer, long long j, const int* sel,
     }
     p.cap_bytes = c->cap_bytes;
     p.tok_bytes = c->tok_bytes;
-    p.cap_tokens = c->cap_bytes / c->tok_bytes;
+    p.cap_tokens = c->cap_bytes == ~0ull ? ~0ull : c->cap_bytes / c->tok_bytes;  // unbounded: never fails
     p.layer = layer;
     p.step = j;
     p.status = c->status_dev;

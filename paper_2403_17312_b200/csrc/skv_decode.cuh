@@ -33,6 +33,9 @@
 #ifndef SKV_STAGES
 #define SKV_STAGES 4
 #endif
+#ifndef SKV_U8_META_PREFETCH
+#define SKV_U8_META_PREFETCH 1
+#endif
 
 namespace skvd {
 
@@ -443,7 +446,7 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
         // row's dot after the transposed reduction picks its own below; a
         // scattered read at that point conflicted ~7-way, profiles/r2)
         float2 msv[QUANT ? RS : 1];
-        if constexpr (QUANT) {
+        if constexpr (QUANT && SKV_U8_META_PREFETCH) {
 #pragma unroll
             for (int i = 0; i < RS; ++i) msv[i] = meta_at(ring + stage * STAGEB, slot + i * SLOTS);
         }
@@ -469,8 +472,12 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
             float logit;
             if constexpr (QUANT) {
                 float2 ms = msv[0];
+                if constexpr (SKV_U8_META_PREFETCH) {
 #pragma unroll
-                for (int i = 1; i < RS; ++i) ms = rsel == i ? msv[i] : ms;
+                    for (int i = 1; i < RS; ++i) ms = rsel == i ? msv[i] : ms;
+                } else {
+                    ms = meta_at(ring + stage * STAGEB, r);
+                }
                 // codes arrive as 1024 + c (cvt16x2, KvU8): dot = q.c + 1024 * sum(q)
                 logit = fmaf(ms.x, dot, fmaf(-kBiasU8, ms.x, ms.y) * qsum) * scale;
             } else {
