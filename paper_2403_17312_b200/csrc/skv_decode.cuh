@@ -33,9 +33,6 @@
 #ifndef SKV_STAGES
 #define SKV_STAGES 4
 #endif
-#ifndef SKV_U8_META_PREFETCH
-#define SKV_U8_META_PREFETCH 1
-#endif
 
 namespace skvd {
 
@@ -120,11 +117,6 @@ struct DecodeCfg {
     static_assert(SLOTS * D * 4 <= S * STAGEB, "reduction scratch aliases the ring");
 };
 
-// Row stride of the per-head logit / weight rows in shared memory: m padded
-// to 1 (mod 32), so the lanes that store one chunk's logits (4 heads x 4
-// tokens per warp) hit 16 distinct banks.
-__host__ __device__ inline int wts_stride(int m) { return m + ((33 - (m & 31)) & 31); }
-
 struct DecodeSmem {
     size_t ring, bars, tok, slot, wts, topk, scratch, flag, total;
 };
@@ -145,8 +137,8 @@ __host__ __device__ inline DecodeSmem decode_smem(int m, bool gmem = false, bool
     o = align_up(o + static_cast<size_t>(m) * 4, 16);
     s.slot = o;  // paged: the selected tokens' slots
     o = align_up(o + (paged ? static_cast<size_t>(m) * 4 : 0), 16);
-    s.wts = o;  // logits, then weights [HG][wts_stride(m)] f32
-    o = align_up(o + static_cast<size_t>(HG) * wts_stride(m) * 4, 16);
+    s.wts = o;  // logits, then weights [HG][m] f32
+    o = align_up(o + static_cast<size_t>(HG) * m * 4, 16);
     s.topk = o;
     o = align_up(o + sizeof(TopkSmem<kConsumerThreads>), 16);
     s.scratch = o;
@@ -217,8 +209,7 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
     int* tok = gmem ? p.gtok + (static_cast<size_t>(b) * gridDim.x + g) * p.Ncap
                     : reinterpret_cast<int*>(smem + L.tok);
     float* wts = gmem ? p.gwts + (static_cast<size_t>(b) * gridDim.x + g) * HG * p.Ncap
-                      : reinterpret_cast<float*>(smem + L.wts);  // [HG][mw]
-    const int mw = gmem ? m : wts_stride(m);  // row stride of wts
+                      : reinterpret_cast<float*>(smem + L.wts);  // [HG][m]
 
     // Let the next kernel in the stream (the select kernel) get scheduled now;
     // it waits for this grid's completion before touching our outputs.
@@ -441,15 +432,6 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
             for (int i = 0; i < RS; ++i)
                 raw[i] = slot + i * SLOTS < rows ? ld16(st + i * SLOTS * ROWE) : make_uint4(0u, 0u, 0u, 0u);
         }
-        // INT8: this lane's rows' (scale, bias) pairs, read now in the same
-        // broadcast pattern as the codes (the lane that ends up holding a
-        // row's dot after the transposed reduction picks its own below; a
-        // scattered read at that point conflicted ~7-way, profiles/r2)
-        float2 msv[QUANT ? RS : 1];
-        if constexpr (QUANT && SKV_U8_META_PREFETCH) {
-#pragma unroll
-            for (int i = 0; i < RS; ++i) msv[i] = meta_at(ring + stage * STAGEB, slot + i * SLOTS);
-        }
         float part[RS];
 #pragma unroll
         for (int i = 0; i < RS; ++i) {
@@ -471,19 +453,13 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
             const int t = r / HG;
             float logit;
             if constexpr (QUANT) {
-                float2 ms = msv[0];
-                if constexpr (SKV_U8_META_PREFETCH) {
-#pragma unroll
-                    for (int i = 1; i < RS; ++i) ms = rsel == i ? msv[i] : ms;
-                } else {
-                    ms = meta_at(ring + stage * STAGEB, r);
-                }
+                const float2 ms = meta_at(ring + stage * STAGEB, r);
                 // codes arrive as 1024 + c (cvt16x2, KvU8): dot = q.c + 1024 * sum(q)
                 logit = fmaf(ms.x, dot, fmaf(-kBiasU8, ms.x, ms.y) * qsum) * scale;
             } else {
                 logit = dot * scale;
             }
-            wts[h * mw + base + t] = logit;
+            wts[h * m + base + t] = logit;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
@@ -492,7 +468,7 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
 
     // ---- softmax with the reference's normaliser (attention.hpp:213-218)
     for (int hh = warp; hh < HG; hh += kConsumerWarps) {
-        float* wl = wts + hh * mw;
+        float* wl = wts + hh * m;
         float mx = -INFINITY;
         for (int i = lane; i < m; i += 32) mx = fmaxf(mx, wl[i]);
 #pragma unroll
@@ -516,14 +492,14 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
         for (int pos = ctid; pos < m; pos += kConsumerThreads) {
             float s = 0.f;
 #pragma unroll
-            for (int hh = 0; hh < HG; ++hh) s += wts[hh * mw + pos];
+            for (int hh = 0; hh < HG; ++hh) s += wts[hh * m + pos];
             wp[pos] = s;
         }
         if (p.idx_out != nullptr && g == 0)
             for (int pos = ctid; pos < m; pos += kConsumerThreads) p.idx_out[static_cast<size_t>(b) * m + pos] = tok[pos];
         if (p.w_out != nullptr)
             for (int i = ctid; i < HG * m; i += kConsumerThreads)
-                p.w_out[(static_cast<size_t>(b) * H + g * HG) * m + i] = wts[(i / m) * mw + i % m];
+                p.w_out[(static_cast<size_t>(b) * H + g * HG) * m + i] = wts[i];
     }
 
     // ---- pass 2: attn = sum_t w_t * V[t]  (attention.hpp:219-225)
@@ -531,7 +507,7 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
 #pragma unroll
     for (int i = 0; i < V2; ++i) acc[i] = make_float2(0.f, 0.f);
     float bsum = 0.f;
-    const float* wh = wts + h * mw;
+    const float* wh = wts + h * m;
     for (int u = nchunks; u < 2 * nchunks; ++u) {
         const int stage = u % S;
         mbar_wait(&full[stage], (u / S) & 1);
