@@ -538,9 +538,10 @@ namespace {
 // Pick heads-per-CTA. Bigger head groups mean bigger bulk copies (the
 // producer's per-copy issue cost is the limiter, profiles/r1_v3_*) and fewer
 // per-CTA select/softmax phases; layer-to-layer PDL overlap covers a grid
-// smaller than one wave. So: the largest group that still gives >= half an
-// SM's worth of CTAs per SM count; for tiny batches the smallest group (most
-// parallelism). SKV_HG overrides (tuning).
+// smaller than one wave. So: the largest group that still gives at least one
+// CTA per SM (config 3: HG 4, 160 CTAs -- isolated 0.44 -> 0.50 of the copy
+// peak at an equal step, profiles/r2); for tiny batches the smallest group
+// (most parallelism). SKV_HG overrides (tuning).
 //
 // Selections too long for any head group's shared-memory token list and
 // weights (m beyond ~24 k) run with both in global scratch (gmem).
@@ -567,7 +568,7 @@ skv_status pick_attend(skv_cache* c, int m, const DecodeLaunch** dl_out, size_t*
             smallest = dl;
             smallest_smem = smem;
             const long long ctas = static_cast<long long>(c->d.batch) * (c->d.heads / hg);
-            if (!chosen && 2 * ctas >= c->num_sms) {
+            if (!chosen && ctas >= c->num_sms) {
                 chosen = dl;
                 chosen_smem = smem;
             }
