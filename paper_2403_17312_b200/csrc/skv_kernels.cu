@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(256) kv_move_kernel(const MoveParams p) {
 }
 
 // Importance fold + next selection, one CTA per sequence (skv_select.cuh).
-__global__ void __launch_bounds__(kSelectThreads, 4) swa_select_kernel(const SelectParams p) {
+__global__ void __launch_bounds__(kSelectThreads) swa_select_kernel(const SelectParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     TopkSmem<kSelectThreads>& s = *reinterpret_cast<TopkSmem<kSelectThreads>*>(smem);
     uint64_t* keys = reinterpret_cast<uint64_t*>(smem + align_up(sizeof(TopkSmem<kSelectThreads>), 16));

@@ -102,9 +102,7 @@ __device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<N
     const int nc = topk ? p.n - p.k : 0;
     double* kd = reinterpret_cast<double*>(keys);
     SEL_TRACE(0);
-    // folded positions per thread held in registers (fast path): 128-thread
-    // batched selects cover m_prev <= 1024 (config 4: m = 820) in one round trip
-    constexpr int R = NT >= 256 ? 4 : 8;
+    constexpr int R = 4;  // folded positions per thread held in registers (fast path)
     if (p.apply) {
         const float* wp = p.wpart + static_cast<size_t>(b) * p.G * p.m_prev;
         const int* tp = p.tok_prev ? p.tok_prev + static_cast<size_t>(b) * p.tok_prev_ld : nullptr;
