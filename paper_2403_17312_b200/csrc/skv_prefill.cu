@@ -564,19 +564,22 @@ __global__ void __launch_bounds__(kFThreads, 1)
 __global__ void prefill_seed_kernel(const float* __restrict__ wlast, const float* __restrict__ llast,
                                     const unsigned* __restrict__ below, double* __restrict__ imp,
                                     double* __restrict__ psp, int H, int s, long long imp_ld, int h_div) {
+    extern __shared__ double inv_l[];  // [H] 1 / l per head, once per block (not one fp64 divide per cell)
     const int b = blockIdx.y;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int h = threadIdx.x; h < H; h += blockDim.x) inv_l[h] = 1.0 / static_cast<double>(llast[b * H + h]);
     if (psp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
         const double cells = 0.5 * static_cast<double>(s) * static_cast<double>(s + 1);
         double sp = 0.0;
         for (int h = 0; h < H; ++h) sp += static_cast<double>(below[b * H + h]) / cells;
         psp[b] = sp / static_cast<double>(h_div);  // h_div = all heads of the model (H unless head-sharded)
     }
+    __syncthreads();
     if (j >= s) return;
+    const float* w = wlast + static_cast<size_t>(b) * H * s + j;
     double acc = 0.0;
-    for (int h = 0; h < H; ++h)
-        acc += static_cast<double>(wlast[(static_cast<size_t>(b) * H + h) * s + j]) /
-               static_cast<double>(llast[b * H + h]);
+#pragma unroll 8
+    for (int h = 0; h < H; ++h) acc = fma(static_cast<double>(w[static_cast<size_t>(h) * s]), inv_l[h], acc);
     imp[static_cast<size_t>(b) * imp_ld + j] = acc;
 }
 
@@ -687,8 +690,8 @@ cudaError_t launch_prefill(bool bf16, bool out_f32, const void* kv, const void* 
     if (e != cudaSuccess) return e;
     e = bf16 ? run_flash<true, false>(mq, mkv, p, st) : run_flash<false, false>(mq, mkv, p, st);
     if (e != cudaSuccess) return e;
-    prefill_seed_kernel<<<dim3((s + 255) / 256, B), 256, 0, st>>>(wlast, llast, below, imp, psp, H, s, imp_ld,
-                                                                  h_div > 0 ? h_div : H);
+    prefill_seed_kernel<<<dim3((s + 127) / 128, B), 128, static_cast<size_t>(H) * 8, st>>>(
+        wlast, llast, below, imp, psp, H, s, imp_ld, h_div > 0 ? h_div : H);
     count_launch();
     return cudaGetLastError();
 }
