@@ -151,11 +151,30 @@ __device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<N
                 vmax = v[r] > vmax ? v[r] : vmax;
             }
         } else {
-            for (int pos = tid; pos < p.m_prev; pos += NT) {
-                const double w = row(pos);
-                const int t = tp ? tp[pos] : pos;
-                imp[t] = (assign_all || t == p.cur_tok) ? w : imp[t] + w;
-                vmax = w > vmax ? w : vmax;
+            // Long selections (config 4: m = 820 at 128 threads): rounds of R
+            // positions per thread, every load of a round issued before its
+            // adds (the serial per-position chain was latency-bound, profiles/r2)
+            for (int base = tid; base < p.m_prev; base += R * NT) {
+                int t[R];
+                double w[R], old[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int pos = base + r * NT;
+                    t[r] = -1;
+                    w[r] = 0.0;
+                    old[r] = 0.0;
+                    if (pos < p.m_prev) {
+                        t[r] = tp ? tp[pos] : pos;
+                        w[r] = row(pos);
+                        if (!assign_all && t[r] != p.cur_tok) old[r] = imp[t[r]];
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if (t[r] < 0) continue;
+                    imp[t[r]] = (assign_all || t[r] == p.cur_tok) ? w[r] : old[r] + w[r];
+                    vmax = w[r] > vmax ? w[r] : vmax;
+                }
             }
             named_sync(BAR, NT);  // the folded importance is visible to the staging
             stage_candidates<NT>(kd, imp, nc, tid);
@@ -179,7 +198,13 @@ __device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<N
 #pragma unroll
                 for (int r = 0; r < R; ++r) below += (tid + r * NT < p.m_prev) && v[r] < thr;
             } else {
-                for (int pos = tid; pos < p.m_prev; pos += NT) below += row(pos) < thr;
+                for (int base = tid; base < p.m_prev; base += R * NT) {
+                    double w[R];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) w[r] = base + r * NT < p.m_prev ? row(base + r * NT) : thr;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) below += w[r] < thr;
+                }
             }
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) below += __shfl_xor_sync(0xffffffffu, below, off);
