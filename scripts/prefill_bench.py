@@ -80,6 +80,29 @@ def main():
             line["flash_attn_tflops"] = round(flops / fms / 1e9, 1)
         except Exception as ex:  # library absent or unsupported arch
             line["flash_attn"] = f"unavailable: {type(ex).__name__}: {ex}"[:160]
+        try:
+            # cuDNN's fused attention through torch SDPA (a Blackwell-native library kernel), [B, H, s, D] views
+            from torch.nn.attention import SDPBackend, sdpa_kernel
+
+            qt, kt, vt = (x.transpose(1, 2) for x in (q, k, v))
+            with sdpa_kernel(SDPBackend.CUDNN_ATTENTION):
+                for _ in range(2):
+                    torch.nn.functional.scaled_dot_product_attention(qt, kt, vt, is_causal=True)
+                torch.cuda.synchronize()
+                cts = []
+                for _ in range(args.iters):
+                    flush.zero_()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    torch.nn.functional.scaled_dot_product_attention(qt, kt, vt, is_causal=True)
+                    e1.record()
+                    torch.cuda.synchronize()
+                    cts.append(e0.elapsed_time(e1))
+            cms = sorted(cts)[len(cts) // 2]
+            line["cudnn_sdpa_ms"] = round(cms, 3)
+            line["cudnn_sdpa_tflops"] = round(flops / cms / 1e9, 1)
+        except Exception as ex:
+            line["cudnn_sdpa"] = f"unavailable: {type(ex).__name__}: {ex}"[:160]
         print(json.dumps(line), flush=True)
         cache.close()
         del k, v, q
