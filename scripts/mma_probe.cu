@@ -69,6 +69,17 @@ __global__ void probe(long long* out, int variant, int n, int iters) {
                     case 3:  // TS (A from TMEM), B K-major
                         mma_ts(tmem + 256, tmem + kk * 8, desc(sm + 65536 + kk * 32, 16, 1024), idesc(n, false), 1);
                         break;
+                    case 4:  // SS A-K B-K, two independent accumulators alternating
+                        mma_ss(tmem + 256 + (i & 1) * 128, desc(sm + kk * 32, 16, 1024),
+                               desc(sm + 65536 + kk * 32, 16, 1024), idesc(n, false), 1);
+                        break;
+                    case 5:  // alternating an S-like SS MMA and a P.V-like TS MMA into separate accumulators
+                        if (i & 1)
+                            mma_ts(tmem + 384, tmem + kk * 8, desc(sm + 65536 + kk * 2048, 16384, 1024), idesc(128, true), 1);
+                        else
+                            mma_ss(tmem + 256, desc(sm + kk * 32, 16, 1024), desc(sm + 65536 + kk * 32, 16, 1024),
+                                   idesc(n > 128 ? 128 : n, false), 1);
+                        break;
                 }
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -93,8 +104,9 @@ int main() {
     long long* d;
     cudaMalloc(&d, 8);
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    const char* names[4] = {"SS  A-K B-K ", "SS  A-K B-MN", "TS  A-T B-MN", "TS  A-T B-K "};
-    for (int v = 0; v < 4; ++v)
+    const char* names[6] = {"SS  A-K B-K ", "SS  A-K B-MN", "TS  A-T B-MN", "TS  A-T B-K ", "SS x2 accum ",
+                            "SS|TS alt   "};
+    for (int v = 0; v < 6; ++v)
         for (int n : {64, 128, 256}) {
             const int iters = 512;
             probe<<<1, 128, 200 * 1024>>>(d, v, n, iters);
