@@ -142,8 +142,8 @@ __host__ __device__ constexpr uint32_t flash_idesc() {
 template <bool BF16, bool STATS>
 struct FlashSmem {
     static constexpr int kQ = 0;                                // [2] query tiles (double buffered across items)
-    static constexpr int kK = kQ + 2 * kFTileBytes;             // [kFBufs] key tiles
-    static constexpr int kV = kK + kFBufs * kFKBytes;           // [kFBufs] value tiles (pass 2)
+    static constexpr int kK = kQ + 2 * kFTileBytes;             // [kFBufs] key tiles (pass 1: 256 keys)
+    static constexpr int kV = kK + kFBufs * kFKBytes * (STATS ? 2 : 1);  // [kFBufs] value tiles (pass 2)
     static constexpr int kM = kV + (STATS ? 0 : kFBufs * kFKBytes);  // [2][128] row max (pass 2)
     static constexpr int kR = kM + 2 * 128 * 4;                 // [2][2][128] per-half row partials
     static constexpr int kL = kR + 2 * 2 * 128 * 4;             // [2][128] 1 / l per O buffer (pass 2)
@@ -211,6 +211,16 @@ __global__ void __launch_bounds__(kFThreads, 1)
     flash_prefill_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
                          const FlashParams p) {
     using L = FlashSmem<BF16, STATS>;
+    // Key tile of this pass: the max pass has no P.V, so its S tiles are 256
+    // keys wide (two 256-column TMEM buffers) -- a tcgen05.mma costs the same
+    // ~163 cycles for any N <= 256 (scripts/mma_probe.cu), so N = 256 halves
+    // the pass's tensor time; the P.V pass keeps 128-key tiles (its TMEM
+    // holds S / P and two O buffers).
+    constexpr int NK = STATS ? 2 * kFKeys : kFKeys;
+    constexpr int NKH = NK * 128;  // one 64-column SW128 box of a key tile
+    constexpr int NKB = 2 * NKH;
+    constexpr int HK = NK / 2;     // keys per row thread per tile
+    auto key_tiles = [](int qt) { return (qt * kFTile + kFTile + NK - 1) / NK; };
     extern __shared__ __align__(1024) uint8_t raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -277,7 +287,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
             for (int it = first; it < last; ++it, ++n) {
                 const int qt = p.nqt - 1 - it % p.nqt, z = it / p.nqt;
                 const int b = z / p.H, xq = (z % p.H) * 128;
-                const int T = qt + 1;
+                const int T = key_tiles(qt);
                 const int qb = n & 1;
                 if (n >= 2) mbar_wait(&q_empty[qb], ((n >> 1) - 1) & 1);
                 mbar_arrive_expect_tx(&q_full[qb], kFTileBytes + (STATS ? 0 : 512));
@@ -291,10 +301,10 @@ __global__ void __launch_bounds__(kFThreads, 1)
                     const int st = g & 1;
                     if (g >= 2) mbar_wait(&k_empty[st], ((g >> 1) - 1) & 1);
                     PFT("tma_k", g);
-                    uint8_t* dk = sK + st * kFKBytes;
-                    mbar_arrive_expect_tx(&k_full[st], kFKBytes);
-                    tma3d(dk, &map_kv, xq, j * kFKeys, b, &k_full[st]);
-                    tma3d(dk + kFKHalf, &map_kv, xq + 64, j * kFKeys, b, &k_full[st]);
+                    uint8_t* dk = sK + st * NKB;
+                    mbar_arrive_expect_tx(&k_full[st], NKB);
+                    tma3d(dk, &map_kv, xq, j * NK, b, &k_full[st]);
+                    tma3d(dk + NKH, &map_kv, xq + 64, j * NK, b, &k_full[st]);
                     if constexpr (!STATS) {
                         if (g >= 2) mbar_wait(&v_empty[st], ((g >> 1) - 1) & 1);
                         uint8_t* dv = sV + st * kFKBytes;
@@ -308,7 +318,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
     } else if (warp == 1) {
         // ---------------------------------------------------------------- MMA
         if (lane == 0) {
-            constexpr uint32_t id_s = flash_idesc<BF16, false, kFKeys>();
+            constexpr uint32_t id_s = flash_idesc<BF16, false, NK>();
             constexpr uint32_t id_o = flash_idesc<BF16, true, 128>();
             int g = 0, n = 0;
             auto issue_s = [&](int gg, const uint8_t* q) {
@@ -317,11 +327,11 @@ __global__ void __launch_bounds__(kFThreads, 1)
                 mbar_wait(&k_full[sb], (gg >> 1) & 1);
                 PFT("mma_s", gg);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint8_t* k = sK + sb * kFKBytes;
+                const uint8_t* k = sK + sb * NKB;
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                    umma(tmem + sb * kFKeys, desc_k(q + (kk >> 2) * kFHalf + (kk & 3) * 32),
-                         desc_k(k + (kk >> 2) * kFKHalf + (kk & 3) * 32), id_s, kk > 0);
+                    umma(tmem + sb * NK, desc_k(q + (kk >> 2) * kFHalf + (kk & 3) * 32),
+                         desc_k(k + (kk >> 2) * NKH + (kk & 3) * 32), id_s, kk > 0);
                 umma_commit(&k_empty[sb]);
                 umma_commit(&s_full[sb]);
             };
@@ -332,7 +342,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
             int itS = first, jS = 0, nS = 0, gS = 0;
             auto issue_next_s = [&]() {
                 if (itS >= last) return;
-                const int TS = p.nqt - itS % p.nqt;
+                const int TS = key_tiles(p.nqt - 1 - itS % p.nqt);
                 const int qb = nS & 1;
                 if (jS == 0) mbar_wait(&q_full[qb], (nS >> 1) & 1);
                 issue_s(gS++, sQ + qb * kFTileBytes);
@@ -345,7 +355,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
             };
             issue_next_s();
             for (int it = first; it < last; ++it, ++n) {
-                const int T = p.nqt - it % p.nqt;
+                const int T = key_tiles(p.nqt - 1 - it % p.nqt);
                 const int ob = n & 1;
                 for (int j = 0; j < T; ++j, ++g) {
                     issue_next_s();  // S_{g+1}
@@ -380,7 +390,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
         int g = 0, n = 0;
         for (int it = first; it < last; ++it, ++n) {
             const int qt = p.nqt - 1 - it % p.nqt, z = it / p.nqt;
-            const int T = qt + 1;
+            const int T = key_tiles(qt);
             const int r = qt * kFTile + rl;
             const int qb = n & 1;
             const bool valid = r < p.s;
@@ -398,31 +408,41 @@ __global__ void __launch_bounds__(kFThreads, 1)
             for (int j = 0; j < T; ++j, ++g) {
                 const int sb = g & 1;
                 // key tiles past the query tile's first row need the causal mask
-                const bool diag = (j + 1) * kFKeys - 1 > qt * kFTile;
-                const uint32_t ca = tl + sb * kFKeys + hf * kFHK;
+                const bool diag = (j + 1) * NK - 1 > qt * kFTile;
+                const uint32_t ca = tl + sb * NK + hf * HK;
                 mbar_wait(&s_full[sb], (g >> 1) & 1);
                 if (warp == 4 && lane == 0) PFT("row_s", g);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                float sv[kFHK];
-#pragma unroll
-                for (int c = 0; c < kFHK / 32; ++c) tmem_ld32(ca + c * 32, sv + c * 32);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (warp == 4 && lane == 0) PFT("row_ld", g);
-                const int lim = valid ? min(r - j * kFKeys - hf * kFHK, kFHK - 1) : -1;  // keys 0..lim of this half count
+                const int lim = valid ? min(r - j * NK - hf * HK, HK - 1) : -1;  // keys 0..lim of this half count
                 if constexpr (STATS) {
-                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                    mbar_arrive(&s_free[sb]);
+                    // 128 keys per thread: two 64-key rounds of loads (register budget)
                     float m4[4] = {mx, mx, mx, mx};
-                    if (diag) {
 #pragma unroll
-                        for (int k = 0; k < kFHK; ++k)
-                            if (k <= lim) m4[k & 3] = fmaxf(m4[k & 3], sv[k]);
-                    } else {
+                    for (int c0 = 0; c0 < HK; c0 += 64) {
+                        float sv[64];
+                        tmem_ld32(ca + c0, sv);
+                        tmem_ld32(ca + c0 + 32, sv + 32);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        if (c0 + 64 == HK) {
+                            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                            mbar_arrive(&s_free[sb]);
+                        }
+                        if (diag) {
 #pragma unroll
-                        for (int k = 0; k < kFHK; ++k) m4[k & 3] = fmaxf(m4[k & 3], sv[k]);
+                            for (int k = 0; k < 64; ++k)
+                                if (c0 + k <= lim) m4[k & 3] = fmaxf(m4[k & 3], sv[k]);
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < 64; ++k) m4[k & 3] = fmaxf(m4[k & 3], sv[k]);
+                        }
                     }
                     mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
                 } else {
+                    float sv[kFHK];
+#pragma unroll
+                    for (int c = 0; c < kFHK / 32; ++c) tmem_ld32(ca + c * 32, sv + c * 32);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (warp == 4 && lane == 0) PFT("row_ld", g);
                     float l4[4] = {0.f, 0.f, 0.f, 0.f};
                     unsigned c4[4] = {0u, 0u, 0u, 0u};
                     if (diag) {
@@ -668,9 +688,10 @@ cudaError_t launch_prefill(bool bf16, bool out_f32, const void* kv, const void* 
     unsigned* below = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(llast) + align256(static_cast<size_t>(Z) * 4));
     cudaError_t e = cudaMemsetAsync(below, 0, static_cast<size_t>(Z) * 4, st);
     if (e != cudaSuccess) return e;
-    CUtensorMap mq, mkv;
+    CUtensorMap mq, mkv, mk256;  // mk256: the max pass's 256-key tiles
     if (!map3d(&mq, q, bf16, HD, s, B, HD * 2, HD * 2 * s, kFTile) ||
-        !map3d(&mkv, kv, bf16, 2 * HD, s, B, 2 * HD * 2, 2 * HD * 2 * Ncap, kFKeys))
+        !map3d(&mkv, kv, bf16, 2 * HD, s, B, 2 * HD * 2, 2 * HD * 2 * Ncap, kFKeys) ||
+        !map3d(&mk256, kv, bf16, 2 * HD, s, B, 2 * HD * 2, 2 * HD * 2 * Ncap, 2 * kFKeys))
         return cudaErrorInvalidValue;
     FlashParams p{};
     p.s = s;
@@ -686,7 +707,7 @@ cudaError_t launch_prefill(bool bf16, bool out_f32, const void* kv, const void* 
     p.out_f32 = out_f32 ? 1 : 0;
     p.wlast = wlast;
     p.below = below;
-    e = bf16 ? run_flash<true, true>(mq, mkv, p, st) : run_flash<false, true>(mq, mkv, p, st);
+    e = bf16 ? run_flash<true, true>(mq, mk256, p, st) : run_flash<false, true>(mq, mk256, p, st);
     if (e != cudaSuccess) return e;
     e = bf16 ? run_flash<true, false>(mq, mkv, p, st) : run_flash<false, false>(mq, mkv, p, st);
     if (e != cudaSuccess) return e;
