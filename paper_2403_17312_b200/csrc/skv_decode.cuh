@@ -214,6 +214,9 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
     // Let the next kernel in the stream (the select kernel) get scheduled now;
     // it waits for this grid's completion before touching our outputs.
     pdl_launch_dependents();
+#ifdef SKV_DECODE_TRACE
+    if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) dtr[0] = gtimer();
+#endif
 
     const size_t TOKB = static_cast<size_t>(2) * H * ROWE;  // bytes per token (K and V planes)
     // this sequence's token rows; a token holds K then V, H heads each
@@ -416,6 +419,7 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
     // 16-byte vector at q (16-byte aligned for every storage type)
     auto ld16 = [](const uint8_t* q) -> uint4 { return *reinterpret_cast<const uint4*>(q); };
 
+    DTR(1);  // consumers: token list, append and q done
     // ---- pass 1: logits = (q . k) * scale  (attention.hpp:204-212)
     for (int u = 0; u < nchunks; ++u) {
         const int stage = u % S;
@@ -466,6 +470,7 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
     }
     named_sync(kBarConsumers, kConsumerThreads);
 
+    DTR(2);
     // ---- softmax with the reference's normaliser (attention.hpp:213-218)
     for (int hh = warp; hh < HG; hh += kConsumerWarps) {
         float* wl = wts + hh * m;
@@ -486,6 +491,7 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
     }
     named_sync(kBarConsumers, kConsumerThreads);
 
+    DTR(3);
     // ---- head-group partial of the importance update (+ optional outputs)
     {
         float* wp = p.wpart + (static_cast<size_t>(b) * G + g) * m;
@@ -502,6 +508,7 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
                 p.w_out[(static_cast<size_t>(b) * H + g * HG) * m + i] = wts[i];
     }
 
+    DTR(4);
     // ---- pass 2: attn = sum_t w_t * V[t]  (attention.hpp:219-225)
     float2 acc[V2];
 #pragma unroll
@@ -584,6 +591,7 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
             static_cast<QT*>(p.out)[at] = from_f<QT>(s);
     }
 
+    DTR(5);
     // ---- tail: the last CTA of the sequence folds the G partials (fixed
     // group order, deterministic) into the importance and selects the next
     // step's tokens, while the other sequences' CTAs keep streaming.
@@ -601,10 +609,20 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
             SelectParams sp = p.sel;
             sp.tok_prev = tok;  // this CTA's (shared) token list, same for every group
             sp.tok_prev_ld = 0;
+            DTR_TAIL(6);
             fold_and_select<kConsumerThreads, kBarConsumers>(
                 sp, b, ctid, *reinterpret_cast<TopkSmem<kConsumerThreads>*>(smem + L.topk),
                 reinterpret_cast<uint64_t*>(ring), *reinterpret_cast<SelectScratch<kConsumerThreads>*>(smem + L.scratch));
             if (ctid == 0) p.counters[b] = 0;
+#ifdef SKV_DECODE_TRACE
+            if (ctid == 0 && p.n % 50 == 0) {
+                const unsigned long long t = gtimer();
+                printf("DTR n=%d: cta0 start->q %llu, pass1 %llu, softmax %llu, wpart %llu, pass2+out %llu | "
+                       "tail wait %llu, fold %llu, keys %llu, topk %llu ns; total %llu\n", p.n, dtr[1] - dtr[0],
+                       dtr[2] - dtr[1], dtr[3] - dtr[2], dtr[4] - dtr[3], dtr[5] - dtr[4], dtr[6] - dtr[5],
+                       dtr[7] - dtr[6], dtr[8] - dtr[7], t - dtr[8], t - dtr[0]);
+            }
+#endif
         }
     }
 }

@@ -7,7 +7,29 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 
+#ifdef SKV_DECODE_TRACE
+#include <cstdio>
+#endif
+
 namespace skvd {
+
+// Debug build only (-DSKV_DECODE_TRACE): globaltimer stamps of CTA (0, 0)'s
+// phases and the tail's, printed every 50th n (latency anatomy of config 1).
+#ifdef SKV_DECODE_TRACE
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define DTR(slot) do { if (ctid == 0 && (blockIdx.x == 0 && blockIdx.y == 0)) dtr[slot] = gtimer(); } while (0)
+#define DTR_TAIL(slot) do { if (ctid == 0) dtr[slot] = gtimer(); } while (0)
+#define DTR_T(slot, id) do { if ((id) == 0) dtr[slot] = gtimer(); } while (0)
+__device__ unsigned long long dtr[16];
+#else
+#define DTR(slot) do { } while (0)
+#define DTR_TAIL(slot) do { } while (0)
+#define DTR_T(slot, id) do { } while (0)
+#endif
 
 // ---------------------------------------------------------------- smem / sync
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -222,6 +222,7 @@ __device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<N
     }
     if (!p.select) return;
     named_sync(BAR, NT);  // the fold and the staged candidates are complete
+    DTR_T(7, tid);
     int* o = p.idx + static_cast<size_t>(b) * p.idx_ld;
     if (p.variant == 2) {  // local_attention_mask (attention.hpp:247-256): the last m tokens
         for (int i = tid; i < p.m; i += NT) o[i] = p.n - p.m + i;
@@ -239,6 +240,7 @@ __device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<N
     SEL_TRACE(1);
     for (int i = tid; i < nc; i += NT) keys[i] = order_key(kd[i]);  // in place, same thread
     named_sync(BAR, NT);
+    DTR_T(8, tid);
     SEL_TRACE(2);
     block_topk<NT, BAR>(keys, nc, p.k, o, s, tid);                  // global picks, ascending
     SEL_TRACE(3);

@@ -56,11 +56,8 @@ if os.environ.get("TRACE") == "1":
         torch.cuda.synchronize()
     ev = sorted([e for e in prof.events() if e.device_type.name == "CUDA"], key=lambda e: e.time_range.start)
     t0 = ev[0].time_range.start
-    prev_end = t0
-    for e in ev:
+    sels = [i for i, e in enumerate(ev) if "select" in e.name]
+    print("TR kernels", len(ev), "selects at", sels)
+    for i, e in enumerate(ev):
         st, en = e.time_range.start - t0, e.time_range.end - t0
-        if "attend" not in e.name or e is ev[0] or e is ev[-1] or ev.index(e) % 12 == 0:
-            print(f"TR {e.name[:40]:40s} start {st:9.1f} end {en:9.1f} dur {en - st:7.1f} gap {e.time_range.start - prev_end:7.1f}")
-        prev_end = max(prev_end, e.time_range.end)
-    att = [e.time_range.end - e.time_range.start for e in ev if "attend" in e.name]
-    print(f"TR attends {len(att)} mean {sum(att) / len(att):.1f} us; span {ev[-1].time_range.end - t0:.1f} us")
+        print(f"TR {i:3d} {e.name[13:30]:17s} start {st:9.1f} end {en:9.1f} dur {en - st:7.1f}")
