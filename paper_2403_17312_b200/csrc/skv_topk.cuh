@@ -16,14 +16,6 @@ namespace skvd {
 __device__ long long g_sel_trace[16];
 #endif
 
-// SKV_TOPK_RANK (default 1): once the k-th element's radix bucket holds at
-// most kRankMax candidates, resolve it by ranking them against each other
-// (one step) instead of further 8-bit passes (three barriers each). The
-// bucket's (key, index) list reuses the histogram's 1 KB.
-#ifndef SKV_TOPK_RANK
-#define SKV_TOPK_RANK 1
-#endif
-
 template <int NT>
 struct TopkSmem {
     uint32_t hist[256];
@@ -33,13 +25,7 @@ struct TopkSmem {
     uint64_t mask;
     int remaining;
     int done;
-#if SKV_TOPK_RANK
-    uint64_t kstar;
-    int cnt, nlist, ngt;
-#endif
 };
-constexpr int kRankMax = 64;  // 64 x (8-byte key + 4-byte index) fit in TopkSmem::hist
-static_assert(kRankMax * 12 <= 256 * 4, "rank list aliases the histogram");
 
 // Inclusive warp scan of a u64.
 __device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t v, int lane) {
@@ -166,11 +152,6 @@ __device__ void block_topk(const uint64_t* keys, int nc, int k, int* out, TopkSm
                 s.mask = mask | (0xFFull << shift);
                 s.remaining = remaining - static_cast<int>(above);
                 s.done = (cnt == static_cast<uint32_t>(remaining) - above) ? 1 : 0;
-#if SKV_TOPK_RANK
-                s.cnt = static_cast<int>(cnt);
-                s.nlist = 0;
-                s.ngt = 0;
-#endif
             }
         }
         named_sync(BAR, NT);
@@ -178,45 +159,6 @@ __device__ void block_topk(const uint64_t* keys, int nc, int k, int* out, TopkSm
         mask = s.mask;
         remaining = s.remaining;
         if (s.done) break;
-#if SKV_TOPK_RANK
-        if (shift > 0 && s.cnt <= kRankMax) {
-            uint64_t* lkey = reinterpret_cast<uint64_t*>(s.hist);
-            int* lidx = reinterpret_cast<int*>(lkey + kRankMax);
-            // Gather the bucket, rank each member under (value desc, index
-            // asc), and make the remaining-th one the full-key threshold K*:
-            // the compaction then takes every key > K* and the first
-            // `remaining` keys == K* by index (exact ties), as before.
-            for (int i = tid; i < nc; i += NT) {
-                const uint64_t key = keys[i];
-                if ((key & mask) == prefix) {
-                    const int slot = atomicAdd(&s.nlist, 1);
-                    lkey[slot] = key;
-                    lidx[slot] = i;
-                }
-            }
-            named_sync(BAR, NT);
-            const int c = s.nlist;
-            uint64_t kt = 0;
-            if (tid < c) {
-                kt = lkey[tid];
-                const int it = lidx[tid];
-                int rank = 0;
-                for (int u = 0; u < c; ++u) {
-                    const uint64_t ku = lkey[u];
-                    rank += (ku > kt) || (ku == kt && lidx[u] < it);
-                }
-                if (rank == remaining - 1) s.kstar = kt;
-            }
-            named_sync(BAR, NT);
-            const uint64_t ks = s.kstar;
-            if (tid < c && kt > ks) atomicAdd(&s.ngt, 1);
-            named_sync(BAR, NT);
-            prefix = ks;
-            mask = ~0ull;
-            remaining -= s.ngt;
-            break;
-        }
-#endif
     }
 #ifdef SKV_SELECT_TRACE
     if (tid == 0 && blockIdx.x == 0) { g_sel_trace[8] = npass; g_sel_trace[9] = top; g_sel_trace[10] = clock64(); }
