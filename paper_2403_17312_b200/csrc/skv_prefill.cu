@@ -157,6 +157,16 @@ __device__ __forceinline__ float ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// The same, but issued unconditionally: in the causal (diagonal) tiles the
+// masked cells select 0 afterwards (FSEL). Left to the compiler, the mask
+// became a predicate over each cell's constant reload, FFMA and MUFU, a
+// serial chain that made a diagonal tile cost ~2.5 k cycles against ~1.3 k
+// for a full one (PF_TRACE).
+__device__ __forceinline__ float ex2_all(float x) {
+    float y;
+    asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
 // A operand from TMEM (P), B from shared memory (V)
 __device__ __forceinline__ void umma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -446,10 +456,13 @@ __global__ void __launch_bounds__(kFThreads, 1)
                     float l4[4] = {0.f, 0.f, 0.f, 0.f};
                     unsigned c4[4] = {0u, 0u, 0u, 0u};
                     if (diag) {
+                        const float c1 = p.c1;
 #pragma unroll
                         for (int k = 0; k < kFHK; ++k) {
-                            const float e = k <= lim ? ex2(fmaf(sv[k], p.c1, -mc)) : 0.f;
-                            c4[k & 3] += (k <= lim) & (e < 0.01f);
+                            const float ex = ex2_all(fmaf(sv[k], c1, -mc));
+                            const bool in = k <= lim;
+                            const float e = in ? ex : 0.f;
+                            c4[k & 3] += in & (e < 0.01f);
                             l4[k & 3] += e;
                             sv[k] = e;
                         }
@@ -577,6 +590,519 @@ __global__ void __launch_bounds__(kFThreads, 1)
     }
 }
 
+// ============================================================================
+// 2-CTA version (cta_group::2): a cluster of two CTAs on one TPC processes a
+// 256-query super-tile; the leader's single thread issues M = 256 MMAs whose
+// A / D halves live in each CTA (its 128 query rows) and whose B operand is
+// split by N (each CTA stages half of the key tile, or half of V's head
+// dims). scripts/mma2_probe.cu: an M = 256, N = 128 2-CTA MMA costs ~86
+// (SS) / ~94 (TS) cycles against ~163 for the 1-CTA M = 128 one -- four times
+// the work per SM-cycle at N = 128. Barrier protocol:
+//  - TMA: each CTA loads its Q tile and its B half into its own shared memory
+//    with .cta_group::2, completing bytes on the LEADER's full barrier (the
+//    leader posts expect_tx for both halves); each CTA recycles a stage on
+//    its own empty barrier, which the leader's commit multicasts to both.
+//  - rows / epilogue of both CTAs arrive (one lane per warp) on the leader's
+//    p_full / s_free / o_pair barriers through shared::cluster addresses; the
+//    leader's commits multicast s_full / o_full / q_empty to both CTAs.
+// Rows and epilogue run per CTA exactly as in the 1-CTA kernel, on the CTA's
+// own TMEM lanes.
+// K / V shared-memory stages. V runs six tiles deep: one TMA thread issues
+// K(g) then V(g), and V(g) waits for P.V(g - stages) -- with three stages
+// the P.V stream waited ~6 k cycles per tile for V (PF_TRACE: the V load
+// latency every three tiles), and K behind it.
+template <bool STATS>
+struct F2Stages {
+    static constexpr int K = STATS ? 4 : 3;
+    static constexpr int V = 6;
+};
+// Warps as the 1-CTA kernel: 0 TMA, 1 MMA, 4..11 rows (two per TMEM lane
+// quarter, each half of a tile's keys), 2, 3, 12, 13 the O epilogue. TMEM:
+// two S / P buffers, two O buffers.
+constexpr int kF2RowQ = 2;
+constexpr int kF2Threads = 448;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same offset in the leader CTA (rank 0)
+__device__ __forceinline__ uint32_t leader_addr(const void* p) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(p)));
+    return r;
+}
+// (default .release.cta semantics, as CUTLASS's ClusterBarrier::arrive: the
+// TMEM data it publishes is ordered by the tcgen05 fences, and a cluster-scope
+// release measured as the pass's top stall)
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// TMA 3D load into this CTA's shared memory, bytes completed on the leader's
+// barrier at the same offset (peer bit cleared, as CUTLASS's 2SM loads)
+__device__ __forceinline__ void tma3d_2sm(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+        : "memory");
+}
+__device__ __forceinline__ void umma2(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma2_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+// completion of the leader's MMAs so far -> the barrier at this offset in the CTAs of `mask`
+__device__ __forceinline__ void umma2_commit(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+// MN-major B of one CTA's half of V: a single 64-dim SW128 atom column, 8-key groups 1024 B apart
+__device__ __forceinline__ uint64_t desc_mn64(const void* p) {
+    const uint64_t a = smem_u32(p);
+    return ((a >> 4) & 0x3FFFull) | (uint64_t(kFKHalf >> 4) << 16) | ((1024ull >> 4) << 32) | (1ull << 46) |
+           (2ull << 61);
+}
+
+template <bool BF16, bool STATS>
+struct Flash2Smem {
+    static constexpr int NK = STATS ? 2 * kFKeys : kFKeys;  // keys per S tile
+    static constexpr int KHB = (NK / 2) * 128;  // one 64-column SW128 box of this CTA's key half
+    static constexpr int KB = 2 * KHB;          // this CTA's key half, both 64-column boxes
+    static constexpr int VB = kFKeys * 128;     // this CTA's 64 head dims of a 128-key V tile
+    static constexpr int kQ = 0;                                     // [2] query tiles
+    static constexpr int kK = kQ + 2 * kFTileBytes;                  // [K stages] key halves
+    static constexpr int kV = kK + F2Stages<STATS>::K * KB;          // [V stages] value halves (pass 2)
+    static constexpr int kM = kV + (STATS ? 0 : F2Stages<STATS>::V * VB);  // [2][128] row max (pass 2)
+    static constexpr int kR = kM + 2 * 128 * 4;                      // [2][kF2RowQ][128] per-quarter row partials
+    static constexpr int kL = kR + 2 * kF2RowQ * 128 * 4;            // [2][128] 1 / l per O buffer
+    static constexpr int kBar = kL + 2 * 128 * 4;
+    static constexpr int kNBar = 48;
+    static constexpr int kBytes = kBar + kNBar * 8 + 16 + 1024;
+    static_assert(kBytes <= 227 * 1024, "shared memory");
+};
+
+#ifdef PF_TRACE
+__device__ long long g_pft2[2][8][32];
+#define PFT2(slot, gg)                                                                     \
+    do {                                                                                   \
+        if (blockIdx.x < 2 && (gg) < 32) g_pft2[blockIdx.x][slot][gg] = clock64();           \
+    } while (0)
+#else
+#define PFT2(slot, gg) \
+    do {               \
+    } while (0)
+#endif
+template <bool BF16, bool STATS>
+__global__ void __launch_bounds__(kF2Threads, 1)
+    flash2_prefill_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                          const __grid_constant__ CUtensorMap map_v, const FlashParams p) {
+    using L = Flash2Smem<BF16, STATS>;
+    constexpr int NK = L::NK, KHB = L::KHB, KB = L::KB, VB = L::VB;
+    constexpr int HK = NK / kF2RowQ;  // keys per row thread per tile
+    extern __shared__ __align__(1024) uint8_t raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    uint8_t* sQ = sm + L::kQ;
+    uint8_t* sK = sm + L::kK;
+    uint8_t* sV = sm + L::kV;
+    float* sM = reinterpret_cast<float*>(sm + L::kM);
+    float* sR = reinterpret_cast<float*>(sm + L::kR);
+    float* sL = reinterpret_cast<float*>(sm + L::kL);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::kBar);
+    uint64_t* q_full = bar;         // [2] leader: both Q tiles landed
+    uint64_t* q_empty = bar + 2;    // [2] each: leader's commit (+ own rows read sM)
+    constexpr int KS = F2Stages<STATS>::K, VS = F2Stages<STATS>::V;
+    uint64_t* k_full = bar + 4;     // [4] leader: both key halves landed
+    uint64_t* k_empty = bar + 8;    // [4] each: leader's commit
+    uint64_t* v_full = bar + 12;    // [6] leader
+    uint64_t* v_empty = bar + 18;   // [6] each
+    uint64_t* s_full = bar + 24;    // [kSB] each: S in this CTA's TMEM
+    uint64_t* s_free = bar + 27;    // [kSB] leader: pass 1 rows of both read S (16 warps); pass 2 P.V consumed P
+    uint64_t* p_full = bar + 30;    // [kSB] leader: rows of both wrote P (16 warps)
+    uint64_t* o_full = bar + 33;    // [2] each: the item's O complete
+    uint64_t* o_pair = bar + 35;    // [2] leader: both epilogues read O (8 warps)
+    uint64_t* o_empty = bar + 37;   // [2] each: own epilogue read O and 1 / l (128)
+    uint64_t* l_full = bar + 39;    // [2] each: rows wrote 1 / l (128)
+    uint64_t* m_full = bar + 41;    // [2] each: own row max landed (pass 2)
+    constexpr int kSB = 2;  // S / P buffers
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + L::kNBar);
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 43; ++i) mbar_init(&bar[i], 1);
+        if (!STATS) {
+            mbar_init(&q_empty[0], 257);  // the leader's commit + this CTA's 256 row threads (sM read)
+            mbar_init(&q_empty[1], 257);
+        }
+        for (int i = 0; i < kSB; ++i) {
+            if (STATS) mbar_init(&s_free[i], 16);  // 8 row warps x 2 CTAs
+            mbar_init(&p_full[i], 16);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&o_pair[i], 8);  // 4 epilogue warps x 2 CTAs
+            mbar_init(&o_empty[i], 128);
+            mbar_init(&l_full[i], 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                     "n"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    cluster_sync_all();  // both CTAs' barriers initialised, TMEM allocated
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tslot;
+    // Work items: (sequence-head z, 256-query super-tile qs), heaviest first,
+    // contiguous runs per CTA pair; rank r owns query tile 2 qs + r.
+    const int nqs = (p.nqt + 1) / 2;
+    const int items = p.Z * nqs;
+    const int npairs = gridDim.x / 2, pair = blockIdx.x / 2;
+    const int first = static_cast<int>(static_cast<long long>(items) * pair / npairs);
+    const int last = static_cast<int>(static_cast<long long>(items) * (pair + 1) / npairs);
+    const int nkt = (p.s + NK - 1) / NK;
+    auto key_tiles = [&](int qs) { return min(nkt, (qs * 2 * kFTile + 2 * kFTile + NK - 1) / NK); };
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ TMA (both CTAs)
+        if (lane == 0) {
+            int g = 0, n = 0;
+            for (int it = first; it < last; ++it, ++n) {
+                const int qs = nqs - 1 - it % nqs, z = it / nqs;
+                const int qt = 2 * qs + static_cast<int>(rank);
+                const int b = z / p.H, xq = (z % p.H) * 128;
+                const int T = key_tiles(qs);
+                const int qb = n & 1;
+                if (n >= 2) mbar_wait(&q_empty[qb], ((n >> 1) - 1) & 1);
+                if (leader) mbar_arrive_expect_tx(&q_full[qb], 2 * kFTileBytes);
+                uint8_t* dq = sQ + qb * kFTileBytes;
+                tma3d_2sm(dq, &map_q, xq, qt * kFTile, b, &q_full[qb]);
+                tma3d_2sm(dq + kFHalf, &map_q, xq + 64, qt * kFTile, b, &q_full[qb]);
+                if constexpr (!STATS) {
+                    mbar_arrive_expect_tx(&m_full[qb], 512);
+                    bulk_g2s(sM + qb * 128, p.mrow + static_cast<size_t>(z) * p.s_pad + qt * kFTile, 512, &m_full[qb],
+                             policy_evict_first());
+                }
+                for (int j = 0; j < T; ++j, ++g) {
+                    const int st = g % KS;
+                    if (g >= KS) mbar_wait(&k_empty[st], ((g / KS) - 1) & 1);
+                    if (leader) mbar_arrive_expect_tx(&k_full[st], 2 * KB);
+                    PFT2(0, g);
+                    uint8_t* dk = sK + st * KB;
+                    const int key0 = j * NK + static_cast<int>(rank) * (NK / 2);
+                    tma3d_2sm(dk, &map_k, xq, key0, b, &k_full[st]);
+                    tma3d_2sm(dk + KHB, &map_k, xq + 64, key0, b, &k_full[st]);
+                    if constexpr (!STATS) {
+                        const int vt = g % VS;
+                        if (g >= VS) mbar_wait(&v_empty[vt], ((g / VS) - 1) & 1);
+                        if (leader) mbar_arrive_expect_tx(&v_full[vt], 2 * VB);
+                        PFT2(3, g);
+                        tma3d_2sm(sV + vt * VB, &map_v, p.HD + xq + static_cast<int>(rank) * 64, j * kFKeys, b,
+                                  &v_full[vt]);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------- MMA (the leader's one thread)
+        if (leader && lane == 0) {
+            constexpr uint32_t id_s = (1u << 4) | ((BF16 ? 1u : 0u) << 7) | ((BF16 ? 1u : 0u) << 10) |
+                                      (uint32_t(NK >> 3) << 17) | (uint32_t(256 >> 4) << 24);
+            constexpr uint32_t id_o = (1u << 4) | ((BF16 ? 1u : 0u) << 7) | ((BF16 ? 1u : 0u) << 10) | (1u << 16) |
+                                      (uint32_t(128 >> 3) << 17) | (uint32_t(256 >> 4) << 24);
+            int g = 0, n = 0;
+            auto issue_s = [&](int gg, const uint8_t* q) {
+                const int sb = gg % kSB, ks = gg % KS;
+                if (gg >= kSB) mbar_wait(&s_free[sb], ((gg / kSB) - 1) & 1);
+                mbar_wait(&k_full[ks], (gg / KS) & 1);
+                PFT2(1, gg);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint8_t* k = sK + ks * KB;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    umma2(tmem + sb * NK, desc_k(q + (kk >> 2) * kFHalf + (kk & 3) * 32),
+                          desc_k(k + (kk >> 2) * KHB + (kk & 3) * 32), id_s, kk > 0);
+                umma2_commit(&k_empty[ks], 3);
+                umma2_commit(&s_full[sb], 3);
+            };
+            int itS = first, jS = 0, nS = 0, gS = 0;
+            auto issue_next_s = [&]() {
+                if (itS >= last) return;
+                const int TS = key_tiles(nqs - 1 - itS % nqs);
+                const int qb = nS & 1;
+                if (jS == 0) mbar_wait(&q_full[qb], (nS >> 1) & 1);
+                issue_s(gS++, sQ + qb * kFTileBytes);
+                if (++jS == TS) {
+                    umma2_commit(&q_empty[qb], 3);  // the item's last S: both Q tiles are free
+                    jS = 0;
+                    ++itS;
+                    ++nS;
+                }
+            };
+            issue_next_s();
+            for (int it = first; it < last; ++it, ++n) {
+                const int T = key_tiles(nqs - 1 - it % nqs);
+                const int ob = n & 1;
+                for (int j = 0; j < T; ++j, ++g) {
+                    issue_next_s();  // S_{g+1}
+                    if constexpr (!STATS) {
+                        const int sb = g % kSB, vs = g % VS;
+                        mbar_wait(&v_full[vs], (g / VS) & 1);
+                        mbar_wait(&p_full[sb], (g / kSB) & 1);
+                        if (j == 0 && n >= 2) mbar_wait(&o_pair[ob], ((n >> 1) - 1) & 1);  // both drained this O buffer
+                        PFT2(6, g);
+                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                        const uint8_t* v = sV + vs * VB;
+                        const uint32_t od = tmem + 256 + ob * 128;
+#pragma unroll
+                        for (int kk = 0; kk < kFKeys / 16; ++kk) {
+                            const uint32_t pa = tmem + sb * kFKeys + (kk >> 1) * 32 + (kk & 1) * 8;
+                            umma2_ts(od, pa, desc_mn64(v + kk * 2048), id_o, (j | kk) != 0);
+                            if constexpr (BF16) umma2_ts(od, pa + 16, desc_mn64(v + kk * 2048), id_o, 1);
+                        }
+                        umma2_commit(&v_empty[vs], 3);
+                        umma2_commit(&s_free[sb], 1);
+                        if (j + 1 == T) umma2_commit(&o_full[ob], 3);
+                    }
+                }
+            }
+        }
+    } else if (warp >= 4 && warp < 4 + 4 * kF2RowQ) {
+        // ------------------------------------------ rows: softmax / P (this CTA's 128 rows)
+        const int q4 = warp & 3;
+        const int hf = (warp - 4) >> 2;  // key quarter
+        const int rl = q4 * 32 + lane;
+        const uint32_t tl = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
+        const uint32_t s_free_l = leader_addr(&s_free[0]), p_full_l = leader_addr(&p_full[0]);
+        int g = 0, n = 0;
+        for (int it = first; it < last; ++it, ++n) {
+            const int qs = nqs - 1 - it % nqs, z = it / nqs;
+            const int qt = 2 * qs + static_cast<int>(rank);
+            const int T = key_tiles(qs);
+            const int r = qt * kFTile + rl;
+            const int qb = n & 1;
+            const bool valid = r < p.s;
+            const size_t zrow = static_cast<size_t>(z) * p.s;
+            float mx = -INFINITY;
+            float mc = 0.f;
+            float l = 0.f;
+            if constexpr (!STATS) {
+                mbar_wait(&m_full[qb], (n >> 1) & 1);
+                mc = valid ? sM[qb * 128 + rl] * p.c1 : 0.f;
+                mbar_arrive(&q_empty[qb]);
+            }
+            unsigned cnt = 0;
+            const bool last_row = r == p.s - 1;
+            for (int j = 0; j < T; ++j, ++g) {
+                const int sb = g % kSB;
+                const bool diag = (j + 1) * NK - 1 > qt * kFTile;
+                const uint32_t ca = tl + sb * NK + hf * HK;
+                mbar_wait(&s_full[sb], (g / kSB) & 1);
+                if (warp == 4 && lane == 0) PFT2(2, g);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const int lim = valid ? min(r - j * NK - hf * HK, HK - 1) : -1;
+                if constexpr (STATS) {
+                    float m4[4] = {mx, mx, mx, mx};
+#pragma unroll
+                    for (int c0 = 0; c0 < HK; c0 += 32) {
+                        float sv[32];
+                        tmem_ld32(ca + c0, sv);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        if (c0 + 32 == HK) {
+                            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_cluster(s_free_l + sb * 8);
+                        }
+                        if (diag) {
+#pragma unroll
+                            for (int k = 0; k < 32; ++k)
+                                if (c0 + k <= lim) m4[k & 3] = fmaxf(m4[k & 3], sv[k]);
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < 32; ++k) m4[k & 3] = fmaxf(m4[k & 3], sv[k]);
+                        }
+                    }
+                    mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+                } else {
+                    // 32-key chunks (register budget of 576 threads); packed pairs: FFMA2 for
+                    // S * c1 - max, FADD2 for l
+                    float2 l2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+                    unsigned c4[4] = {0u, 0u, 0u, 0u};
+                    const float2 c1v = make_float2(p.c1, p.c1), nmc = make_float2(-mc, -mc);
+#pragma unroll
+                    for (int c0 = 0; c0 < HK; c0 += 32) {
+                        float sv[32];
+                        tmem_ld32(ca + c0, sv);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        if (diag) {
+#pragma unroll
+                            for (int k = 0; k < 32; k += 2) {
+                                const float2 x = __ffma2_rn(make_float2(sv[k], sv[k + 1]), c1v, nmc);
+                                const bool in0 = c0 + k <= lim, in1 = c0 + k + 1 <= lim;
+                                const float x0 = ex2_all(x.x), x1 = ex2_all(x.y);
+                                const float e0 = in0 ? x0 : 0.f, e1 = in1 ? x1 : 0.f;
+                                c4[k & 3] += in0 & (e0 < 0.01f);
+                                c4[(k + 1) & 3] += in1 & (e1 < 0.01f);
+                                l2[(k >> 1) & 1] = __fadd2_rn(l2[(k >> 1) & 1], make_float2(e0, e1));
+                                sv[k] = e0;
+                                sv[k + 1] = e1;
+                            }
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < 32; k += 2) {
+                                const float2 x = __ffma2_rn(make_float2(sv[k], sv[k + 1]), c1v, nmc);
+                                const float e0 = ex2(x.x), e1 = ex2(x.y);
+                                c4[k & 3] += e0 < 0.01f;
+                                c4[(k + 1) & 3] += e1 < 0.01f;
+                                l2[(k >> 1) & 1] = __fadd2_rn(l2[(k >> 1) & 1], make_float2(e0, e1));
+                                sv[k] = e0;
+                                sv[k + 1] = e1;
+                            }
+                        }
+                        if (last_row) {
+                            float* wl = p.wlast + zrow + j * kFKeys + hf * HK + c0;
+#pragma unroll
+                            for (int k = 0; k < 32; ++k)
+                                if (c0 + k <= lim) wl[k] = sv[k];
+                        }
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) pk[i] = pack2<BF16>(sv[2 * i], sv[2 * i + 1]);
+                        tmem_st16(ca + c0, pk);
+                        if constexpr (BF16) {
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) pk[i] = pack2<true>(bf16_rest(sv[2 * i]), bf16_rest(sv[2 * i + 1]));
+                            tmem_st16(ca + c0 + 16, pk);
+                        }
+                    }
+                    l += (l2[0].x + l2[0].y) + (l2[1].x + l2[1].y);
+                    const unsigned ct = (c4[0] + c4[1]) + (c4[2] + c4[3]);
+                    cnt += valid ? ct : 0u;
+                    if (warp == 4 && lane == 0) PFT2(4, g);
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(p_full_l + sb * 8);
+                    if (warp == 4 && lane == 0) PFT2(5, g);
+                }
+            }
+            // combine the key quarters of each row (fixed order)
+            float* red = sR + (n & 1) * (kF2RowQ * 128);
+            red[hf * 128 + rl] = STATS ? mx : l;
+            named_sync(1, kF2RowQ * 128);
+            if constexpr (STATS) {
+                if (hf == 0 && valid) {
+                    float m = red[rl];
+#pragma unroll
+                    for (int q = 1; q < kF2RowQ; ++q) m = fmaxf(m, red[q * 128 + rl]);
+                    p.mrow[static_cast<size_t>(z) * p.s_pad + r] = m;
+                }
+            } else {
+                l = red[rl];
+#pragma unroll
+                for (int q = 1; q < kF2RowQ; ++q) l += red[q * 128 + rl];
+                if (hf == 0) {
+                    if (last_row) p.llast[z] = l;
+                    const int ob = n & 1;
+                    if (n >= 2) mbar_wait(&o_empty[ob], ((n >> 1) - 1) & 1);  // sL[ob] of item n - 2 read
+                    sL[ob * 128 + rl] = 1.0f / l;
+                    mbar_arrive(&l_full[ob]);
+                }
+#pragma unroll
+                for (int o2 = 16; o2 > 0; o2 >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o2);
+                if (lane == 0 && cnt) atomicAdd(&p.below[z], cnt);
+            }
+        }
+    } else if (!STATS && (warp >= 4 + 4 * kF2RowQ || warp == 2 || warp == 3)) {
+        // ------------------------------------------- O epilogue (this CTA's 128 rows)
+        const int q4 = warp & 3;
+        const int rl = q4 * 32 + lane;
+        const uint32_t tl = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
+        const uint32_t o_pair_l = leader_addr(&o_pair[0]);
+        int n = 0;
+        for (int it = first; it < last; ++it, ++n) {
+            const int qs = nqs - 1 - it % nqs, z = it / nqs;
+            const int qt = 2 * qs + static_cast<int>(rank);
+            const int r = qt * kFTile + rl;
+            const bool valid = r < p.s;
+            const int ob = n & 1;
+            mbar_wait(&l_full[ob], (n >> 1) & 1);
+            const float inv_l = sL[ob * 128 + rl];
+            mbar_wait(&o_full[ob], (n >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const size_t row0 =
+                (static_cast<size_t>(z / p.H) * p.s + r) * p.HD + static_cast<size_t>(z % p.H) * 128;
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                float o[32];
+                tmem_ld32(tl + 256 + ob * 128 + c * 32, o);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (!valid) continue;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) o[i] *= inv_l;
+                if (p.out_f32) {
+                    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + row0 + c * 32);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) dst[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+                } else {
+                    uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(p.out) + row0 + c * 32);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        uint4 v;
+                        v.x = pack2<BF16>(o[8 * i + 0], o[8 * i + 1]);
+                        v.y = pack2<BF16>(o[8 * i + 2], o[8 * i + 3]);
+                        v.z = pack2<BF16>(o[8 * i + 4], o[8 * i + 5]);
+                        v.w = pack2<BF16>(o[8 * i + 6], o[8 * i + 7]);
+                        dst[i] = v;
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            mbar_arrive(&o_empty[ob]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(o_pair_l + ob * 8);
+            if (warp == 2 && lane == 0) PFT2(7, n);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+#ifdef PF_TRACE
+    cluster_sync_all();
+    if (blockIdx.x == 0 && threadIdx.x == 0 && !STATS) {
+        const char* names[8] = {"tma_k", "mma_s", "row_s", "tma_v", "row_math", "row_p", "mma_pv", "epi_rel(n)"};
+        const long long t0 = g_pft2[0][0][0];
+        for (int rk = 0; rk < 2; ++rk)
+            for (int gg = 0; gg < 24; ++gg) {
+                printf("Q2 r%d g=%2d", rk, gg);
+                for (int t = 0; t < 8; ++t) printf(" %s=%7lld", names[t], g_pft2[rk][t][gg] - t0);
+                printf("\n");
+            }
+    }
+#endif
+    cluster_sync_all();  // the peer's last MMAs and arrives are done before the TMEM goes
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+    }
+}
+
 // importance[b][j] = sum_h e_h[j] / l_h (head order, fp64): engine.hpp:
 // 508-512 seeds each head's accumulator with the last attention row,
 // attention.hpp:77-85 sums them. Block x = 0 also folds the per-head
@@ -661,6 +1187,40 @@ cudaError_t run_flash(const CUtensorMap& mq, const CUtensorMap& mkv, const Flash
     return e;
 }
 
+// The 2-CTA kernel: clusters of two CTAs (one TPC), one pair per two SMs.
+template <bool BF16, bool STATS>
+cudaError_t run_flash2(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const FlashParams& p,
+                       cudaStream_t st) {
+    constexpr int smem = Flash2Smem<BF16, STATS>::kBytes;
+    const void* fn = reinterpret_cast<const void*>(&flash2_prefill_kernel<BF16, STATS>);
+    static std::once_flag once;
+    static cudaError_t attr = cudaSuccess;
+    std::call_once(once, [&] { attr = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
+    if (attr != cudaSuccess) return attr;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int items = p.Z * ((p.nqt + 1) / 2);
+    const int pairs = std::max(1, std::min(sms / 2, items));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(kF2Threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    void* args[] = {const_cast<CUtensorMap*>(&mq), const_cast<CUtensorMap*>(&mk), const_cast<CUtensorMap*>(&mv),
+                    const_cast<FlashParams*>(&p)};
+    const cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
+    count_launch();
+    return e;
+}
+
 size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 
@@ -707,10 +1267,30 @@ cudaError_t launch_prefill(bool bf16, bool out_f32, const void* kv, const void* 
     p.out_f32 = out_f32 ? 1 : 0;
     p.wlast = wlast;
     p.below = below;
-    e = bf16 ? run_flash<true, true>(mq, mk256, p, st) : run_flash<false, true>(mq, mk256, p, st);
-    if (e != cudaSuccess) return e;
-    e = bf16 ? run_flash<true, false>(mq, mkv, p, st) : run_flash<false, false>(mq, mkv, p, st);
-    if (e != cudaSuccess) return e;
+    // CTA pairs from s = 1536 on: measured faster at s = 2048 (1.96 vs 2.17 ms, config 5's prompt), slower
+    // at s = 512 / 1024 (0.43 vs 0.39 ms, 3.63 vs 3.48 ms): with the MMAs four times cheaper, both kernels
+    // are bound by the row softmax, and the pair's lock-step costs more on short items.
+    // SKV_PREFILL_1CTA=1 / SKV_PREFILL_2CTA=1 force one kernel (A/B, tests).
+    static const bool force1 = std::getenv("SKV_PREFILL_1CTA") != nullptr;
+    static const bool force2 = std::getenv("SKV_PREFILL_2CTA") != nullptr;
+    const bool one_cta = force1 || (!force2 && s < 1536);
+    if (one_cta) {
+        e = bf16 ? run_flash<true, true>(mq, mk256, p, st) : run_flash<false, true>(mq, mk256, p, st);
+        if (e != cudaSuccess) return e;
+        e = bf16 ? run_flash<true, false>(mq, mkv, p, st) : run_flash<false, false>(mq, mkv, p, st);
+        if (e != cudaSuccess) return e;
+    } else {
+        // each CTA of a pair stages half a key tile: 128 keys of the max pass's 256, 64 of the P.V
+        // pass's 128; and 64 of V's 128 head dims
+        CUtensorMap mk64, mv64;
+        if (!map3d(&mk64, kv, bf16, 2 * HD, s, B, 2 * HD * 2, 2 * HD * 2 * Ncap, kFKeys / 2) ||
+            !map3d(&mv64, kv, bf16, 2 * HD, s, B, 2 * HD * 2, 2 * HD * 2 * Ncap, kFKeys))
+            return cudaErrorInvalidValue;
+        e = bf16 ? run_flash2<true, true>(mq, mkv, mkv, p, st) : run_flash2<false, true>(mq, mkv, mkv, p, st);
+        if (e != cudaSuccess) return e;
+        e = bf16 ? run_flash2<true, false>(mq, mk64, mv64, p, st) : run_flash2<false, false>(mq, mk64, mv64, p, st);
+        if (e != cudaSuccess) return e;
+    }
     prefill_seed_kernel<<<dim3((s + 127) / 128, B), 128, static_cast<size_t>(H) * 8, st>>>(
         wlast, llast, below, imp, psp, H, s, imp_ld, h_div > 0 ? h_div : H);
     count_launch();

@@ -161,3 +161,22 @@ def test_prefill_int8(api, port):
             sp_ref += port.attention_sparsity(aw, 0.01, True)
         np.testing.assert_allclose(imp[b], seed_row, rtol=1e-4, atol=1e-7)
         assert abs(sp[b] - sp_ref / H) <= 2e-3, (b, sp[b], sp_ref / H)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kernel", ["SKV_PREFILL_2CTA", "SKV_PREFILL_1CTA"])
+def test_prefill_both_kernels(kernel):
+    """The 1-CTA and the CTA-pair (cta_group::2) prefill kernels are chosen by
+    prompt length (skv_prefill.cu); each one, forced for every shape of this
+    file, matches the oracle. The switch is read once per process, hence the
+    subprocess."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, **{kernel: "1"})
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_prefill.py"), "-k", "not both_kernels"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
