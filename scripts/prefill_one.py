@@ -1,4 +1,5 @@
-"""One config-2-shaped prefill layer (B=64, H=32, s=512, fp16) for ncu captures."""
+"""One prefill layer for ncu captures: config-2 shape (B=64, H=32, s=512, fp16, the 1-CTA kernel) or, with
+--c5, config 5's prompt (B=32, H=32, s=2048, fp16, the CTA-pair kernel)."""
 import os
 import sys
 
@@ -7,7 +8,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2403_17312_b200 import api  # noqa: E402
 
-B, H, s, D = 64, 32, 512, 128
+B, H, s, D = (32, 32, 2048, 128) if "--c5" in sys.argv else (64, 32, 512, 128)
 dt = torch.bfloat16 if "--bf16" in sys.argv else torch.float16
 k = torch.randn(B, s, H, D, device="cuda").to(dt)
 v = torch.randn_like(k)

@@ -17,3 +17,5 @@ timeout -s KILL 900 $NCU --set full -k regex:swa_select -s 1 -c 1 -o gpurun_out/
   python bench.py --config 2 --profile-only --steps 2 --warmup 3 > /dev/null 2>&1; echo "select c2 rc=$?"
 timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:flash_prefill -s 2 -c 2 \
   -o gpurun_out/${TAG}_prefill python scripts/prefill_one.py > gpurun_out/${TAG}_prefill.log 2>&1; echo "prefill rc=$?"
+timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:flash2_prefill -s 2 -c 2 \
+  -o gpurun_out/${TAG}_prefill2 python scripts/prefill_one.py --c5 > gpurun_out/${TAG}_prefill2.log 2>&1; echo "prefill2 rc=$?"

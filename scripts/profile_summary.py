@@ -22,6 +22,29 @@ import bench  # noqa: E402
 EXTRA = ["sm__pipe_tensor_op_tcgen05_cycles_active.avg.pct_of_peak_sustained_active"]
 
 
+def full_all(rep):
+    """Every launch of a capture: [(metrics, kernel name)]."""
+    import csv
+    import io
+    import subprocess
+
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    if len(rows) < 3:
+        return []
+    hdr, units = rows[0], rows[1]
+    out = []
+    for vals in rows[2:]:
+        res, name = {}, ""
+        for i, h in enumerate(hdr):
+            if h == "Kernel Name":
+                name = vals[i]
+            if h in KEYS + EXTRA:
+                res[h] = f"{vals[i]} {units[i]}".strip()
+        out.append((res, name))
+    return out
+
+
 def num(v):
     try:
         return float(str(v).split()[0].replace(",", ""))
@@ -84,17 +107,20 @@ def main():
                "(grid = sequences x layers)", "", "| metric | value |", "|---|---|"]
         md += [f"| {k} | {res[k]} |" for k in KEYS if k in res]
         md.append("")
-    rep = g("prefill.ncu-rep")
-    if os.path.exists(rep):
-        res, name = full(rep)
-        dur_us = num(res.get("gpu__time_duration.sum"))
-        B, H, s, D = 64, 32, 512, 128
+    for fname, (B, H, s, D), shape in (("prefill.ncu-rep", (64, 32, 512, 128), "config-2 shape B=64 H=32 s=512 fp16"),
+                                       ("prefill2.ncu-rep", (32, 32, 2048, 128),
+                                        "config-5 prompt B=32 H=32 s=2048 fp16 (CTA pairs)")):
+        rep = g(fname)
+        if not os.path.exists(rep):
+            continue
         fl = 4.0 * B * H * (s * (s + 1) / 2) * D
-        md += [f"## Prefill (`{name.split('(')[0]}`), config-2 shape B=64 H=32 s=512 fp16, one pass", "",
-               f"Causal GEMM flops of the layer {fl / 1e9:.1f} GFLOP (both passes together); this launch "
-               f"{dur_us} us.", "", "| metric | value |", "|---|---|"]
-        md += [f"| {k} | {res[k]} |" for k in KEYS if k in res]
-        md.append("")
+        for res, name in full_all(rep):
+            dur_us = num(res.get("gpu__time_duration.sum"))
+            md += [f"## Prefill (`{name.split('(')[0]}`), {shape}", "",
+                   f"Causal GEMM flops of the layer {fl / 1e9:.1f} GFLOP (the two passes together); this launch "
+                   f"{dur_us} us.", "", "| metric | value |", "|---|---|"]
+            md += [f"| {k} | {res[k]} |" for k in KEYS + EXTRA if k in res]
+            md.append("")
     open(os.path.join(ROOT, "profiles", f"{tag}.md"), "w").write("\n".join(md))
     if traffic:
         json.dump(traffic, open(os.path.join(ROOT, "profiles", "traffic.json"), "w"), indent=1)
