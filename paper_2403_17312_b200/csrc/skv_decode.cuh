@@ -618,9 +618,11 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
             if (ctid == 0 && p.n % 50 == 0) {
                 const unsigned long long t = gtimer();
                 printf("DTR n=%d: cta0 start->q %llu, pass1 %llu, softmax %llu, wpart %llu, pass2+out %llu | "
-                       "tail wait %llu, fold %llu, keys %llu, topk %llu ns; total %llu\n", p.n, dtr[1] - dtr[0],
+                       "tail wait %llu, fold %llu (loads %llu, adds %llu, sparsity %llu), keys %llu, topk %llu ns; "
+                       "total %llu\n", p.n, dtr[1] - dtr[0],
                        dtr[2] - dtr[1], dtr[3] - dtr[2], dtr[4] - dtr[3], dtr[5] - dtr[4], dtr[6] - dtr[5],
-                       dtr[7] - dtr[6], dtr[8] - dtr[7], t - dtr[8], t - dtr[0]);
+                       dtr[7] - dtr[6], dtr[9] - dtr[6], dtr[10] - dtr[9], dtr[7] - dtr[10], dtr[8] - dtr[7],
+                       t - dtr[8], t - dtr[0]);
             }
 #endif
         }

@@ -142,6 +142,7 @@ __device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<N
             }
             stage_candidates<NT>(kd, imp, nc, tid);
             named_sync(BAR, NT);  // staged candidates complete; every old value read
+            DTR_T(9, tid);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 if (t[r] < 0) continue;
@@ -179,6 +180,7 @@ __device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<N
             named_sync(BAR, NT);  // the folded importance is visible to the staging
             stage_candidates<NT>(kd, imp, nc, tid);
         }
+        DTR_T(10, tid);
         if (p.sp_n > 0) {
             // attention_sparsity (attention.hpp:275-310) of the head-summed step
             // row new_aw_row (length sp_n, zeros off-selection), threshold 0.01
