@@ -9,6 +9,10 @@
 // PCIe traffic is inside the timed loop. The same steps also run through the
 // device-buffer decode_step on a twin cache and the two must agree bit for
 // bit -- outputs and importance -- which checks the host pipeline from C++.
+// A third cache runs the steps the way a CPU-side Engine::decode_step would
+// feed a GPU attention layer by layer: per layer, synchronous uploads of its
+// q / k / v, decode_layer, a synchronous download of its output before the
+// next layer (e2e_layer_sync_tokens_per_s; must agree bit for bit too).
 // Prints one JSON line; exit 0 = agreement.
 #include <chrono>
 #include <cmath>
@@ -67,6 +71,7 @@ int main(int argc, char** argv) {
     try {
         skv::b200::DeviceCache host_path(L, B, H, D, s + steps + 1, SKV_F16, SKV_F16);
         skv::b200::DeviceCache dev_path(L, B, H, D, s + steps + 1, SKV_F16, SKV_F16);
+        skv::b200::DeviceCache layer_path(L, B, H, D, s + steps + 1, SKV_F16, SKV_F16);
         std::mt19937_64 rng(2403'17312);
         {  // prompt: s tokens per layer, then the importance seed (engine.hpp:508-512)
             const std::size_t prompt = static_cast<std::size_t>(B) * s * H * D;
@@ -79,7 +84,7 @@ int main(int argc, char** argv) {
                 dk.upload(k.p, prompt * 2);
                 dv.upload(v.p, prompt * 2);
                 dq.upload(q.p, row * 2);
-                for (auto* c : {&host_path, &dev_path}) {
+                for (auto* c : {&host_path, &dev_path, &layer_path}) {
                     c->append_tokens(l, 0, B, 0, s, dk.get(), dv.get());
                     c->prefill_seed(l, s, dq.get(), dout.get());
                 }
@@ -101,6 +106,28 @@ int main(int argc, char** argv) {
                                        out_host.as<std::uint8_t>() + step_bytes * j);
         skv::b200::check(skv_stream_synchronize(nullptr));
         const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        // layer by layer, synchronous (a host-side model consuming each layer's output)
+        std::vector<std::uint8_t> layer_out(step_bytes * steps);
+        double sec_layer = 0.0;
+        {
+            const std::size_t lb = row * 2;
+            skv::b200::DeviceBuffer lq(lb), lk(lb), lv(lb), lo(lb);
+            const auto t1 = std::chrono::steady_clock::now();
+            for (int j = 0; j < steps; ++j)
+                for (int l = 0; l < L; ++l) {
+                    lq.upload(qkv[3 * j]->as<std::uint8_t>() + lb * l, lb);
+                    lk.upload(qkv[3 * j + 1]->as<std::uint8_t>() + lb * l, lb);
+                    lv.upload(qkv[3 * j + 2]->as<std::uint8_t>() + lb * l, lb);
+                    layer_path.decode_layer(l, s + j + 1, r, lq.get(), lk.get(), lv.get(), lo.get());
+                    lo.download(layer_out.data() + step_bytes * j + lb * l, lb);
+                }
+            sec_layer = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+        }
+        int mismatched_layer_steps = 0;
+        for (int j = 0; j < steps; ++j)
+            if (std::memcmp(layer_out.data() + step_bytes * j, out_host.as<std::uint8_t>() + step_bytes * j,
+                            step_bytes) != 0)
+                ++mismatched_layer_steps;
         // device-buffer path on the twin cache: must agree bit for bit
         skv::b200::DeviceBuffer dq(step_bytes), dk(step_bytes), dv(step_bytes), dout(step_bytes);
         std::vector<std::uint8_t> got(step_bytes);
@@ -126,9 +153,11 @@ int main(int argc, char** argv) {
         for (Pinned* p : qkv) delete p;
         std::printf(
             "{\"program\": \"decode_loop\", \"layers\": %d, \"batch\": %d, \"heads\": %d, \"prompt\": %d, "
-            "\"steps\": %d, \"e2e_tokens_per_s\": %.1f, \"mismatched_steps\": %d, \"mismatched_layers\": %d}\n",
-            L, B, H, s, steps, static_cast<double>(B) * steps / sec, mismatched_steps, mismatched_layers);
-        return (mismatched_steps == 0 && mismatched_layers == 0) ? 0 : 1;
+            "\"steps\": %d, \"e2e_tokens_per_s\": %.1f, \"e2e_layer_sync_tokens_per_s\": %.1f, "
+            "\"mismatched_steps\": %d, \"mismatched_layers\": %d, \"mismatched_layer_sync_steps\": %d}\n",
+            L, B, H, s, steps, static_cast<double>(B) * steps / sec, static_cast<double>(B) * steps / sec_layer,
+            mismatched_steps, mismatched_layers, mismatched_layer_steps);
+        return (mismatched_steps == 0 && mismatched_layers == 0 && mismatched_layer_steps == 0) ? 0 : 1;
     } catch (const std::exception& e) {
         std::printf("{\"program\": \"decode_loop\", \"error\": \"%s\"}\n", e.what());
         return 2;

@@ -27,7 +27,8 @@ def test_cpp_host_decode_loop():
     """A C++ host (tests/cpp/decode_loop.cpp) runs the device-resident decode
     through include/skv/b200.hpp with pinned host buffers -- no Python on the
     path -- and its host-buffer steps agree bit for bit with the device-buffer
-    steps of a twin cache (outputs and importance)."""
+    steps of a twin cache (outputs and importance), as do the steps of a
+    layer-by-layer synchronous caller on a third cache."""
     import json
 
     exe = os.path.join(HERE, "cpp", "build", "decode_loop")
@@ -40,7 +41,8 @@ def test_cpp_host_decode_loop():
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert r.returncode == 0, r.stdout + r.stderr
     assert line["mismatched_steps"] == 0 and line["mismatched_layers"] == 0, line
-    assert line["e2e_tokens_per_s"] > 0
+    assert line["mismatched_layer_sync_steps"] == 0, line  # layer-by-layer synchronous caller, bit for bit
+    assert line["e2e_tokens_per_s"] > 0 and line["e2e_layer_sync_tokens_per_s"] > 0
 
 
 @pytest.mark.gpu
