@@ -951,7 +951,12 @@ __global__ void __launch_bounds__(kF2Threads, 1)
                         float sv[32];
                         tmem_ld32(ca + c0, sv);
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                        if (diag) {
+                        if (diag && __all_sync(0xffffffffu, lim < c0)) {
+                            // keys past every row of the warp (the causal triangle, or the pair's
+                            // last tile for rank 0's rows): P = 0, no exps
+#pragma unroll
+                            for (int k = 0; k < 32; ++k) sv[k] = 0.f;
+                        } else if (diag) {
 #pragma unroll
                             for (int k = 0; k < 32; k += 2) {
                                 const float2 x = __ffma2_rn(make_float2(sv[k], sv[k + 1]), c1v, nmc);
