@@ -83,6 +83,14 @@ def test_prefill_long_prompt(api, port):
     _case(api, port, "f16", B=1, H=2, s=1100, ncap=1100, seed=11)
 
 
+@pytest.mark.parametrize("dt", ["f16", "bf16"])
+def test_prefill_long_prompt_cta_pairs(api, port, dt):
+    # prompts from s = 1536 take the CTA-pair (cta_group::2) kernel by default;
+    # s = 1700 leaves the last 256-query super-tile ragged (rows past s in
+    # both CTAs of the pair)
+    _case(api, port, dt, B=1, H=2, s=1700, ncap=1710, seed=17, out_f32=(dt == "bf16"))
+
+
 def test_prefill_then_decode(api, port):
     """Prefill on tensor cores, then SWA decode steps: selections and outputs
     follow the oracle engine order (engine.hpp:592-629)."""
