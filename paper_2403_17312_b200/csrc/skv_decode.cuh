@@ -108,7 +108,15 @@ struct DecodeCfg {
     static constexpr int T = ((T0 < TMIN ? TMIN : T0) + TMIN - 1) / TMIN * TMIN;
     static constexpr int RS = T * HG / SLOTS;  // rows per slot per stage
     static constexpr int S = SKV_STAGES;
-    static constexpr int STAGEB = T * ROWB;
+    // Ring stride of one token's rows. A whole INT8 block (HG = 8) is padded
+    // by 96 bytes to a stride = 32 mod 128: the (scale, bias) pairs of four
+    // consecutive tokens x four heads, read once per row by a warp, then fall
+    // in 16 distinct bank pairs (with 1088 they met in the same banks).
+    static constexpr int TS = (QUANT && HG == kU8Group) ? ROWB + 96 : ROWB;
+    // INT8 8-head groups give each lane slot RS CONSECUTIVE tokens (others:
+    // tokens SLOTS / HG apart), so those metadata reads spread over the banks
+    static constexpr bool TOK_ROWS = QUANT && HG == kU8Group;
+    static constexpr int STAGEB = T * TS;
     static_assert(SLOTS % HG == 0, "head group must tile the consumer slots");
     static_assert(T * HG % SLOTS == 0 && RS >= 1 && RS <= LR, "stage rows must tile the slots");
     static_assert(T <= 32, "one producer lane per token row");
@@ -297,7 +305,7 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
                 int t = tslot ? tslot[base + i] : tok[base + i];
                 if (paged && !tslot) t = max(slot_row[t], 0);
                 const uint8_t* tb = kvb + static_cast<size_t>(t) * TOKB;
-                uint8_t* dst = ring + stage * STAGEB + i * ROWB;
+                uint8_t* dst = ring + stage * STAGEB + i * C::TS;
                 const uint8_t* src = tb + (vsel ? off_v : off_k);
                 if constexpr (QUANT) {
                     if constexpr (HG == kU8Group) {  // codes + (scale, bias) of the block: one copy
@@ -408,12 +416,19 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
 #pragma unroll
         for (int off = LR / 2; off > 0; off >>= 1) qsum += __shfl_xor_sync(0xffffffffu, qsum, off);
     }
-    // row r of a stage = (token r / HG, head r % HG); INT8 rows sit at 128-byte
-    // strides inside their token's block, the (scale, bias) pairs after them
-    const uint32_t lane_off = QUANT ? static_cast<uint32_t>((slot / HG) * ROWB + (slot % HG) * D + c * 16)
-                                    : static_cast<uint32_t>(slot * ROWE + c * 16);
-    auto meta_at = [&](const uint8_t* stage_base, int r) {
-        return *reinterpret_cast<const float2*>(stage_base + (r / HG) * ROWB + HG * D + (r % HG) * 8);
+    // A lane's row i of a stage is (token row_tok(i), head h): rows SLOTS
+    // apart (token (slot + i SLOTS) / HG), or for INT8 8-head groups RS
+    // consecutive tokens. INT8 rows sit at 128-byte strides inside their
+    // token's block, the (scale, bias) pairs after them.
+    constexpr int TS = C::TS;
+    const int tok0 = C::TOK_ROWS ? (slot / HG) * RS : 0;
+    auto row_tok = [&](int i) { return C::TOK_ROWS ? tok0 + i : (slot + i * SLOTS) / HG; };
+    const uint32_t lane_off =
+        QUANT ? static_cast<uint32_t>((C::TOK_ROWS ? tok0 : slot / HG) * TS + (slot % HG) * D + c * 16)
+              : static_cast<uint32_t>(slot * ROWE + c * 16);
+    constexpr int RSTRIDE = C::TOK_ROWS ? TS : (QUANT ? (SLOTS / HG) * TS : SLOTS * ROWE);
+    auto meta_of = [&](const uint8_t* stage_base, int t) {  // (scale, bias) of token t, head h
+        return *reinterpret_cast<const float2*>(stage_base + t * TS + HG * D + h * 8);
     };
     const float scale = p.scale;
     // 16-byte vector at q (16-byte aligned for every storage type)
@@ -425,16 +440,16 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
         const int stage = u % S;
         mbar_wait(&full[stage], (u / S) & 1);
         const int base = u * T;
-        const int rows = min(T, m - base) * HG;
+        const int cnt = min(T, m - base);  // tokens copied this round
         const uint8_t* st = ring + stage * STAGEB + lane_off;
         uint4 raw[RS];
-        if (rows == T * HG) {
+        if (cnt == T) {
 #pragma unroll
-            for (int i = 0; i < RS; ++i) raw[i] = ld16(st + i * SLOTS * ROWE);
+            for (int i = 0; i < RS; ++i) raw[i] = ld16(st + i * RSTRIDE);
         } else {  // last chunk: rows past it were not copied this round
 #pragma unroll
             for (int i = 0; i < RS; ++i)
-                raw[i] = slot + i * SLOTS < rows ? ld16(st + i * SLOTS * ROWE) : make_uint4(0u, 0u, 0u, 0u);
+                raw[i] = row_tok(i) < cnt ? ld16(st + i * RSTRIDE) : make_uint4(0u, 0u, 0u, 0u);
         }
         float part[RS];
 #pragma unroll
@@ -452,12 +467,11 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
         }
         int rsel;
         const float dot = reduce_rows<RS, LR>(part, c, rsel);
-        const int r = slot + rsel * SLOTS;
-        if ((c & (LR / RS - 1)) == 0 && r < rows) {
-            const int t = r / HG;
+        const int t = row_tok(rsel);
+        if ((c & (LR / RS - 1)) == 0 && t < cnt) {
             float logit;
             if constexpr (QUANT) {
-                const float2 ms = meta_at(ring + stage * STAGEB, r);
+                const float2 ms = meta_of(ring + stage * STAGEB, t);
                 // codes arrive as 1024 + c (cvt16x2, KvU8): dot = q.c + 1024 * sum(q)
                 logit = fmaf(ms.x, dot, fmaf(-kBiasU8, ms.x, ms.y) * qsum) * scale;
             } else {
@@ -519,20 +533,20 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
         const int stage = u % S;
         mbar_wait(&full[stage], (u / S) & 1);
         const int base = (u - nchunks) * T;
-        const int rows = min(T, m - base) * HG;
+        const int cnt = min(T, m - base);
         const uint8_t* st = ring + stage * STAGEB + lane_off;
-        if (rows == T * HG) {
+        if (cnt == T) {
             uint4 raw[RS];
 #pragma unroll
-            for (int i = 0; i < RS; ++i) raw[i] = ld16(st + i * SLOTS * ROWE);
+            for (int i = 0; i < RS; ++i) raw[i] = ld16(st + i * RSTRIDE);
 #pragma unroll
             for (int i = 0; i < RS; ++i) {
-                const int r = slot + i * SLOTS;
-                const float w = wh[base + r / HG];
+                const int t = row_tok(i);
+                const float w = wh[base + t];
                 float2 vf[V2];
                 cvt16x2(raw[i], vf, KV{});
                 if constexpr (QUANT) {
-                    const float2 ms = meta_at(ring + stage * STAGEB, r);
+                    const float2 ms = meta_of(ring + stage * STAGEB, t);
                     const float a = w * ms.x;
                     const float2 a2 = make_float2(a, a);
 #pragma unroll
@@ -547,13 +561,13 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
         } else {
 #pragma unroll
             for (int i = 0; i < RS; ++i) {
-                const int r = slot + i * SLOTS;
-                if (r < rows) {
-                    const float w = wh[base + r / HG];
+                const int t = row_tok(i);
+                if (t < cnt) {
+                    const float w = wh[base + t];
                     float2 vf[V2];
-                    cvt16x2(ld16(st + i * SLOTS * ROWE), vf, KV{});
+                    cvt16x2(ld16(st + i * RSTRIDE), vf, KV{});
                     if constexpr (QUANT) {
-                        const float2 ms = meta_at(ring + stage * STAGEB, r);
+                        const float2 ms = meta_of(ring + stage * STAGEB, t);
                         const float a = w * ms.x;
                         const float2 a2 = make_float2(a, a);
 #pragma unroll
