@@ -122,7 +122,10 @@ struct DecodeCfg {
     static_assert(T <= 32, "one producer lane per token row");
     static_assert(!QUANT || (HG % 2 == 0 && kU8Group % HG == 0),
                   "INT8 head groups split the 8-head storage blocks into 16-byte sized copies");
-    static_assert(SLOTS * D * 4 <= S * STAGEB, "reduction scratch aliases the ring");
+    // reduction scratch: per slot, each lane's VE partial sums padded to VE + 1
+    // floats, so a warp's stores hit 32 distinct banks
+    static constexpr int RED_SP = LR * (VE + 1);
+    static_assert(SLOTS * RED_SP * 4 <= S * STAGEB, "reduction scratch aliases the ring");
 };
 
 struct DecodeSmem {
@@ -586,18 +589,20 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
     }
     // all stages consumed, no copy in flight: the ring is free scratch now
     named_sync(kBarConsumers, kConsumerThreads);
-    float* red = reinterpret_cast<float*>(ring);  // [SLOTS][D]
+    float* red = reinterpret_cast<float*>(ring);  // [SLOTS][LR][VE + 1]
+    constexpr int SP = C::RED_SP;
 #pragma unroll
     for (int i = 0; i < V2; ++i) {
-        red[slot * D + c * VE + 2 * i] = acc[i].x + bsum;
-        red[slot * D + c * VE + 2 * i + 1] = acc[i].y + bsum;
+        red[slot * SP + c * (VE + 1) + 2 * i] = acc[i].x + bsum;
+        red[slot * SP + c * (VE + 1) + 2 * i + 1] = acc[i].y + bsum;
     }
     named_sync(kBarConsumers, kConsumerThreads);
     for (int o = ctid; o < HG * D; o += kConsumerThreads) {
         const int hh = o / D, d = o % D;
+        const int cell = (d / VE) * (VE + 1) + d % VE;
         float s = 0.f;
 #pragma unroll
-        for (int sl = 0; sl < SLOTS / HG; ++sl) s += red[(sl * HG + hh) * D + d];
+        for (int sl = 0; sl < SLOTS / HG; ++sl) s += red[(sl * HG + hh) * SP + cell];
         const size_t at = (static_cast<size_t>(b) * H + g * HG + hh) * D + d;
         if (p.out_f32)
             static_cast<float*>(p.out)[at] = s;
