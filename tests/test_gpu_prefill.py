@@ -138,13 +138,15 @@ def test_prefill_rejects_unsupported_and_bad_shapes(api):
         c.prefill_sparsity(0)
 
 
-def test_prefill_int8(api, port):
+@pytest.mark.parametrize("s", [300, 1600])
+def test_prefill_int8(api, port, s):
     """INT8 KV (fp16 queries): the layer is dequantised to fp16 for the tensor
     cores; the seed row and the last query's output are redone on the exact
     dequantisation. Reference: dense_attention on the fake-quantised K/V
     (engine.hpp:469-483 groups of D per (token, head))."""
-    B, H, s, D = 2, 8, 300, 128
-    rng = np.random.default_rng(88)
+    # s = 1600: the dequantised layer goes through the CTA-pair kernel (config 4's prompt path)
+    B, H, D = (2, 8, 128) if s < 1000 else (1, 8, 128)
+    rng = np.random.default_rng(88 + s)
     k = round_to(rng.standard_normal((B, s, H, D)), "f16")
     v = round_to(rng.standard_normal((B, s, H, D)), "f16")
     q = round_to(rng.standard_normal((B, s, H, D)) * 0.5, "f16")
