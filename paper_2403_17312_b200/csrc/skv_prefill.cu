@@ -448,54 +448,137 @@ __global__ void __launch_bounds__(kFThreads, 1)
                     }
                     mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
                 } else {
-                    float sv[kFHK];
-#pragma unroll
-                    for (int c = 0; c < kFHK / 32; ++c) tmem_ld32(ca + c * 32, sv + c * 32);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    if (warp == 4 && lane == 0) PFT("row_ld", g);
-                    float l4[4] = {0.f, 0.f, 0.f, 0.f};
-                    unsigned c4[4] = {0u, 0u, 0u, 0u};
-                    if (diag) {
-                        const float c1 = p.c1;
-#pragma unroll
-                        for (int k = 0; k < kFHK; ++k) {
-                            const float ex = ex2_all(fmaf(sv[k], c1, -mc));
-                            const bool in = k <= lim;
-                            const float e = in ? ex : 0.f;
-                            c4[k & 3] += in & (e < 0.01f);
-                            l4[k & 3] += e;
-                            sv[k] = e;
+                    if constexpr (BF16) {
+                        // bf16: scalar row math and count (the packed path costs its hi + lo P a spill)
+                        float sv[kFHK];
+    #pragma unroll
+                        for (int c = 0; c < kFHK / 32; ++c) tmem_ld32(ca + c * 32, sv + c * 32);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        if (warp == 4 && lane == 0) PFT("row_ld", g);
+                        float l4[4] = {0.f, 0.f, 0.f, 0.f};
+                        unsigned c4[4] = {0u, 0u, 0u, 0u};
+                        if (diag) {
+                            const float c1 = p.c1;
+    #pragma unroll
+                            for (int k = 0; k < kFHK; ++k) {
+                                const float ex = ex2_all(fmaf(sv[k], c1, -mc));
+                                const bool in = k <= lim;
+                                const float e = in ? ex : 0.f;
+                                c4[k & 3] += in & (e < 0.01f);
+                                l4[k & 3] += e;
+                                sv[k] = e;
+                            }
+                        } else {
+    #pragma unroll
+                            for (int k = 0; k < kFHK; ++k) {
+                                const float e = ex2(fmaf(sv[k], p.c1, -mc));
+                                c4[k & 3] += e < 0.01f;
+                                l4[k & 3] += e;
+                                sv[k] = e;
+                            }
+                        }
+                        l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
+                        const unsigned ct = (c4[0] + c4[1]) + (c4[2] + c4[3]);
+                        cnt += valid ? ct : 0u;
+                        if (last_row) {
+                            float* wl = p.wlast + zrow + j * kFKeys + hf * kFHK;
+    #pragma unroll
+                            for (int k = 0; k < kFHK; ++k)
+                                if (k <= lim) wl[k] = sv[k];
+                        }
+    #pragma unroll
+                        for (int c = 0; c < kFHK / 32; ++c) {  // 32-key chunks: hi in 16 columns, bf16 lo in the next 16
+                            uint32_t pk[16];
+    #pragma unroll
+                            for (int i = 0; i < 16; ++i) pk[i] = pack2<BF16>(sv[c * 32 + 2 * i], sv[c * 32 + 2 * i + 1]);
+                            tmem_st16(ca + c * 32, pk);
+                            if constexpr (BF16) {
+    #pragma unroll
+                                for (int i = 0; i < 16; ++i)
+                                    pk[i] = pack2<true>(bf16_rest(sv[c * 32 + 2 * i]), bf16_rest(sv[c * 32 + 2 * i + 1]));
+                                tmem_st16(ca + c * 32 + 16, pk);
+                            }
                         }
                     } else {
-#pragma unroll
-                        for (int k = 0; k < kFHK; ++k) {
-                            const float e = ex2(fmaf(sv[k], p.c1, -mc));
-                            c4[k & 3] += e < 0.01f;
-                            l4[k & 3] += e;
-                            sv[k] = e;
+                        float sv[kFHK];
+    #pragma unroll
+                        for (int c = 0; c < kFHK / 32; ++c) tmem_ld32(ca + c * 32, sv + c * 32);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        if (warp == 4 && lane == 0) PFT("row_ld", g);
+                        // packed pairs: FFMA2 for S * c1 - max, FADD2 for l. fp16: the sparsity count
+                        // runs on the packed P (HSET2 + HADD2 per pair, e < 0.01 in fp16), masked
+                        // cells (P = 0) taken off after; bf16 counts the fp32 e.
+                        constexpr bool kHCount = !BF16;
+                        float2 l2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+                        unsigned c4[4] = {0u, 0u, 0u, 0u};
+                        const float2 c1v = make_float2(p.c1, p.c1), nmc = make_float2(-mc, -mc);
+                        if (diag) {
+    #pragma unroll
+                            for (int k = 0; k < kFHK; k += 2) {
+                                const float2 x = __ffma2_rn(make_float2(sv[k], sv[k + 1]), c1v, nmc);
+                                const float x0 = ex2_all(x.x), x1 = ex2_all(x.y);
+                                const bool in0 = k <= lim, in1 = k + 1 <= lim;
+                                const float e0 = in0 ? x0 : 0.f, e1 = in1 ? x1 : 0.f;
+                                if (!kHCount) {
+                                    c4[k & 3] += in0 & (e0 < 0.01f);
+                                    c4[(k + 1) & 3] += in1 & (e1 < 0.01f);
+                                }
+                                l2[(k >> 1) & 1] = __fadd2_rn(l2[(k >> 1) & 1], make_float2(e0, e1));
+                                sv[k] = e0;
+                                sv[k + 1] = e1;
+                            }
+                        } else {
+    #pragma unroll
+                            for (int k = 0; k < kFHK; k += 2) {
+                                const float2 x = __ffma2_rn(make_float2(sv[k], sv[k + 1]), c1v, nmc);
+                                const float e0 = ex2(x.x), e1 = ex2(x.y);
+                                if (!kHCount) {
+                                    c4[k & 3] += e0 < 0.01f;
+                                    c4[(k + 1) & 3] += e1 < 0.01f;
+                                }
+                                l2[(k >> 1) & 1] = __fadd2_rn(l2[(k >> 1) & 1], make_float2(e0, e1));
+                                sv[k] = e0;
+                                sv[k + 1] = e1;
+                            }
                         }
-                    }
-                    l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
-                    const unsigned ct = (c4[0] + c4[1]) + (c4[2] + c4[3]);
-                    cnt += valid ? ct : 0u;
-                    if (last_row) {
-                        float* wl = p.wlast + zrow + j * kFKeys + hf * kFHK;
-#pragma unroll
-                        for (int k = 0; k < kFHK; ++k)
-                            if (k <= lim) wl[k] = sv[k];
-                    }
-#pragma unroll
-                    for (int c = 0; c < kFHK / 32; ++c) {  // 32-key chunks: hi in 16 columns, bf16 lo in the next 16
-                        uint32_t pk[16];
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) pk[i] = pack2<BF16>(sv[c * 32 + 2 * i], sv[c * 32 + 2 * i + 1]);
-                        tmem_st16(ca + c * 32, pk);
-                        if constexpr (BF16) {
-#pragma unroll
-                            for (int i = 0; i < 16; ++i)
-                                pk[i] = pack2<true>(bf16_rest(sv[c * 32 + 2 * i]), bf16_rest(sv[c * 32 + 2 * i + 1]));
-                            tmem_st16(ca + c * 32 + 16, pk);
+                        l += (l2[0].x + l2[0].y) + (l2[1].x + l2[1].y);
+                        if (last_row) {
+                            float* wl = p.wlast + zrow + j * kFKeys + hf * kFHK;
+    #pragma unroll
+                            for (int k = 0; k < kFHK; ++k)
+                                if (k <= lim) wl[k] = sv[k];
                         }
+                        __half2 hc = __floats2half2_rn(0.f, 0.f);
+                        const __half2 thr = __floats2half2_rn(0.01f, 0.01f);
+    #pragma unroll
+                        for (int c = 0; c < kFHK / 32; ++c) {  // 32-key chunks: hi in 16 columns, bf16 lo in the next 16
+                            uint32_t pk[16];
+    #pragma unroll
+                            for (int i = 0; i < 16; ++i) {
+                                pk[i] = pack2<BF16>(sv[c * 32 + 2 * i], sv[c * 32 + 2 * i + 1]);
+                                if constexpr (kHCount) {
+                                    __half2 ph;
+                                    memcpy(&ph, &pk[i], 4);
+                                    hc = __hadd2(hc, __hlt2(ph, thr));
+                                }
+                            }
+                            tmem_st16(ca + c * 32, pk);
+                            if constexpr (BF16) {
+    #pragma unroll
+                                for (int i = 0; i < 16; ++i)
+                                    pk[i] = pack2<true>(bf16_rest(sv[c * 32 + 2 * i]), bf16_rest(sv[c * 32 + 2 * i + 1]));
+                                tmem_st16(ca + c * 32 + 16, pk);
+                            }
+                        }
+                        unsigned ct;
+                        if constexpr (kHCount) {  // masked cells (k > lim) hold P = 0: not part of the count
+                            const int kept = lim < 0 ? 0 : min(lim + 1, kFHK);
+                            ct = static_cast<unsigned>(__half2float(__low2half(hc)) + __half2float(__high2half(hc))) -
+                                 static_cast<unsigned>(kFHK - kept);
+                        } else {
+                            ct = (c4[0] + c4[1]) + (c4[2] + c4[3]);
+                        }
+                        cnt += valid ? ct : 0u;
                     }
                     if (warp == 4 && lane == 0) PFT("row_math", g);
                     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
