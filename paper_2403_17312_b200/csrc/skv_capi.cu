@@ -129,6 +129,7 @@ struct skv_cache {
     std::vector<long long> ledger_j;  // per layer: last step whose actions were applied (-1: none)
     std::vector<int> pend_n;     // per layer: n the index buffer was selected for (-1: none)
     std::vector<double> pend_r;  // per layer: its ratio
+    std::vector<uint8_t> pend_topk;  // per layer: the pending selection is an SWA top-k (incremental_select)
     uint64_t device_bytes = 0;
     int num_sms = 0;
     int max_smem = 0;
@@ -377,6 +378,7 @@ static skv_status cache_create_impl(const skv_cache_desc* desc, uint64_t paged_c
     }
     c->pend_n.assign(d.layers, -1);
     c->pend_r.assign(d.layers, 0.0);
+    c->pend_topk.assign(d.layers, 0);
     c->ledger_j.assign(d.layers, -1);
     c->rec_x.assign(d.layers, nullptr);
     c->rec_wt.assign(d.layers, nullptr);
@@ -735,9 +737,21 @@ void note_pending(skv_cache* c, int layer, const skvd::SelectParams& p, double r
     if (p.select) {
         c->pend_n[layer] = p.n;
         c->pend_r[layer] = r_next;
+        c->pend_topk[layer] = !p.dense && p.variant == 1;
     } else {
         c->pend_n[layer] = -1;
     }
+}
+
+// A fold of the pending selection of layer (tok = its index buffer, made by
+// an SWA top-k at n = cur_tok + 1 with ratio r_next, nothing else written to
+// the importance since: any other writer drops pend_n) lets the select kernel
+// derive the next selection incrementally (incremental_select). Head shards
+// sum the step rows across GPUs first and keep the full top-k.
+bool incr_ok(const skv_cache* c, int layer, const int* tok, int cur_tok, double r_next) {
+    static const bool off = std::getenv("SKV_SELECT_FULL") != nullptr;  // A/B: always the full top-k
+    return !off && !c->reduce && tok == layer_idx(c, layer) && c->pend_topk[layer] &&
+           c->pend_n[layer] == cur_tok + 1 && c->pend_r[layer] == r_next;
 }
 
 // The standalone per-sequence select kernel (skv_select.cuh).
@@ -745,10 +759,12 @@ skv_status launch_select_c(skv_cache* c, int layer, int apply, const int* tok_pr
                            int m_prev, int G, int cur_tok, int n_next, double r_next, bool pdl, cudaStream_t st,
                            int sp_n = 0, double* wsum_out = nullptr, const double* wsum = nullptr) {
     skvd::SelectParams p;
+    const bool incr = apply == 1 && incr_ok(c, layer, tok_prev, cur_tok, r_next);
     c->pend_n[layer] = -1;
     if (skv_status e = make_select_params(c, layer, apply, tok_prev, tok_prev_ld, m_prev, G, cur_tok, n_next, r_next,
                                           sp_n, &p))
         return e;
+    p.incr = incr ? 1 : 0;
     p.wsum_out = wsum_out;
     p.wsum = wsum;
     if (!p.apply && !p.select) return SKV_OK;
@@ -789,6 +805,7 @@ skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok
         if (skv_status e = make_select_params(c, layer, fold.apply, nullptr, 0, m, G, fold.cur_tok, fold.n_next,
                                               fold.r_next, fold.sp_n, &sel))
             return e;
+        sel.incr = fold.apply == 1 && incr_ok(c, layer, tok, fold.cur_tok, fold.r_next) ? 1 : 0;
         // The tail's selection runs on one CTA per sequence while it holds its
         // attend slot: worth it for short candidate lists (configs 2/3: step
         // 0.98->1.02, 0.88->1.01), not for n-k in the thousands (config 4:
@@ -895,6 +912,7 @@ skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok
             if (skv_status e = make_select_params(c, layer, fold.apply, tok, tok_ld, m, G, fold.cur_tok, fold.n_next,
                                                   fold.r_next, fold.sp_n, &sp))
                 return e;
+            sp.incr = fold.apply == 1 && incr_ok(c, layer, tok, fold.cur_tok, fold.r_next) ? 1 : 0;
             c->pend_n[layer] = -1;
             c->deferred.emplace_back(layer, sp);
             note_pending(c, layer, sp, fold.r_next);
@@ -1237,10 +1255,12 @@ static skv_status launch_deferred(skv_cache* c, cudaStream_t st) {
     skvd::SelectParams p = c->deferred.front().second;
     const int first = c->deferred.front().first;
     const int cnt = static_cast<int>(c->deferred.size());
-    for (int i = 0; i < cnt; ++i)
+    for (int i = 0; i < cnt; ++i) {
         SKV_REQUIRE(c->deferred[i].first == first + i && c->deferred[i].second.m_prev == p.m_prev &&
                         c->deferred[i].second.G == p.G,
                     "decode_step: deferred selects must be consecutive layers of one shape");
+        p.incr &= c->deferred[i].second.incr;  // one flag for the whole batched launch
+    }
     p.ls_imp = static_cast<long long>(c->d.batch) * c->d.capacity;
     p.ls_wpart = static_cast<long long>(c->d.batch) * c->d.heads * c->d.capacity;
     p.ls_idx = static_cast<long long>(c->d.batch) * c->d.capacity;

@@ -42,6 +42,11 @@ struct SelectParams {
     int* idx;  // [B][idx_ld]
     long long idx_ld;
     int pdl_wait;
+    // 1: tok_prev is an SWA top-k selection made at n0 = cur_tok + 1 (its k0
+    // global picks, then the local window) over the importance as it stands
+    // before this fold (the host tracks it per layer). The next selection may
+    // then be derived from it (incremental_select) instead of a full top-k.
+    int incr;
     // head sharding (the cache holds some of the model's heads): the step row
     // v[pos] = sum over ALL heads of w is summed across the shards between a
     // partial pass (wsum_out: this shard's head sum, nothing else) and the
@@ -93,6 +98,123 @@ __device__ __forceinline__ void stage_candidates(double* kd, const double* imp, 
 #define SEL_TRACE(i)
 #endif
 
+// Incremental swa_select (attention.hpp:142-171) for step n0 + 1 from the
+// selection of step n0, exact under the reference's order (value desc, index
+// asc). G0, the k0 global picks of step n0, are the top k0 of [0, n0 - k0)
+// before the fold; the fold only raises their importance (w >= 0) and leaves
+// every other candidate unchanged, so they are still the top k0 of that range.
+// Step n0 + 1 selects k1 in {k0, k0 + 1} (k is non-decreasing, by <= 1 per
+// step):
+//  - k1 = k0: the range gains x = n0 - k0 (leaving the local window), and the
+//    top k0 of G0 + {x} is G0 with its weakest member replaced by x if x ranks
+//    above it;
+//  - k1 = k0 + 1: same range, top k0 + 1 = G0 + the best candidate outside G0
+//    (one pass over the candidates).
+// Either way there are no radix passes, and for k1 = k0 (most steps) no
+// candidate is read. G0 sits ascending in positions [0, k0) of the token
+// list, x at k0; o may alias the token list (every read is in registers).
+template <int NT, int BAR, int R>
+__device__ __forceinline__ void incremental_select(const SelectParams& p, int tid, int k0, int n0, int nc,
+                                                   const int (&ti)[R], const double (&nvi)[R], const double* imp,
+                                                   uint32_t* bm, TopkSmem<NT>& s, int* o) {
+    const int lane = tid & 31, warp = tid >> 5, k1 = p.k;
+    const bool weak = k1 == k0;  // find G0's weakest member (else: the best candidate outside G0)
+    // a ranks before b (the reference's comparator, matrix.hpp:168-173)
+    auto beats = [](uint64_t ka, int ia, uint64_t kb, int ib) { return ka > kb || (ka == kb && ia < ib); };
+    auto better = [&](uint64_t ka, int ia, uint64_t kb, int ib) {
+        return weak ? beats(kb, ib, ka, ia) : beats(ka, ia, kb, ib);
+    };
+    uint64_t bk = weak ? ~0ull : 0ull;  // sentinels: every real element ranks below / above them
+    int bi = weak ? -1 : 0x7fffffff;
+    if (weak) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int pos = tid + r * NT;
+            if (pos < k0) {
+                const uint64_t kk = order_key(nvi[r]);
+                if (better(kk, ti[r], bk, bi)) {
+                    bk = kk;
+                    bi = ti[r];
+                }
+            } else if (pos == k0) {
+                s.mask = order_key(nvi[r]);  // x = n0 - k0, the first local token
+            }
+        }
+    } else {
+        const int words = (nc + 31) >> 5;
+        for (int i = tid; i < words; i += NT) bm[i] = 0u;
+        named_sync(BAR, NT);
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+            if (tid + r * NT < k0) atomicOr(&bm[ti[r] >> 5], 1u << (ti[r] & 31));
+        named_sync(BAR, NT);
+        for (int i = tid; i < nc; i += NT) {
+            if ((bm[i >> 5] >> (i & 31)) & 1u) continue;
+            const uint64_t kk = order_key(imp[i]);
+            if (better(kk, i, bk, bi)) {
+                bk = kk;
+                bi = i;
+            }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (better(ok, oi, bk, bi)) {
+            bk = ok;
+            bi = oi;
+        }
+    }
+    if (lane == 0) {
+        s.warp_tot[warp] = bk;
+        s.warp_and[warp] = static_cast<uint64_t>(static_cast<uint32_t>(bi));
+    }
+    named_sync(BAR, NT);
+    if (tid == 0) {
+        for (int w = 1; w < NT / 32; ++w) {
+            const uint64_t ok = s.warp_tot[w];
+            const int oi = static_cast<int>(static_cast<uint32_t>(s.warp_and[w]));
+            if (better(ok, oi, bk, bi)) {
+                bk = ok;
+                bi = oi;
+            }
+        }
+        // weak: the member of G0 that x replaces (-1: none); else the added candidate
+        s.remaining = weak ? (beats(s.mask, n0 - k0, bk, bi) ? bi : -1) : bi;
+    }
+    named_sync(BAR, NT);
+    const int e = s.remaining;
+    if (weak) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int pos = tid + r * NT;
+            if (pos >= k0 || ti[r] == e) continue;
+            o[(e >= 0 && ti[r] > e) ? pos - 1 : pos] = ti[r];
+        }
+        if (e >= 0 && tid == 0) o[k0 - 1] = n0 - k0;
+    } else {
+        int below = 0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int pos = tid + r * NT;
+            if (pos >= k0) continue;
+            o[ti[r] > e ? pos + 1 : pos] = ti[r];
+            below += ti[r] < e;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) below += __shfl_xor_sync(0xffffffffu, below, off);
+        if (lane == 0) s.warp_tot[warp] = static_cast<uint64_t>(below);  // tid 0's reads precede the last barrier
+        named_sync(BAR, NT);
+        if (tid == 0) {
+            int cnt = 0;
+            for (int w = 0; w < NT / 32; ++w) cnt += static_cast<int>(s.warp_tot[w]);
+            o[cnt] = e;
+        }
+    }
+    for (int i = tid; i < k1; i += NT) o[k1 + i] = p.n - k1 + i;  // local window
+}
+
 template <int NT, int BAR>
 __device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<NT>& s, uint64_t* keys,
                                 SelectScratch<NT>& sc) {
@@ -103,6 +225,14 @@ __device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<N
     double* kd = reinterpret_cast<double*>(keys);
     SEL_TRACE(0);
     constexpr int R = 4;  // folded positions per thread held in registers (fast path)
+    // Incremental selection (incremental_select): decided from the parameters
+    // alone, before anything is staged.
+    const int k0 = p.m_prev / 2, n0 = p.cur_tok + 1;
+    const bool incr = p.incr && topk && p.apply == 1 && p.tok_prev != nullptr && !p.wsum && !p.wsum_out &&
+                      p.m_prev <= R * NT && p.m_prev == 2 * k0 && 2 * k0 < n0 && p.n == n0 + 1 &&
+                      (p.k == k0 || p.k == k0 + 1) && p.variant == 1;
+    int ti[R];      // fast path: folded token per position (-1: none)
+    double nvi[R];  // and its new importance
     if (p.apply) {
         const float* wp = p.wpart + static_cast<size_t>(b) * p.G * p.m_prev;
         const int* tp = p.tok_prev ? p.tok_prev + static_cast<size_t>(b) * p.tok_prev_ld : nullptr;
@@ -140,15 +270,18 @@ __device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<N
                     if (!assign_all && t[r] != p.cur_tok) old[r] = imp[t[r]];
                 }
             }
-            stage_candidates<NT>(kd, imp, nc, tid);
+            if (!incr) stage_candidates<NT>(kd, imp, nc, tid);
             named_sync(BAR, NT);  // staged candidates complete; every old value read
             DTR_T(9, tid);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
+                ti[r] = t[r];
+                nvi[r] = 0.0;
                 if (t[r] < 0) continue;
                 const double nv = (assign_all || t[r] == p.cur_tok) ? v[r] : old[r] + v[r];
                 imp[t[r]] = nv;
-                if (t[r] < nc) kd[t[r]] = nv;
+                nvi[r] = nv;
+                if (!incr && t[r] < nc) kd[t[r]] = nv;
                 vmax = v[r] > vmax ? v[r] : vmax;
             }
         } else {
@@ -237,6 +370,10 @@ __device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<N
     }
     if (p.dense) {
         for (int i = tid; i < p.m; i += NT) o[i] = i;
+        return;
+    }
+    if (incr) {
+        incremental_select<NT, BAR, R>(p, tid, k0, n0, nc, ti, nvi, imp, reinterpret_cast<uint32_t*>(keys), s, o);
         return;
     }
     SEL_TRACE(1);

@@ -615,3 +615,27 @@ def test_attend_over_indices_unsorted_repeated(api, port, dt):
         assert_close(out[b].float().cpu().numpy(), attn, TOL[dt], f"attn b={b}")
         np.testing.assert_allclose(imp[b] - base[b], aw, rtol=1e-4, atol=1e-7)
         assert abs(sp[b] - port.attention_sparsity(aw[None])) <= 1.0 / n
+
+
+def test_incremental_select_matches_full(tmp_path):
+    """The select kernel derives a decode step's selection from the previous
+    one (incremental_select, skv_select.cuh) whenever the previous selection
+    was an SWA top-k and only this step's fold touched the importance. Every
+    selection of tie-heavy (zero queries: all weights equal), coarse and random
+    trajectories, through the attend tail (per-layer calls) and the batched
+    select (whole steps), at r = 0.2 / 0.5 / 0.05, must equal the full radix
+    top-k's (SKV_SELECT_FULL=1) bit for bit."""
+    import os
+    import subprocess
+    import sys
+
+    helper = os.path.join(os.path.dirname(os.path.abspath(__file__)), "select_traj.py")
+    outs = {}
+    for tag, env in (("incr", {}), ("full", {"SKV_SELECT_FULL": "1"})):
+        path = str(tmp_path / f"{tag}.npz")
+        r = subprocess.run([sys.executable, helper, path], env=dict(os.environ, **env), capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        outs[tag] = np.load(path)
+    for key in outs["full"].files:
+        assert np.array_equal(outs["incr"][key], outs["full"][key]), key
