@@ -229,7 +229,7 @@ __device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<N
     // alone, before anything is staged.
     const int k0 = p.m_prev / 2, n0 = p.cur_tok + 1;
     const bool incr = p.incr && topk && p.apply == 1 && p.tok_prev != nullptr && !p.wsum && !p.wsum_out &&
-                      p.m_prev <= R * NT && p.m_prev == 2 * k0 && 2 * k0 < n0 && p.n == n0 + 1 &&
+                      k0 < R * NT && p.m_prev == 2 * k0 && 2 * k0 < n0 && p.n == n0 + 1 &&
                       (p.k == k0 || p.k == k0 + 1) && p.variant == 1;
     int ti[R];      // fast path: folded token per position (-1: none)
     double nvi[R];  // and its new importance
@@ -311,7 +311,19 @@ __device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<N
                 }
             }
             named_sync(BAR, NT);  // the folded importance is visible to the staging
-            stage_candidates<NT>(kd, imp, nc, tid);
+            if (incr) {
+                // G0 and x (positions 0..k0 of the list) with their folded values, as the fast path
+                // holds them; every read precedes incremental_select's first barrier (o may alias tp)
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int pos = tid + r * NT;
+                    ti[r] = pos <= k0 ? tp[pos] : -1;
+                }
+#pragma unroll
+                for (int r = 0; r < R; ++r) nvi[r] = ti[r] >= 0 ? imp[ti[r]] : 0.0;
+            } else {
+                stage_candidates<NT>(kd, imp, nc, tid);
+            }
         }
         DTR_T(10, tid);
         if (p.sp_n > 0) {

@@ -15,8 +15,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2403_17312_b200 import api  # noqa: E402
 
 
-def run(kind, r, steps, seed):
-    B, H, D, s, L = 3, 8, 128, 60, 2
+def run(kind, r, steps, seed, s=60):
+    B, H, D, L = 3, 8, 128, 2
     g = torch.Generator(device="cuda").manual_seed(seed)
     ncap = s + steps + 2  # the last step still selects for n + 1
     kv = torch.randn(B, ncap, 2, H, D, device="cuda", generator=g).half()
@@ -50,4 +50,7 @@ if __name__ == "__main__":
     for kind in ("ties", "coarse", "random"):
         for r in (0.2, 0.5, 0.05):
             out[f"{kind}_{r}"] = run(kind, r, 40, 7)
+    # m = 2k > 4 x 128: the fold's long path (k0 < 512 still selects incrementally)
+    for kind in ("ties", "random"):
+        out[f"long_{kind}"] = run(kind, 0.2, 30, 9, s=2600)
     np.savez(sys.argv[1], **out)

@@ -623,8 +623,9 @@ def test_incremental_select_matches_full(tmp_path):
     was an SWA top-k and only this step's fold touched the importance. Every
     selection of tie-heavy (zero queries: all weights equal), coarse and random
     trajectories, through the attend tail (per-layer calls) and the batched
-    select (whole steps), at r = 0.2 / 0.5 / 0.05, must equal the full radix
-    top-k's (SKV_SELECT_FULL=1) bit for bit."""
+    select (whole steps), at r = 0.2 / 0.5 / 0.05, and past the fold's fast
+    path (m > 512 at n = 2600), must equal the full radix top-k's
+    (SKV_SELECT_FULL=1) bit for bit."""
     import os
     import subprocess
     import sys
