@@ -29,8 +29,13 @@ def _code(dt) -> int:
 
 
 def _stream(t: torch.Tensor | None = None):
-    dev = t.device if t is not None else torch.device("cuda", torch.cuda.current_device())
-    return C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    # the raw cudaStream_t of the current stream (an int; ctypes passes it as void*)
+    idx = t.device.index if t is not None else torch.cuda.current_device()
+    return _raw_stream(torch.cuda.current_device() if idx is None else idx)
+
+
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None) or (
+    lambda i: torch.cuda.current_stream(i).cuda_stream)
 
 
 def _ptr(t: torch.Tensor | None):
@@ -352,12 +357,15 @@ class SwaCache:
         return out, idx, w
 
     def swa_decode_step(self, n: int, r: float, q, k_new, v_new, out=None):
+        # per-step host cost matters at config 1 (one layer, b = 1): checks kept, object churn trimmed
         shp = (self.layers, self.batch, self.heads, self.head_dim)
         for t in (q, k_new, v_new):
             self._q(t, shp)
         out = torch.empty(q.shape, dtype=self.out_dtype, device=self.dev) if out is None else out
-        check(lib().skv_swa_decode_step(self._h, n, r, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(out),
-                                        _stream(q)))
+        st = _raw_stream(q.device.index) if q.is_cuda else None
+        rc = lib().skv_swa_decode_step(self._h, n, r, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(out), st)
+        if rc:
+            check(rc)
         return out
 
     def swa_decode_step_host(self, n: int, r: float, q, k_new, v_new, out):

@@ -883,6 +883,16 @@ skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok
     // across layers: a PDL-overlapped predecessor could still be using it,
     // so such launches wait for the previous grid to finish.
     if (gmem) pdl = false;
+    // A per-layer step whose attend carries the fold + select tail (config 1:
+    // the whole step is this one launch) launches with PDL and waits at entry:
+    // it is resident while the previous step drains, hiding the launch gap.
+    // Not with a plan: the ledger kernel of Phase I steps does not wait on
+    // its predecessor, so waiting on it would not order after the attend.
+    static const bool entry_pdl = std::getenv("SKV_NO_ENTRY_PDL") == nullptr;
+    if (!pdl && fused && entry_pdl && !c->has_plan && !c->prof) {
+        pdl = true;
+        p.pdl_wait = 2;
+    }
     SKV_CUDA(launch_attend(*dl, p, grid_g, smem, pdl, st));
     c->algo_bytes += attend_algo_bytes(c, m, append);
     c->attend_launches += 1;

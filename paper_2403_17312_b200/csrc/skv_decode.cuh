@@ -66,7 +66,7 @@ struct AttendParams {
     float* w_out;        // optional [B][H][m]
     float* wpart;        // [B][G][m]: sum over the CTA's heads of w, per position
     int B, H, Ncap, n, m;
-    int append, out_f32, pdl_wait;
+    int append, out_f32, pdl_wait;  // pdl_wait: 1 before q / new rows, 2 at entry
     float scale;
     // Tail (fold != 0): the last CTA of each sequence folds the head-group
     // weight partials into the fp64 importance and selects the next step
@@ -107,7 +107,10 @@ struct DecodeCfg {
     static constexpr int T0 = SKV_STAGE_BYTES / ROWB > 32 ? 32 : SKV_STAGE_BYTES / ROWB;
     static constexpr int T = ((T0 < TMIN ? TMIN : T0) + TMIN - 1) / TMIN * TMIN;
     static constexpr int RS = T * HG / SLOTS;  // rows per slot per stage
-    static constexpr int S = SKV_STAGES;
+    // fp32 rows at 1-2 heads per CTA are the small-grid latency case (config
+    // 1: b = 1, 32 CTAs on 148 SMs): a ring twice as deep keeps a whole K pass
+    // (and the first V chunks) in flight instead of two round trips.
+    static constexpr int S = (E == 4 && !QUANT && HG <= 2) ? 2 * SKV_STAGES : SKV_STAGES;
     // Ring stride of one token's rows. A whole INT8 block (HG = 8) is padded
     // by 96 bytes to a stride = 32 mod 128: the (scale, bias) pairs of four
     // consecutive tokens x four heads, read once per row by a warp, then fall
@@ -222,6 +225,10 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
     float* wts = gmem ? p.gwts + (static_cast<size_t>(b) * gridDim.x + g) * HG * p.Ncap
                       : reinterpret_cast<float*>(smem + L.wts);  // [HG][m]
 
+    // pdl_wait == 2: a PDL launch that reads its predecessor's outputs from
+    // the start (per-layer steps, skv_capi.cu launch_attend_c): wait first,
+    // so a kernel launched behind this one never overtakes that predecessor.
+    if (p.pdl_wait == 2) pdl_wait();
     // Let the next kernel in the stream (the select kernel) get scheduled now;
     // it waits for this grid's completion before touching our outputs.
     pdl_launch_dependents();
@@ -489,7 +496,41 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
 
     DTR(2);
     // ---- softmax with the reference's normaliser (attention.hpp:213-218)
-    for (int hh = warp; hh < HG; hh += kConsumerWarps) {
+    if constexpr (HG < kConsumerWarps) {
+        // fewer heads than warps (fp32 / bf16 groups): WPH warps share a head's
+        // row, max and sum combined through shared memory (the select scratch,
+        // idle until the tail) -- config 1 ran this on one warp of eight
+        constexpr int WPH = kConsumerWarps / HG;
+        float* sred = reinterpret_cast<float*>(smem + L.scratch);  // [2][kConsumerWarps]
+        const int hh = warp / WPH, part = warp % WPH;
+        float* wl = wts + hh * m;
+        const int i0 = part * 32 + lane;
+        float mx = -INFINITY;
+        for (int i = i0; i < m; i += WPH * 32) mx = fmaxf(mx, wl[i]);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        if (lane == 0) sred[warp] = mx;
+        named_sync(kBarConsumers, kConsumerThreads);
+        mx = sred[hh * WPH];
+#pragma unroll
+        for (int j = 1; j < WPH; ++j) mx = fmaxf(mx, sred[hh * WPH + j]);
+        float sum = 0.f;
+        for (int i = i0; i < m; i += WPH * 32) {
+            const float e = expf(wl[i] - mx);
+            wl[i] = e;
+            sum += e;
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+        if (lane == 0) sred[kConsumerWarps + warp] = sum;
+        named_sync(kBarConsumers, kConsumerThreads);
+        sum = 0.f;
+#pragma unroll
+        for (int j = 0; j < WPH; ++j) sum += sred[kConsumerWarps + hh * WPH + j];
+        const float inv = 1.0f / sum;
+        for (int i = i0; i < m; i += WPH * 32) wl[i] *= inv;
+    }
+    for (int hh = warp; hh < HG && HG >= kConsumerWarps; hh += kConsumerWarps) {
         float* wl = wts + hh * m;
         float mx = -INFINITY;
         for (int i = lane; i < m; i += 32) mx = fmaxf(mx, wl[i]);
