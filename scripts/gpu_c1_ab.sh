@@ -1,13 +1,13 @@
 # config-1 change check: all GPU tests + the parity soak on the new build, then config 1 (c1_probe and
-# bench) and config 3 / 2 with the new build vs build_var/libbase.so (the previous commit), twice
+# bench) and config 4 / 2 with the new build vs build_var/libbase.so (the previous commit), twice
 TAG=${1:-c1ab}
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out/$TAG
 timeout -s KILL 1500 python -m pytest tests -m gpu -q -x --timeout 600 -p no:cacheprovider > gpurun_out/$TAG/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/$TAG/pytest_gpu.log
-timeout -s KILL 900 python scripts/parity_soak.py --seeds 12 > gpurun_out/$TAG/soak.log 2>&1; echo "soak rc=$?"; tail -2 gpurun_out/$TAG/soak.log
+timeout -s KILL 900 python scripts/parity_soak.py --seeds 6 > gpurun_out/$TAG/soak.log 2>&1; echo "soak rc=$?"; tail -2 gpurun_out/$TAG/soak.log
 for rep in 1 2; do for lib in new base; do
   if [ $lib = base ]; then E="SKV_LIB=build_var/libbase.so"; else E="SKV_X=1"; fi
   env $E timeout -s KILL 300 python scripts/c1_probe.py > gpurun_out/$TAG/c1_$lib$rep.log 2>&1; echo "c1 $lib: $(grep 'C1 step' gpurun_out/$TAG/c1_$lib$rep.log)"
-  for c in 1 3 2; do
+  for c in 1 4 2; do
   env $E timeout -s KILL 600 python bench.py --config $c --steps 30 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/$TAG/b.log 2>&1
   python -c "
 import json,sys
