@@ -670,7 +670,7 @@ __global__ void __launch_bounds__(kDecodeThreads, attend_min_blocks<KV>())
             sp.tok_prev = tok;  // this CTA's (shared) token list, same for every group
             sp.tok_prev_ld = 0;
             DTR_TAIL(6);
-            fold_and_select<kConsumerThreads, kBarConsumers>(
+            fold_and_select<kConsumerThreads, kBarConsumers, (KV::E == 4 && !KV::QUANT)>(
                 sp, b, ctid, *reinterpret_cast<TopkSmem<kConsumerThreads>*>(smem + L.topk),
                 reinterpret_cast<uint64_t*>(ring), *reinterpret_cast<SelectScratch<kConsumerThreads>*>(smem + L.scratch));
             if (ctid == 0) p.counters[b] = 0;

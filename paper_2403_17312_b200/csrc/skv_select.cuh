@@ -215,7 +215,7 @@ __device__ __forceinline__ void incremental_select(const SelectParams& p, int ti
     for (int i = tid; i < k1; i += NT) o[k1 + i] = p.n - k1 + i;  // local window
 }
 
-template <int NT, int BAR>
+template <int NT, int BAR, bool WIDE = false>
 __device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<NT>& s, uint64_t* keys,
                                 SelectScratch<NT>& sc) {
     double* imp = p.imp + static_cast<size_t>(b) * p.imp_ld;
@@ -241,7 +241,23 @@ __device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<N
         auto row = [&](int pos) {
             if (ws) return ws[pos];
             double v = 0.0;
-            for (int g = 0; g < p.G; ++g) v += static_cast<double>(__ldcg(wp + static_cast<size_t>(g) * p.m_prev + pos));
+            if constexpr (WIDE) {
+                // fp32 attend tails (config 1's 32 one-head CTAs; the 16-bit
+                // kernels' 56-register budget would spill): every load of a
+                // 32-group block is issued before the first add -- one L2 round
+                // trip instead of two batches of 16; the adds keep the group order
+                int g = 0;
+                for (; g + 32 <= p.G; g += 32) {
+                    float x[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) x[j] = __ldcg(wp + static_cast<size_t>(g + j) * p.m_prev + pos);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v += static_cast<double>(x[j]);
+                }
+                for (; g < p.G; ++g) v += static_cast<double>(__ldcg(wp + static_cast<size_t>(g) * p.m_prev + pos));
+            } else {
+                for (int g = 0; g < p.G; ++g) v += static_cast<double>(__ldcg(wp + static_cast<size_t>(g) * p.m_prev + pos));
+            }
             return v;
         };
         if (p.wsum_out) {  // head-shard partial pass: this shard's sum only
