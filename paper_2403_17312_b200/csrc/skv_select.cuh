@@ -69,7 +69,8 @@ __host__ __device__ inline size_t select_smem(int nc) {
 template <int NT>
 struct SelectScratch {
     double red_max[NT / 32];
-    int red_cnt[NT / 32];
+    int red_cnt[NT / 32];  // (unused since the count went to `below`)
+    int below;             // the sparsity count, summed with shared atomics
 };
 
 // The body shared by swa_select_kernel and the attend kernel's tail: NT
@@ -224,6 +225,29 @@ __device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<N
     const int nc = topk ? p.n - p.k : 0;
     double* kd = reinterpret_cast<double*>(keys);
     SEL_TRACE(0);
+    // sparsity helpers: each warp's max of the step row goes to sc.red_max
+    // before a barrier the fold already has (tid 0 zeroes the count there too)
+    auto publish_max = [&](double vm) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double o = __shfl_xor_sync(0xffffffffu, vm, off);
+            vm = o > vm ? o : vm;
+        }
+        if ((tid & 31) == 0) sc.red_max[tid >> 5] = vm;
+        if (tid == 0) sc.below = 0;
+    };
+    auto row_max = [&]() {
+        double mx = 0.0;
+        for (int w = 0; w < NT / 32; ++w) mx = sc.red_max[w] > mx ? sc.red_max[w] : mx;
+        return mx;
+    };
+    auto finish_sparsity = [&]() {
+        if (tid == 0) {
+            const double mx = row_max();
+            const int sparse = mx == 0.0 ? p.sp_n : sc.below + (p.sp_n - p.m_prev);
+            p.sparsity[b] = static_cast<double>(sparse) / static_cast<double>(p.sp_n);
+        }
+    };
     constexpr int R = 4;  // folded positions per thread held in registers (fast path)
     // Incremental selection (incremental_select): decided from the parameters
     // alone, before anything is staged.
@@ -287,7 +311,10 @@ __device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<N
                 }
             }
             if (!incr) stage_candidates<NT>(kd, imp, nc, tid);
-            named_sync(BAR, NT);  // staged candidates complete; every old value read
+#pragma unroll
+            for (int r = 0; r < R; ++r) vmax = t[r] >= 0 && v[r] > vmax ? v[r] : vmax;
+            if (p.sp_n > 0) publish_max(vmax);
+            named_sync(BAR, NT);  // staged candidates complete; every old value read (+ the warps' maxima)
             DTR_T(9, tid);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -298,7 +325,6 @@ __device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<N
                 imp[t[r]] = nv;
                 nvi[r] = nv;
                 if (!incr && t[r] < nc) kd[t[r]] = nv;
-                vmax = v[r] > vmax ? v[r] : vmax;
             }
         } else {
             // Long selections (config 4: m = 820 at 128 threads): rounds of R
@@ -326,7 +352,8 @@ __device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<N
                     vmax = w[r] > vmax ? w[r] : vmax;
                 }
             }
-            named_sync(BAR, NT);  // the folded importance is visible to the staging
+            if (p.sp_n > 0) publish_max(vmax);
+            named_sync(BAR, NT);  // the folded importance is visible to the staging (+ the warps' maxima)
             if (incr) {
                 // G0 and x (positions 0..k0 of the list) with their folded values, as the fast path
                 // holds them; every read precedes incremental_select's first barrier (o may alias tp)
@@ -344,17 +371,10 @@ __device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<N
         DTR_T(10, tid);
         if (p.sp_n > 0) {
             // attention_sparsity (attention.hpp:275-310) of the head-summed step
-            // row new_aw_row (length sp_n, zeros off-selection), threshold 0.01
-            const int lane = tid & 31, warp = tid >> 5;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                const double o = __shfl_xor_sync(0xffffffffu, vmax, off);
-                vmax = o > vmax ? o : vmax;
-            }
-            if (lane == 0) sc.red_max[warp] = vmax;
-            named_sync(BAR, NT);
-            double mx = 0.0;
-            for (int w = 0; w < NT / 32; ++w) mx = sc.red_max[w] > mx ? sc.red_max[w] : mx;
+            // row new_aw_row (length sp_n, zeros off-selection), threshold 0.01.
+            // The row max was published before the fold's barrier; the count is
+            // summed into sc.below and read after the next barrier (finish_sparsity)
+            const double mx = row_max();
             const double thr = 0.01 * mx;
             int below = 0;
             if (p.m_prev <= R * NT) {
@@ -371,20 +391,20 @@ __device__ void fold_and_select(const SelectParams p, int b, int tid, TopkSmem<N
             }
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) below += __shfl_xor_sync(0xffffffffu, below, off);
-            if (lane == 0) sc.red_cnt[warp] = below;
-            named_sync(BAR, NT);
-            if (tid == 0) {
-                int cnt = 0;
-                for (int w = 0; w < NT / 32; ++w) cnt += sc.red_cnt[w];
-                const int sparse = mx == 0.0 ? p.sp_n : cnt + (p.sp_n - p.m_prev);
-                p.sparsity[b] = static_cast<double>(sparse) / static_cast<double>(p.sp_n);
-            }
+            if ((tid & 31) == 0 && below) atomicAdd(&sc.below, below);
         }
     } else {
         stage_candidates<NT>(kd, imp, nc, tid);
     }
-    if (!p.select) return;
-    named_sync(BAR, NT);  // the fold and the staged candidates are complete
+    if (!p.select) {
+        if (p.sp_n > 0) {
+            named_sync(BAR, NT);  // every warp's count is in
+            finish_sparsity();
+        }
+        return;
+    }
+    named_sync(BAR, NT);  // the fold and the staged candidates are complete (and the sparsity count)
+    if (p.sp_n > 0) finish_sparsity();
     DTR_T(7, tid);
     int* o = p.idx + static_cast<size_t>(b) * p.idx_ld;
     if (p.variant == 2) {  // local_attention_mask (attention.hpp:247-256): the last m tokens
