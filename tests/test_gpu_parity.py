@@ -640,3 +640,44 @@ def test_incremental_select_matches_full(tmp_path):
         outs[tag] = np.load(path)
     for key in outs["full"].files:
         assert np.array_equal(outs["incr"][key], outs["full"][key]), key
+
+
+@pytest.mark.parametrize("dt", ["f32", "f16"])
+def test_entry_pdl_orders_after_device_producer(api, dt):
+    """Single-layer steps launch their attend with PDL and wait at entry
+    (launch_attend_c, pdl_wait = 2). Inputs written by a device kernel right
+    before each call, into buffers reused every step (and the output read
+    right after), must give the same bits as steps separated by a full
+    synchronize with fresh tensors."""
+    L, B, H, D, s, steps = 1, 1, 32, 128, 300, 24
+    g = torch.Generator(device="cuda").manual_seed(7)
+    k0 = torch.randn(B, s, H, D, device="cuda", generator=g).to(TD[dt])
+    v0 = torch.randn(B, s, H, D, device="cuda", generator=g).to(TD[dt])
+    q0 = torch.randn(B, H, D, device="cuda", generator=g).to(TD[dt])
+    src = [torch.randn(3, L, B, H, D, device="cuda", generator=g).to(TD[dt]) for _ in range(steps)]
+    caches = []
+    for _ in range(2):
+        c = api.SwaCache(L, B, H, D, s + steps + 1, kv_dtype=dt)
+        c.append_tokens(0, 0, 0, k0, v0)
+        c.prefill_seed(0, s, q0)
+        caches.append(c)
+    torch.cuda.synchronize()
+    # fast: device producer -> decode -> device consumer, no host sync in between
+    qb, kb, vb = (torch.empty(L, B, H, D, device="cuda", dtype=TD[dt]) for _ in range(3))
+    out_b = torch.empty(L, B, H, D, device="cuda", dtype=caches[0].out_dtype)
+    fast = torch.empty(steps, L, B, H, D, device="cuda", dtype=caches[0].out_dtype)
+    for j in range(steps):
+        torch.mul(src[j][0], 1.0, out=qb)
+        torch.mul(src[j][1], 1.0, out=kb)
+        torch.mul(src[j][2], 1.0, out=vb)
+        caches[0].swa_decode_step(s + j + 1, 0.2, qb, kb, vb, out_b)
+        fast[j].copy_(out_b)
+    torch.cuda.synchronize()
+    for j in range(steps):
+        q, k, v = (src[j][i].clone() for i in range(3))
+        torch.cuda.synchronize()
+        o = caches[1].swa_decode_step(s + j + 1, 0.2, q, k, v)
+        torch.cuda.synchronize()
+        assert torch.equal(o, fast[j]), j
+    n = s + steps
+    assert torch.equal(caches[0].importance(0, n), caches[1].importance(0, n))
