@@ -369,12 +369,15 @@ def test_decode_multilayer_step(api, s):
             assert torch.equal(caches[0].importance(l, n), caches[2].importance(l, n))
 
 
-def test_decode_step_host_pipelined(api):
+@pytest.mark.parametrize("L,H,steps", [(11, 4, 4), (1, 32, 12)])
+def test_decode_step_host_pipelined(api, L, H, steps):
     """The host-buffer step (layer chunks pipelined over two copy streams)
     over several back-to-back calls with no synchronisation in between ==
-    the device step, bit for bit; L=11 gives uneven chunks."""
+    the device step, bit for bit; L=11 gives uneven chunks. L=1 is one chunk
+    whose attend launches with the entry-wait PDL behind the copy stream's
+    event."""
     rng = np.random.default_rng(9)
-    L, B, H, D, s, steps = 11, 3, 4, 128, 60, 4
+    B, D, s = 3, 128, 60
     kv = torch.from_numpy(rng.standard_normal((L, B, s, 2, H, D))).half().cuda()
     qs = [[torch.from_numpy(rng.standard_normal((L, B, H, D))).half() for _ in range(3)] for _ in range(steps)]
     caches = [api.SwaCache(L, B, H, D, s + steps, kv_dtype="f16") for _ in range(2)]
