@@ -884,12 +884,14 @@ skv_status launch_attend_c(skv_cache* c, int layer, int n, int m, const int* tok
     // so such launches wait for the previous grid to finish.
     if (gmem) pdl = false;
     // A per-layer step whose attend carries the fold + select tail (config 1:
-    // the whole step is this one launch) launches with PDL and waits at entry:
-    // it is resident while the previous step drains, hiding the launch gap.
+    // the whole step is this one launch), and the first attend of a whole
+    // step, launch with PDL and wait at entry: resident while the previous
+    // step drains (its select triggers at entry), hiding the launch gap. The
+    // chained attends behind it launch only once it has passed its wait.
     // Not with a plan: the ledger kernel of Phase I steps does not wait on
     // its predecessor, so waiting on it would not order after the attend.
     static const bool entry_pdl = std::getenv("SKV_NO_ENTRY_PDL") == nullptr;
-    if (!pdl && fused && entry_pdl && !c->has_plan && !c->prof) {
+    if (!pdl && (fused || c->in_step) && entry_pdl && !c->has_plan && !c->prof) {
         pdl = true;
         p.pdl_wait = 2;
     }
